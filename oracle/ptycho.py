@@ -1,0 +1,335 @@
+"""Float64 CPU oracle for the PtyGer ML-CG iteration (arXiv 2106.07575).
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and the
+``cpu_baseline`` / ``--impl reference`` legs of ``bench.py`` may import this
+module.  The product path (``paper_2106_07575_b200`` + ``libptyger.so``) never
+imports, calls or links it, and shares no code, table or constant with it.
+
+Citation convention: ``P:a-b`` = /root/reference/PAPER.md lines a-b,
+``S:a-b`` = SPEC.md lines a-b (used only for interface/edge-case readings),
+``R#k`` = reading k in DESIGN.md "Readings of the paper".
+
+Everything is written in the paper's order and notation (Alg. 1
+P:626-677), plain NumPy in float64.  The only library primitive used as a step
+is the unitary 2-D DFT (``numpy.fft.fft2(norm="ortho")``), itself pinned by a
+brute-force DFT test (tests/test_oracle_operators.py).
+
+Pins (what fixes each function to something other than itself) are listed in
+DESIGN.md "Oracle pins"; every public function below has at least one.
+The free-running fp32-vs-fp64 trajectory from a flat start is
+"parity unpinned" (chaotic); only teacher-forced steps and
+warm-start trajectories are compared with the GPU.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+import math
+
+import numpy as np
+
+EPS = 1e-16          # modulus guard, R#4
+DEN_EPS = 1e-30      # Dai-Yuan restart threshold, R#9
+
+# direction variants (R#6)
+DIR_DY_COMPLEX = 0   # alpha exactly as printed in Eq.6/Eq.8
+DIR_DY_REAL = 1      # Re(alpha)
+DIR_FR = 2           # Fletcher-Reeves ||g||^2/||g_prev||^2 (north_star)
+
+
+# --------------------------------------------------------------------------
+# Operators Q, F, G = F Q and G^H = Q^H F^H           (Eq.1)
+# --------------------------------------------------------------------------
+
+def extract(psi: np.ndarray, pos, N: int) -> np.ndarray:
+    """Window of psi at integer top-left corner pos=(row, col), N x N (R#3).
+
+    Q's windowing half ("element-wise multiplication of probe p and
+    exit wave psi at all scan positions").
+    """
+    r, c = int(pos[0]), int(pos[1])
+    H, W = psi.shape
+    if not (0 <= r <= H - N and 0 <= c <= W - N):
+        raise IndexError(f"window at {pos} out of bounds for {psi.shape} with N={N}")
+    return psi[r:r + N, c:c + N].copy()
+
+
+def scatter_add(acc: np.ndarray, patch: np.ndarray, pos) -> None:
+    """acc[r+i, c+k] += patch[i, k]: adjoint of ``extract`` (Q^H windowing)."""
+    r, c = int(pos[0]), int(pos[1])
+    N = patch.shape[0]
+    H, W = acc.shape
+    if not (0 <= r <= H - N and 0 <= c <= W - N):
+        raise IndexError(f"window at {pos} out of bounds for {acc.shape} with N={N}")
+    acc[r:r + N, c:c + N] += patch
+
+
+def ufft2(x: np.ndarray) -> np.ndarray:
+    """Unitary 2-D DFT, e^{-2 pi i k.n/N}, DC at [0,0], no shift (R#1, R#2).
+
+    F in Eq.1.  Scale 1/N per 2-D transform so F^H = F^{-1}.
+    Applied over the last two axes.
+    """
+    return np.fft.fft2(x, norm="ortho")
+
+
+def uifft2(x: np.ndarray) -> np.ndarray:
+    """Unitary inverse 2-D DFT = F^H ("F^H is the inverse Fourier transform")."""
+    return np.fft.ifft2(x, norm="ortho")
+
+
+def forward_G(psi: np.ndarray, probe: np.ndarray, scan: np.ndarray) -> np.ndarray:
+    """(G psi)_j = F(p * psi[window s_j]) for every frame j (Eq.1).
+
+    Returns an (n, N, N) complex128 array, frames in input order.
+    """
+    N = probe.shape[0]
+    out = np.empty((len(scan), N, N), dtype=np.complex128)
+    for j, s in enumerate(scan):
+        out[j] = ufft2(probe * extract(psi, s, N))
+    return out
+
+
+def adjoint_GH(y: np.ndarray, probe: np.ndarray, scan: np.ndarray, shape) -> np.ndarray:
+    """G^H y = sum_j scatter_{s_j}( conj(p) * F^H y_j ), ascending j."""
+    acc = np.zeros(shape, dtype=np.complex128)
+    pc = np.conj(probe)
+    for j, s in enumerate(scan):
+        scatter_add(acc, pc * uifft2(y[j]), s)
+    return acc
+
+
+def illumination(probe: np.ndarray, scan: np.ndarray, shape) -> np.ndarray:
+    """I(rho) = sum_j |p(rho - s_j)|^2, the diagonal of G^H G (closed form, used as a pin)."""
+    acc = np.zeros(shape, dtype=np.float64)
+    a2 = np.abs(probe) ** 2
+    N = probe.shape[0]
+    for s in scan:
+        r, c = int(s[0]), int(s[1])
+        acc[r:r + N, c:c + N] += a2
+    return acc
+
+
+# --------------------------------------------------------------------------
+# Objective (Eq.2) and gradient (Eq.3)
+# --------------------------------------------------------------------------
+
+def objective_F(far: np.ndarray, d: np.ndarray, eps: float = EPS) -> float:
+    """F = sum_{frames, pixels} ( |G psi|^2 - 2 d log|G psi| )   (Eq.2).
+
+    j runs over all detector pixels of all frames (R#13).
+    log|u| is guarded as log max(|u|, eps) (R#4).
+    """
+    a = np.abs(far)
+    return float(np.sum(a * a - 2.0 * d * np.log(np.maximum(a, eps))))
+
+
+def residual(far: np.ndarray, d: np.ndarray, eps: float = EPS) -> np.ndarray:
+    """Gpsi - d/(Gpsi)^*  (the bracket of Eq.3), written as u - d u/|u|^2.
+
+    Where |u| < eps the quotient term is dropped, r = u (R#4).
+    """
+    a2 = np.abs(far) ** 2
+    ok = np.sqrt(a2) >= eps
+    q = np.zeros_like(far)
+    q[ok] = d[ok] * far[ok] / a2[ok]
+    return far - q
+
+
+def gradient(psi, probe, scan, d, eps: float = EPS):
+    """Wirtinger gradient dF/dpsi* = G^H( G psi - d/(G psi)^* )   (Eq.3, R#5).
+
+    Returns (grad, far) where far = G psi.
+    """
+    far = forward_G(psi, probe, scan)
+    return adjoint_GH(residual(far, d, eps), probe, scan, psi.shape), far
+
+
+# --------------------------------------------------------------------------
+# Solver pieces: Dai-Yuan direction (Eq.6, Eq.8), line search (Eq.7), update (Eq.5)
+# --------------------------------------------------------------------------
+
+def inner(a: np.ndarray, b: np.ndarray) -> complex:
+    """<a, b> = sum_i a_i^* b_i over the z object pixels."""
+    return complex(np.sum(np.conj(a) * b))
+
+
+def dai_yuan(g, g_prev, eta_prev, variant: int = DIR_DY_COMPLEX):
+    """Search direction eta_m (Eq.6; coefficient alpha_m Eq.8).
+
+    m = 0 (g_prev is None): eta_0 = -g.
+    Otherwise alpha = ||g||^2 / <eta_prev, g - g_prev>  (complex as printed, R#6),
+    eta = -g + alpha eta_prev.  |den| < 1e-30 or non-finite alpha => restart
+    eta = -g (R#9).  Returns (eta, alpha, restarted).
+    """
+    if g_prev is None or eta_prev is None:
+        return -g, 0j, False
+    gg = float(np.sum(np.abs(g) ** 2))
+    if variant == DIR_FR:
+        den = complex(float(np.sum(np.abs(g_prev) ** 2)))
+    else:
+        den = inner(eta_prev, g - g_prev)
+    if abs(den) < DEN_EPS:
+        return -g, 0j, True
+    alpha = gg / den
+    if variant == DIR_DY_REAL or variant == DIR_FR:
+        alpha = complex(alpha.real, 0.0)
+    if not (math.isfinite(alpha.real) and math.isfinite(alpha.imag)):
+        return -g, 0j, True
+    return -g + alpha * eta_prev, alpha, False
+
+
+@dataclass
+class LSConfig:
+    gamma0: float = 1.0     # gamma^(0) = 1   (Alg.1)
+    tau: float = 0.5        # tau = 0.5       (Alg.1)
+    t: float = 0.0          # t "usually set to 0"
+    max_shrinks: int = 32   # bound on trials, R#9
+
+
+def line_search(eval_f, f0: float, cfg: LSConfig):
+    """Backtracking line search of Eq.7, Eq.7 semantics (R#7).
+
+    Trials gamma_k = gamma0 * tau^k, k = 0..max_shrinks-1 (first trial is gamma0
+    itself); accept the first with F(psi + gamma eta) <= F(psi) + gamma t.
+    None accepted: gamma = 0, F unchanged, stalled (R#9).
+    Returns (gamma, k, f_new, stalled, trials) with trials = [(gamma_k, f_k)].
+    """
+    trials = []
+    gamma = cfg.gamma0
+    for k in range(cfg.max_shrinks):
+        fk = float(eval_f(gamma))
+        trials.append((gamma, fk))
+        if fk <= f0 + gamma * cfg.t:
+            return gamma, k, fk, False, trials
+        gamma = gamma * cfg.tau
+    return 0.0, cfg.max_shrinks, f0, True, trials
+
+
+def ls_delta(u, v, d, gamma: float, eps: float = EPS) -> float:
+    """Difference form of the LS objective:  F(psi + gamma eta) - F(psi).
+
+    With u = G psi, v = G eta (G linear, Eq.1) and per pixel a = 2 Re(u^* v),
+    b = |v|^2, c = |u|^2:  |u + gamma v|^2 = c + gamma a + gamma^2 b, so
+      dF = sum( gamma a + gamma^2 b - d log(1 + (gamma a + gamma^2 b)/c) ).
+    Pixels where |u| < eps or |u + gamma v| < eps use the clamped definition
+    (log max(., eps)) exactly as objective_F does (R#4).  This is the quantity
+    the GPU line search evaluates; pinned against
+    objective_F(u + gamma v) - objective_F(u) in tests.
+    """
+    a = 2.0 * np.real(np.conj(u) * v)
+    b = np.abs(v) ** 2
+    c = np.abs(u) ** 2
+    q = gamma * a + gamma * gamma * b
+    cn = c + q
+    e2 = eps * eps
+    ok = (c >= e2) & (cn >= e2)
+    out = np.where(ok, q, 0.0)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        lg = np.where(ok, np.log1p(np.where(ok, q / np.where(ok, c, 1.0), 0.0)), 0.0)
+    out = out - d * lg
+    bad = ~ok
+    if np.any(bad):
+        out_b = (cn[bad] - c[bad]) - d[bad] * (np.log(np.maximum(cn[bad], e2))
+                                                 - np.log(np.maximum(c[bad], e2)))
+        out = out.copy()
+        out[bad] = out_b
+    return float(np.sum(out))
+
+
+# --------------------------------------------------------------------------
+# One CG iteration (Fig.3 four stages GRAD -> DIR -> LS -> Update, P:462-471,
+# Alg.1) and the driver.
+# --------------------------------------------------------------------------
+
+@dataclass
+class CGState:
+    psi: np.ndarray                 # psi_m (H x W complex128)
+    g_prev: np.ndarray | None = None   # grad F(psi_{m-1})
+    eta_prev: np.ndarray | None = None  # eta_{m-1}
+    F: float | None = None          # cached F(psi_m) (R#11)
+    m: int = 0
+
+
+@dataclass
+class Trace:
+    iter: int
+    F: float            # F(psi_{m+1}) (accepted trial value)
+    gamma: float
+    shrinks: int
+    alpha: complex
+    restarted: bool
+    stalled: bool
+    step_norm: float    # ||psi_{m+1} - psi_m||_2
+    grad_norm: float
+    trials: list = field(default_factory=list)
+
+
+def cg_iterate(state: CGState, probe, scan, d, ls: LSConfig = LSConfig(),
+               variant: int = DIR_DY_COMPLEX, eps: float = EPS):
+    """One iteration of Alg.1 with Eq.7 LS semantics (R#7).
+
+    GRAD: g = grad F(psi_m) (Eq.3).
+    DIR: eta = Dai-Yuan(g, g_prev, eta_prev) (Eq.6).
+    LS: gamma from line_search, F evaluated BY DEFINITION on
+                      G(psi + gamma eta) for every trial.
+    UPD:     psi_{m+1} = psi_m + gamma eta (Eq.5); F cached (R#11).
+    Returns (new_state, trace, g, eta).
+    """
+    psi = state.psi
+    g, far = gradient(psi, probe, scan, d, eps)
+    f0 = state.F if state.F is not None else objective_F(far, d, eps)
+    eta, alpha, restarted = dai_yuan(g, state.g_prev if state.m > 0 else None,
+                                     state.eta_prev if state.m > 0 else None, variant)
+
+    def eval_f(gamma):
+        return objective_F(forward_G(psi + gamma * eta, probe, scan), d, eps)
+
+    gamma, k, f_new, stalled, trials = line_search(eval_f, f0, ls)
+    psi_new = psi + gamma * eta
+    tr = Trace(iter=state.m, F=f_new, gamma=gamma, shrinks=k, alpha=alpha,
+               restarted=restarted, stalled=stalled,
+               step_norm=float(np.sqrt(np.sum(np.abs(psi_new - psi) ** 2))),
+               grad_norm=float(np.sqrt(np.sum(np.abs(g) ** 2))), trials=trials)
+    return CGState(psi=psi_new, g_prev=g, eta_prev=eta, F=f_new, m=state.m + 1), tr, g, eta
+
+
+def run_cg(psi0, probe, scan, d, iters: int, ls: LSConfig = LSConfig(),
+           variant: int = DIR_DY_COMPLEX, eps: float = EPS):
+    """Alg.1 end to end on one worker: iters CG iterations from psi0 (R#10)."""
+    st = CGState(psi=np.asarray(psi0, dtype=np.complex128).copy())
+    traces = []
+    for _ in range(iters):
+        st, tr, _, _ = cg_iterate(st, probe, scan, d, ls, variant, eps)
+        traces.append(tr)
+    return st, traces
+
+
+def gd_iterate(psi, probe, scan, d, gamma: float, eps: float = EPS):
+    """Gradient-descent update psi - gamma grad F (Eq.4)."""
+    g, _ = gradient(psi, probe, scan, d, eps)
+    return psi - gamma * g
+
+
+# --------------------------------------------------------------------------
+# Teacher-forcing helpers: what one GPU iteration must produce from a given state
+# --------------------------------------------------------------------------
+
+def grad_at(psi, g_prev, eta_prev, m, probe, scan, d, variant=DIR_DY_COMPLEX, eps=EPS):
+    """From state (psi_m, g_{m-1}, eta_{m-1}, m): g_m, alpha_m, eta_m, restarted, u=G psi_m."""
+    g, far = gradient(psi, probe, scan, d, eps)
+    eta, alpha, restarted = dai_yuan(g, g_prev if m > 0 else None,
+                                     eta_prev if m > 0 else None, variant)
+    return g, alpha, eta, restarted, far
+
+
+def ls_at(psi, eta, probe, scan, d, gammas, eps=EPS):
+    """Definition-based F(psi + gamma eta) - F(psi) for each gamma in gammas."""
+    f0 = objective_F(forward_G(psi, probe, scan), d, eps)
+    return [objective_F(forward_G(psi + g * eta, probe, scan), d, eps) - f0 for g in gammas]
+
+
+def round_positions(raw) -> np.ndarray:
+    """Float scan positions (Alg.1 input 'float32 h_s') -> integer top-left
+    corners, round half-up computed in double: floor(x + 0.5) (R#3)."""
+    raw = np.asarray(raw, dtype=np.float32).astype(np.float64)
+    return np.floor(raw + 0.5).astype(np.int64)

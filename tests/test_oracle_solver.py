@@ -1,0 +1,215 @@
+"""Pins for the oracle's objective, gradient, DY direction, line search and CG
+(Alg.1)."""
+import numpy as np
+import pytest
+
+from oracle import ptycho as O
+from paper_2106_07575_b200 import inputs as I
+
+
+def tiny_problem(noisy=False, seed_obj=None):
+    w = I.WORKLOADS["tiny"]
+    psi_true, p, scan = I.workload_inputs(w)
+    mean = w.photons * np.abs(O.forward_G(psi_true, p, scan)) ** 2
+    d = I.poisson_counts(mean, w.seed) if noisy else mean.astype(np.float32)
+    return psi_true, p, scan, d.astype(np.float64)
+
+
+# ---------------------------------------------------------------- objective (Eq.2)
+
+def test_F_closed_forms():
+    far = np.ones((1, 4, 4), complex)
+    assert O.objective_F(far, np.ones((1, 4, 4))) == 16.0
+    assert O.objective_F(far, np.zeros((1, 4, 4))) == 16.0
+    # phase of u does not matter, only |u|: F(e^{i phi} u) = F(u)
+    rng = np.random.default_rng(0)
+    u = I.random_complex((2, 8, 8), seed=5)
+    d = rng.uniform(0, 3, size=u.shape)
+    assert abs(O.objective_F(u * np.exp(0.7j), d) - O.objective_F(u, d)) < 1e-12 * abs(O.objective_F(u, d))
+
+
+def test_F_lower_bound_and_equality():
+    """x - d log x >= d - d log d (x = |u|^2 > 0), equality iff x = d."""
+    rng = np.random.default_rng(1)
+    d = rng.uniform(0.1, 5, size=(3, 8, 8))
+    fmin = float(np.sum(d - d * np.log(d)))
+    u_eq = np.sqrt(d) * np.exp(1j * rng.uniform(0, 6, size=d.shape))
+    assert abs(O.objective_F(u_eq, d) - fmin) < 1e-12 * abs(fmin)
+    for s in range(5):
+        u = I.random_complex(d.shape, seed=10 + s)
+        assert O.objective_F(u, d) > fmin
+
+
+# ---------------------------------------------------------------- gradient (Eq.3)
+
+def test_gradient_finite_difference():
+    """(F(psi + e delta) - F(psi - e delta)) / 2e = 2 Re <grad F, delta> (Wirtinger, R#5)."""
+    rng = np.random.default_rng(17)
+    H, N, n = 32, 8, 9
+    scan = rng.integers(0, H - N + 1, size=(n, 2))
+    p = I.make_probe(N)
+    psi = I.random_complex((H, H), seed=17, scale=0.5) + 1.0
+    d = rng.uniform(0, 4, size=(n, N, N))
+    g, _ = O.gradient(psi, p, scan, d)
+    F = lambda x: O.objective_F(O.forward_G(x, p, scan), d)
+    e = 1e-6
+    for k in range(6):
+        delta = I.random_complex((H, H), seed=100 + k)
+        if k % 2:
+            delta = 1j * delta
+        fd = (F(psi + e * delta) - F(psi - e * delta)) / (2 * e)
+        an = 2 * np.real(np.vdot(g, delta))
+        assert abs(fd - an) <= 1e-6 * abs(an)
+
+
+def test_gradient_stationary_at_noiseless_truth():
+    psi_true, p, scan, d = tiny_problem()
+    d = O.forward_G(psi_true, p, scan)
+    d = np.abs(d) ** 2  # float64 noiseless data
+    g, _ = O.gradient(psi_true, p, scan, d)
+    assert np.linalg.norm(g) <= 1e-12 * np.linalg.norm(psi_true)
+
+
+def test_gradient_d_zero_closed_form():
+    """d = 0 => grad F = G^H G psi = I * psi (closed form)."""
+    psi_true, p, scan, d = tiny_problem()
+    x = I.random_complex(psi_true.shape, seed=4)
+    g, _ = O.gradient(x, p, scan, np.zeros_like(d))
+    Ill = O.illumination(p, scan, x.shape)
+    assert np.max(np.abs(g - Ill * x)) < 1e-12 * np.max(np.abs(Ill * x))
+
+
+def test_residual_guard():
+    u = np.array([0.0 + 0j, 1e-17 + 0j, 2.0 + 0j])
+    d = np.array([3.0, 3.0, 4.0])
+    r = O.residual(u, d)
+    assert r[0] == 0 and r[1] == u[1]            # |u| < eps: quotient dropped (R#4)
+    assert abs(r[2] - (2 - 4 / 2)) < 1e-15       # u - d/u* = 2 - 4/2
+
+
+# ---------------------------------------------------------------- DY direction (Eq.6/8)
+
+def test_dai_yuan_m0_and_restart():
+    g = I.random_complex((4, 4), seed=1)
+    eta, alpha, rs = O.dai_yuan(g, None, None)
+    assert np.array_equal(eta, -g) and not rs
+    eta, alpha, rs = O.dai_yuan(g, g.copy(), I.random_complex((4, 4), seed=2))
+    assert rs and np.array_equal(eta, -g)                                 # zero denominator
+
+
+@pytest.mark.parametrize("variant", [O.DIR_DY_COMPLEX, O.DIR_DY_REAL, O.DIR_FR])
+def test_cg_terminates_on_quadratic(variant):
+    """Nonlinear-CG textbook property: on f = x^H A x - 2 Re(b^H x) (A Hermitian PD) with
+    exact line search, DY / FR directions are A-conjugate and CG converges in n steps.
+    A dropped term, a conj on the wrong side or a sign error in alpha breaks this."""
+    n = 6
+    rng = np.random.default_rng(3)
+    M = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    A = M.conj().T @ M + 0.5 * np.eye(n)
+    b = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    x = np.zeros(n, complex)
+    g_prev = eta_prev = None
+    for m in range(n):
+        g = A @ x - b                                  # Wirtinger gradient
+        eta, alpha, rs = O.dai_yuan(g, g_prev, eta_prev, variant)
+        gamma = -np.real(np.vdot(eta, g)) / np.real(np.vdot(eta, A @ eta))   # exact LS
+        x = x + gamma * eta
+        g_prev, eta_prev = g, eta
+    assert np.linalg.norm(A @ x - b) < 1e-9 * np.linalg.norm(b)
+
+
+# ---------------------------------------------------------------- line search (Eq.7)
+
+def test_line_search_sequences():
+    cfg = O.LSConfig()
+    g, k, f, st, _ = O.line_search(lambda gm: 10.0 - 1.0, 10.0, cfg)
+    assert (g, k, st) == (1.0, 0, False) and f == 9.0
+    g, k, f, st, tr = O.line_search(lambda gm: 11.0, 10.0, O.LSConfig(max_shrinks=4))
+    assert g == 0.0 and st and len(tr) == 4 and f == 10.0
+    g, k, f, st, _ = O.line_search(lambda gm: 10.0 + (gm - 0.2), 10.0, cfg)
+    assert g == 0.125 and k == 3 and not st
+
+
+def test_ls_delta_equals_definition():
+    """Difference form (linearity of G) == F(u + g v) - F(u) by definition."""
+    psi_true, p, scan, d = tiny_problem(noisy=True)
+    psi = np.ones_like(psi_true)
+    eta = I.random_complex(psi.shape, seed=8, scale=0.1)
+    u = O.forward_G(psi, p, scan)
+    v = O.forward_G(eta, p, scan)
+    for gm in [1.0, 0.5, 0.03125, 2.0 ** -12]:
+        ref = O.objective_F(u + gm * v, d) - O.objective_F(u, d)
+        terms = np.sum(np.abs(u + gm * v) ** 2) + np.sum(np.abs(u) ** 2) + 2 * np.sum(d * np.abs(np.log(np.abs(u) + 1e-300)))
+        assert abs(O.ls_delta(u, v, d, gm) - ref) <= 1e-10 * terms
+
+
+def test_ls_delta_guarded_pixels():
+    u = np.array([0.0 + 0j, 1.0 + 0j, 1e-20 + 0j])
+    v = np.array([1.0 + 0j, -1.0 + 0j, 0.0 + 0j])
+    d = np.array([2.0, 1.0, 1.0])
+    for gm in [1.0, 0.5]:
+        ref = O.objective_F(u + gm * v, d) - O.objective_F(u, d)
+        assert abs(O.ls_delta(u, v, d, gm) - ref) < 1e-9 * (1 + abs(ref))
+
+
+def test_ls_analytic_d_zero():
+    """d = 0, m = 0: eta = -I psi, DeltaF(g) = sum I^2 |psi|^2 g (g I - 2);
+    the first accepted trial is computable by hand and must equal the oracle's."""
+    psi_true, p, scan, d = tiny_problem()
+    d0 = np.zeros_like(d)
+    Ill = O.illumination(p, scan, psi_true.shape)
+    psi = psi_true
+    dF = lambda gm: float(np.sum(Ill ** 2 * np.abs(psi) ** 2 * gm * (gm * Ill - 2)))
+    k_hand = next(k for k in range(32) if dF(0.5 ** k) <= 0)
+    st, tr, g, eta = O.cg_iterate(O.CGState(psi=psi), p, scan, d0)
+    assert tr.shrinks == k_hand and tr.gamma == 0.5 ** k_hand
+    f0 = float(np.sum(Ill * np.abs(psi) ** 2))
+    assert abs(tr.F - (f0 + dF(tr.gamma))) < 1e-9 * f0
+
+
+# ---------------------------------------------------------------- CG (Eq.5, Alg.1)
+
+def test_cg_monotone_and_restart_after_stall():
+    psi_true, p, scan, d = tiny_problem(noisy=True)
+    st, trs = O.run_cg(np.ones_like(psi_true), p, scan, d, 8)
+    F = [t.F for t in trs]
+    assert all(F[i + 1] <= F[i] for i in range(len(F) - 1))
+    assert all(1 <= t.shrinks + 1 <= 32 for t in trs)
+
+
+def test_cg_fixed_point_at_truth():
+    psi_true, p, scan, _ = tiny_problem()
+    d = np.abs(O.forward_G(psi_true, p, scan)) ** 2
+    st, tr, g, eta = O.cg_iterate(O.CGState(psi=psi_true.copy()), p, scan, d)
+    assert tr.gamma == 1.0 and tr.step_norm <= 1e-10 * np.linalg.norm(psi_true)
+
+
+def test_cg_recovers_noiseless_object():
+    """Noiseless tiny fixture from psi0 = 1: F - F_min falls by orders of magnitude and the
+    scanned interior matches psi_true up to a global phase."""
+    psi_true, p, scan, _ = tiny_problem()
+    d = np.abs(O.forward_G(psi_true, p, scan)) ** 2
+    dpos = d[d > 0]
+    fmin = float(np.sum(dpos - dpos * np.log(dpos)))
+    st, trs = O.run_cg(np.ones_like(psi_true), p, scan, d, 150)
+    gap0 = trs[0].F - fmin
+    gapN = trs[-1].F - fmin
+    assert gapN < 2e-2 * gap0   # measured 1844 -> 17 after 150 iterations
+    crop = (slice(16, 48), slice(16, 48))
+    a, b = st.psi[crop], psi_true[crop]
+    th = np.angle(np.vdot(b, a))
+    err = np.linalg.norm(a * np.exp(-1j * th) - b) / np.linalg.norm(b)
+    assert err < 0.15            # measured 0.72 after 1 iteration, 0.11 after 150
+
+
+def test_gd_update_trivial_cases():
+    """Eq.4: gamma = 0 or grad F = 0 leave psi unchanged; otherwise
+    psi - gamma grad F decreases F for a small enough gamma (descent direction)."""
+    psi_true, p, scan, _ = tiny_problem()
+    d = np.abs(O.forward_G(psi_true, p, scan)) ** 2
+    assert np.array_equal(O.gd_iterate(psi_true, p, scan, d, 0.0), psi_true)
+    x = O.gd_iterate(psi_true, p, scan, d, 0.25)
+    assert np.max(np.abs(x - psi_true)) < 1e-12
+    y = np.ones_like(psi_true)
+    F = lambda z: O.objective_F(O.forward_G(z, p, scan), d)
+    assert F(O.gd_iterate(y, p, scan, d, 1.0 / 64)) < F(y)
