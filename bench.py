@@ -1,0 +1,358 @@
+#!/usr/bin/env python
+"""Benchmark: diffraction frames/sec per CG iteration (BASELINE.json metric) through libptyger.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config paper] [--impl ours|reference]
+
+One "step" = one CG iteration of the whole hot path (GRAD -> DIR -> LS -> Update, all SURVEY
+8(a) rows) over every frame of the workload.  Default workload: the paper-scale view
+(4096^2 object, 128^2 detector, 158^2 = 24 964 frames), the config BASELINE.json quotes the
+metric on at 1/2/4/8 B200; it fits one GPU.  Synthetic data (DESIGN.md input recipe): Siemens
+star, Gaussian chirped probe, jittered raster, d = Poisson(1e3 |G psi_true|^2) generated on the
+device with torch.fft (data synthesis only; the timed path is libptyger's kernels).
+
+Multi-GPU (torchrun, one rank per GPU): the frames are partitioned into row stripes by the
+library (strong scaling: the total workload is fixed), with an NCCL band exchange + scalar
+allreduces per iteration.  Timing: CUDA events on the library's stream around the graph
+launches, barrier + synchronize on both sides, max over ranks.  u, v, d (8.2 GB at
+paper-scale) exceed the 126 MB L2, so no explicit flush is needed between iterations.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2106_07575_b200 import inputs as I  # noqa: E402
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+METRIC = "diffraction frames/sec per CG iteration"
+UNIT = "frames/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="paper", choices=["tiny", "small", "paper", "mid"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ls-batch", type=int, default=16)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(PEAKS_PATH) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ----------------------------------------------------------------------------- data
+
+def synth_device(w: I.Workload, device):
+    """psi_true, probe, scan on the host (inputs module); d on the device via torch.fft."""
+    import torch
+    psi_true, p, scan = I.workload_inputs(w)
+    pt = torch.from_numpy(p.astype(np.complex64)).to(device)
+    ot = torch.from_numpy(psi_true.astype(np.complex64)).to(device)
+    N = w.N
+    d = torch.empty((len(scan), N, N), dtype=torch.float32, device=device)
+    g = torch.Generator(device=device)
+    g.manual_seed(w.seed)
+    rr = torch.arange(N, device=device)
+    chunk = 1024
+    sc = torch.from_numpy(scan.astype(np.int64)).to(device)
+    for a in range(0, len(scan), chunk):
+        b = min(len(scan), a + chunk)
+        r = sc[a:b, 0][:, None, None] + rr[None, :, None]
+        c = sc[a:b, 1][:, None, None] + rr[None, None, :]
+        patch = ot[r, c] * pt[None]
+        far = torch.fft.fft2(patch, norm="ortho")
+        mean = w.photons * (far.real ** 2 + far.imag ** 2)
+        d[a:b] = torch.poisson(mean, generator=g)
+    return psi_true, p, scan, d
+
+
+# ----------------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+
+        def rd():
+            for line in self.proc.stdout:
+                self.samples.append([x.strip() for x in line.split(",")])
+        self.thread = threading.Thread(target=rd, daemon=True)
+        self.thread.start()
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(2)
+        except Exception:
+            self.proc.kill()
+        sm = [float(s[0]) for s in self.samples if len(s) >= 7 and s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if len(s) >= 7 and s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            if len(s) < 7:
+                continue
+            for i, nm in enumerate(names):
+                if s[3 + i].lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- CPU oracle
+
+def oracle_sample_run(w: I.Workload, budget_s: float, psi_true, p, scan, d_host_fn):
+    """Oracle (float64 NumPy, single-threaded pocketfft) on a bounded sample of the workload:
+    the first n_s frames in raster order with the object cropped to their rows; one CG iteration
+    (definition-based LS).  Returns (frames/s, sample description, shrinks)."""
+    from oracle import ptycho as O
+    N = w.N
+    n_s = 8
+    t_one = None
+    while True:
+        sc = scan[:n_s].copy()
+        r0 = int(sc[:, 0].min())
+        r1 = int(sc[:, 0].max()) + N
+        sub = sc.copy()
+        sub[:, 0] -= r0
+        d = d_host_fn(n_s).astype(np.float64)
+        psi0 = np.ones((r1 - r0, w.W), np.complex128)
+        t0 = time.perf_counter()
+        st, tr, _, _ = O.cg_iterate(O.CGState(psi=psi0), p.astype(np.complex128), sub, d)
+        t_one = time.perf_counter() - t0
+        if t_one >= budget_s / 3 or n_s >= len(scan):
+            break
+        n_s = min(len(scan), int(n_s * max(2.0, min(8.0, (budget_s / 3) / max(t_one, 1e-3)))))
+    desc = (f"oracle float64 NumPy (pocketfft, 1 thread): 1 CG iteration with definition-based line "
+            f"search on the first {n_s} of {len(scan)} frames (rows {r0}..{r1} of the {w.name} workload), "
+            f"{tr.shrinks} shrinks; frames/s = {n_s} / {t_one:.2f} s")
+    return n_s / t_one, desc, tr.shrinks, t_one
+
+
+# ----------------------------------------------------------------------------- main
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    w = I.WORKLOADS[args.config]
+
+    if args.impl == "reference":
+        return reference_arm(args, w, world, rank)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2106_07575_b200 import _lib as L
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        try:
+            import nvidia  # type: ignore
+            for pth in nvidia.__path__:
+                cand = os.path.join(pth, "nccl", "lib", "libnccl.so.2")
+                if os.path.exists(cand):
+                    os.environ.setdefault("PTYGER_NCCL_LIB", cand)
+        except Exception:
+            pass
+    psi_true, p, scan, d = synth_device(w, dev)
+    n = len(scan)
+    cfg = L.default_config(ls_batch=args.ls_batch, device=local, rank=rank, world=world)
+    idbuf = None
+    if world > 1:
+        obj = [L.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        import ctypes
+        idbuf = ctypes.create_string_buffer(obj[0], 128)
+        cfg.nccl_id = ctypes.cast(idbuf, ctypes.c_void_p)
+    psi0 = torch.ones((w.H, w.W), dtype=torch.complex64, device=dev)
+    pdev = torch.from_numpy(p.astype(np.complex64)).to(dev)
+    pt = L.Ptyger(psi0, pdev, scan, d, config=cfg)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # warm-up (real iterations)
+    pt.iterate(args.warmup, traces=False)
+    barrier()
+    clk = ClockSampler(local)
+    clk.start()
+    t_host0 = time.perf_counter()
+    trs = pt.iterate(args.steps)
+    ms = pt.last_iterate_ms()
+    t_host = time.perf_counter() - t_host0
+    barrier()
+    clocks = clk.stop()
+    if world > 1:
+        tt = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    launches = pt.kernel_launches()
+    shrinks = [t["shrinks"] for t in trs]
+    value = n * args.steps / (ms / 1e3)
+
+    # stage times (eager, CUDA events between kernels; real iterations after the timed region)
+    st_iters = 3
+    stage = pt.stage_times(st_iters) / st_iters
+    N = w.N
+    n_local_bytes_grad = 36.0 * n * N * N / world      # u r/w 16, v r 8, d r 4, y w 8
+    n_local_bytes_ls = 20.0 * n * N * N / world + 8.0 * w.H * w.W / world  # v w, u r, d r + eta once
+    pk, pk_kind = peaks()
+    cand = {"k_grad": (stage[1], n_local_bytes_grad), "k_ls": (stage[4], n_local_bytes_ls)}
+    dom = max(cand, key=lambda k: cand[k][0])
+    dur_ms, algo_bytes = cand[dom]
+    achieved = algo_bytes / (dur_ms / 1e3) / 1e9
+    traffic = None
+    prof_json = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof_json):
+        try:
+            with open(prof_json) as f:
+                tj = json.load(f)
+            traffic = tj.get(args.config, {}).get(dom)
+        except Exception:
+            traffic = None
+
+    # end-to-end through the public API from pinned HOST buffers (H2D + 1 iteration + D2H)
+    e2e = None
+    if args.e2e_steps > 0 and world == 1:
+        d_host = d.cpu().pin_memory()
+        psi_h = torch.ones((w.H, w.W), dtype=torch.complex64).pin_memory()
+        p_h = torch.from_numpy(p.astype(np.complex64)).pin_memory()
+        del pt
+        torch.cuda.synchronize()
+        t_list = []
+        for _ in range(args.e2e_steps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            q = L.Ptyger(psi_h, p_h, scan, d_host, config=L.default_config(ls_batch=args.ls_batch, device=local))
+            q.iterate(1, traces=False)
+            out = q.get_object()
+            t_list.append(time.perf_counter() - t0)
+            q.close()
+        tm = float(np.median(t_list))
+        e2e = {"value": n / tm, "unit": UNIT, "h2d_bytes_per_step": int(d_host.numel() * 4 + psi_h.numel() * 8
+                                                                          + p_h.numel() * 8 + scan.size * 4),
+               "d2h_bytes_per_step": int(out.nbytes), "steps": args.e2e_steps,
+               "note": "ptyger_init from pinned host buffers (H2D of d, psi0, probe, scan; u0 = G psi0, F0) + 1 CG "
+                       "iteration + ptyger_get_object (D2H), wall clock per step"}
+    else:
+        pt.close()
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        dh = d.cpu().numpy()
+        v, desc, shr, t_one = oracle_sample_run(w, args.cpu_seconds, psi_true, p, scan, lambda k: dh[:k])
+        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc}
+
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms / args.steps,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": f"{w.name}: {w.H}x{w.W} object, {w.N}^2 probe/detector, {n} frames "
+                               f"({w.k}^2 raster, step {w.step}, jitter {w.jitter}), photons {w.photons:g}, Poisson",
+                   "H": w.H, "W": w.W, "N": w.N, "frames": n, "ls_batch": args.ls_batch,
+                   "parallelism": f"stripes{world}",
+                   "l2": "inputs larger than L2 (u, v, d resident in HBM: %.1f GB)" % (n * N * N * 20 / 1e9)},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": pk, "peak_kind": pk_kind,
+                     "unit": "GB/s", "frac": achieved / pk, "traffic": traffic,
+                     "algorithmic_bytes_per_launch": algo_bytes, "avg_launch_ms": dur_ms},
+        "stage_ms": {"begin": stage[0], "k_grad": stage[1], "k_adj": stage[2], "dir_eta": stage[3],
+                     "k_ls": stage[4], "ls_rest_upd": stage[5], "iteration_eager": stage[6]},
+        "mean_shrinks": float(np.mean(shrinks)),
+        "clocks": clocks,
+        "gpu_launches": int(launches),
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+        "host_wall_s": t_host,
+    }
+    print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def reference_arm(args, w, world, rank):
+    """--impl reference: the float64 oracle (the only reference this paper-tier run has) timed on
+    the host cores on bounded samples of the same workload; rank 0 only."""
+    if rank != 0:
+        return
+    psi_true, p, scan = I.workload_inputs(w)
+    from oracle import ptycho as O
+
+    def d_fn(k):
+        mean = w.photons * np.abs(O.forward_G(psi_true, p, scan[:k])) ** 2
+        return I.poisson_counts(mean, w.seed)
+    per = max(2.0, 120.0 / max(1, args.steps + args.warmup))
+    vals = []
+    desc = None
+    for i in range(args.warmup + args.steps):
+        v, desc, shr, t_one = oracle_sample_run(w, per, psi_true, p, scan, d_fn)
+        if i >= args.warmup:
+            vals.append(v)
+    v = float(np.median(vals))
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": w.name, "H": w.H, "W": w.W, "N": w.N, "frames": w.n},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,197 @@
+/*
+ * libptyger — C ABI of the B200-native PtyGer ML-CG iteration (arXiv 2106.07575).
+ *
+ * The library computes, entirely on the GPU, the conjugate-gradient iteration of the
+ * Poisson maximum-likelihood ptychographic reconstruction of the complex object psi:
+ *
+ *   forward model      |G psi|^2 = |F Q psi|^2 = d                  (Eq.1)
+ *   objective          F(psi) = sum_j |G psi|_j^2 - 2 d_j log|G psi|_j   (Eq.2)
+ *   gradient           grad F = G^H (G psi - d / (G psi)^*)             (Eq.3)
+ *   direction          eta_m = -grad F_m + alpha_m eta_{m-1},
+ *                      alpha_m = ||grad F_m||^2 / <eta_{m-1}, grad F_m - grad F_{m-1}>
+ *                                                                    (Eq.6, 533-538 Eq.8)
+ *   line search        first gamma = gamma0 tau^k with F(psi+gamma eta) <= F(psi) + gamma t
+ *                                                                    (Eq.7, Alg.1 659-668)
+ *   update             psi_{m+1} = psi_m + gamma_m eta_m                (Eq.5)
+ *
+ * Conventions (R#k):
+ *   - F is the UNITARY 2-D DFT, e^{-2 pi i k.n/N}, DC at [0,0], no fftshift (R#1, R#2).
+ *   - Scan positions are integer TOP-LEFT window corners (row, col) (R#3).
+ *   - log|u| and d/u^* are guarded with eps (config.eps, default 1e-16) (R#4).
+ *   - the gradient is the Wirtinger derivative dF/dpsi^* (R#5).
+ *   - complex numbers are interleaved (re, im) float32 pairs ("complex64", Alg.1);
+ *     images are row-major; all scalar accumulation is float64 (R#16).
+ *
+ * Threading / ownership: one context per host thread, not re-entrant.  Input arrays are
+ * COPIED during ptyger_init (host or device pointers, detected with
+ * cudaPointerGetAttributes); the caller keeps ownership.  Outputs go to caller-allocated
+ * HOST buffers unless stated otherwise.  The context owns all device memory, streams,
+ * CUDA graphs and the NCCL communicator; ptyger_destroy frees them.
+ *
+ * Errors: every call returns a ptyger_status; ptyger_last_error(ctx) (or
+ * ptyger_last_error(NULL) after a failed ptyger_init / host helper) gives a message
+ * naming the stage, frame index and iteration where applicable.  There is no CPU
+ * fallback: without a CUDA device every device call returns PTYGER_E_CUDA.
+ */
+#ifndef PTYGER_H
+#define PTYGER_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ptyger_ctx ptyger_ctx;
+
+typedef enum {
+    PTYGER_OK = 0,
+    PTYGER_E_ARG = 2,      /* bad configuration / argument / infeasible partition  */
+    PTYGER_E_DATA = 3,     /* out-of-bounds window, negative or non-finite d, shape */
+    PTYGER_E_NUMERIC = 4,  /* non-finite F, alpha or gamma; last good iterate kept  */
+    PTYGER_E_CUDA = 5,     /* CUDA runtime / driver failure or no device            */
+    PTYGER_E_NCCL = 6,     /* NCCL failure (world > 1)                              */
+    PTYGER_E_OOM = 7,      /* device allocation failed                              */
+    PTYGER_E_STATE = 8     /* call not valid in the current context state           */
+} ptyger_status;
+
+/* Direction variants (R#6). */
+enum { PTYGER_DIR_DY = 0,      /* complex alpha exactly as printed (Eq.6 / Eq.8)   */
+       PTYGER_DIR_DY_REAL = 1, /* Re(alpha)                                        */
+       PTYGER_DIR_FR = 2 };    /* Fletcher-Reeves ||g||^2 / ||g_prev||^2            */
+
+typedef struct {
+    double gamma0;        /* first LS trial, 1.0 (Alg.1)                            */
+    double tau;           /* shrink factor, 0.5 (Alg.1)                             */
+    double t;             /* Armijo-like constant, 0.0                            */
+    double eps;           /* modulus guard, 1e-16 (R#4)                                   */
+    int32_t max_shrinks;  /* trials per iteration before a stall (gamma = 0), 32 (R#9)    */
+    int32_t direction;    /* PTYGER_DIR_*                                                 */
+    int32_t ls_batch;     /* K trials evaluated per pass over the frames, 1..32 (default 16) */
+    int32_t device;       /* CUDA device ordinal                                          */
+    int32_t rank;         /* this process's rank, 0..world-1                              */
+    int32_t world;        /* number of ranks (one GPU each)                               */
+    const void* nccl_id;  /* 128-byte ncclUniqueId from ptyger_nccl_unique_id (world > 1) */
+} ptyger_config;
+
+/* Per-iteration trace (SPEC trace fields S:226-229; step_norm = ||psi_{m+1}-psi_m||_2). */
+typedef struct {
+    int32_t iter;         /* m                                                            */
+    int32_t shrinks;      /* accepted trial index k (gamma = gamma0 tau^k); max_shrinks if stalled */
+    int32_t restarted;    /* 1 if eta = -grad (m = 0 excluded) because |den| < 1e-30 or alpha non-finite */
+    int32_t stalled;      /* 1 if no trial accepted (gamma = 0)                           */
+    double F;             /* F(psi_{m+1}) = F(psi_m) + DeltaF_k (cached, R#11)             */
+    double gamma;         /* accepted step                                                */
+    double alpha_re;      /* alpha_m (0 at m = 0 / restart)                               */
+    double alpha_im;
+    double grad_norm;     /* ||grad F(psi_m)||_2                                          */
+    double step_norm;     /* gamma ||eta_m||_2                                            */
+} ptyger_trace;
+
+/* Fill cfg with the paper's defaults (gamma0 1, tau 0.5, t 0, eps 1e-16, max_shrinks 32,
+ * direction DY, ls_batch 16, device 0, rank 0, world 1, nccl_id NULL). */
+void ptyger_config_default(ptyger_config* cfg);
+
+/*
+ * Create a context and upload one problem (Alg.1).
+ *   object       psi_0: H*W complex64 (2*H*W floats), row-major, host or device.
+ *   probe        p: N*N complex64, host or device; N even, N in {16, 32, 64, 128}.
+ *   scan         n*(row, col) int32 top-left corners, 0<=row<=H-N, 0<=col<=W-N, host.
+ *   intensities  d: n*N*N float32 >= 0 and finite, frame j at offset j*N*N, detector pixel
+ *                (k1, k2) at k1*N + k2 in DFT order (DC at [0,0]); host or device.
+ * When cfg->world > 1 every rank passes the SAME full arrays; the library partitions the
+ * frames into row stripes (ptyger_partition) and uploads only its shard.
+ * Computes u = G psi_0 and F(psi_0) on the device.
+ * Errors: E_ARG (config, N unsupported, infeasible P), E_DATA (window out of bounds,
+ * d negative / non-finite: message names the frame), E_CUDA, E_OOM, E_NCCL.
+ */
+ptyger_status ptyger_init(ptyger_ctx** out, const ptyger_config* cfg,
+                          const float* object, int64_t H, int64_t W,
+                          const float* probe, int32_t N,
+                          const int32_t* scan, int64_t n,
+                          const float* intensities);
+
+/*
+ * Run n_iter CG iterations (Alg.1) as CUDA-graph launches with no host
+ * synchronisation inside; traces (nullable) receives n_iter entries.  Collective when
+ * world > 1.  Errors: E_NUMERIC (non-finite F/alpha/gamma: message names iteration
+ * and stage; psi keeps the last good iterate), E_CUDA, E_NCCL.
+ */
+ptyger_status ptyger_cg_iterate(ptyger_ctx* ctx, int32_t n_iter, ptyger_trace* traces);
+
+/* Current psi_m, H*W complex64 into a host buffer (Alg.1).  Collective when
+ * world > 1 (every rank receives the full united object). */
+ptyger_status ptyger_get_object(ptyger_ctx* ctx, float* out);
+
+/* Last computed gradient grad F(psi_{m-1}) (H*W complex64, zero before the first
+ * iteration).  Collective when world > 1. */
+ptyger_status ptyger_get_gradient(ptyger_ctx* ctx, float* out);
+
+/* Cached far field u = G psi (n*N*N complex64, frames in input order) of the frames this
+ * rank owns (all frames when world = 1), for parity tests. */
+ptyger_status ptyger_get_farfield(ptyger_ctx* ctx, float* out);
+
+/* Teacher-forcing state: psi_m, grad F(psi_{m-1}), eta_{m-1} (H*W complex64 each), the
+ * cached F(psi_m) and m.  get_state: any pointer may be NULL.  set_state uploads
+ * (psi, g_prev, eta_prev, m), recomputes u = G psi and F(psi) by definition on the
+ * device; g_prev / eta_prev are ignored when m == 0.  World == 1 only (E_STATE otherwise). */
+ptyger_status ptyger_get_state(ptyger_ctx* ctx, float* psi, float* g_prev, float* eta_prev,
+                               double* F, int32_t* m);
+ptyger_status ptyger_set_state(ptyger_ctx* ctx, const float* psi, const float* g_prev,
+                               const float* eta_prev, int32_t m);
+
+/* DeltaF_k = F(psi + gamma_k eta) - F(psi) for the trials k = 0..K-1 the last iteration's
+ * line search evaluated (difference form); entries beyond the evaluated
+ * trials are NaN.  Returns the number evaluated in *n_eval (nullable). */
+ptyger_status ptyger_get_ls_partials(ptyger_ctx* ctx, double* dF, int32_t K, int32_t* n_eval);
+
+/* Host-only helpers (no GPU needed) --------------------------------------------------- */
+
+/* Integer stripe partition (R#18; PAPER.md:493-503 workload distribution).
+ *   frame_rank  n int32: rank owning each frame (by centre row r_j + N/2).
+ *   rows        P*6 int64: own_lo, own_hi, ext_lo, ext_hi, store_lo, store_hi per rank.
+ * Returns E_ARG if a stripe's centre-row height is < N (message states the largest
+ * feasible P), E_DATA for a window out of bounds. */
+ptyger_status ptyger_partition(const int32_t* scan, int64_t n, int64_t H, int32_t N, int32_t P,
+                               int32_t* frame_rank, int64_t* rows);
+
+/* Float scan positions (Alg.1 'float32 h_s') -> int32 corners, round half-up
+ * in double: floor((double)x + 0.5) (R#3).  raw and out hold 2*n values. */
+ptyger_status ptyger_round_positions(const float* raw, int64_t n, int32_t* out);
+
+/* Device helpers ------------------------------------------------------------------------ */
+
+/* The library's batched unitary 2-D FFT on DEVICE buffers (cross-check against cuFFT):
+ * batch frames of N*N complex64, forward (inverse = 0, e^{-i}) or inverse (e^{+i}), 1/N scale.
+ * stream is a cudaStream_t (NULL = default stream).  N in {16, 32, 64, 128}. */
+ptyger_status ptyger_fft2(const float* in, float* out, int32_t N, int64_t batch, int32_t inverse,
+                          void* stream);
+
+/* 128-byte NCCL unique id for world > 1 (rank 0 creates, all ranks pass it in config). */
+ptyger_status ptyger_nccl_unique_id(void* out128);
+
+/* Context-owned message for the last error (valid until the next call on ctx); with
+ * ctx == NULL the calling thread's last init / helper error. */
+const char* ptyger_last_error(const ptyger_ctx* ctx);
+
+/* Device time (ms, CUDA events on the context's stream) of the last ptyger_cg_iterate call,
+ * from before its first graph launch to after its last. */
+float ptyger_last_iterate_ms(const ptyger_ctx* ctx);
+
+/* Run n_iter REAL iterations eagerly (no graph) with CUDA events between the kernels and
+ * accumulate device ms into ms[7]: [0] begin, [1] k_grad, [2] k_adj, [3] DY reduce + DIR +
+ * eta (+ band exchange / allreduce), [4] k_ls, [5] LS reduce/pick/extra passes + update,
+ * [6] whole iteration.  For the bench roofline (kernel duration on its launching stream). */
+ptyger_status ptyger_stage_times(ptyger_ctx* ctx, int32_t n_iter, double* ms);
+
+/* Number of kernel launches the last ptyger_cg_iterate call issued (graph nodes counted). */
+int64_t ptyger_kernel_launches(const ptyger_ctx* ctx);
+
+void ptyger_destroy(ptyger_ctx* ctx);
+
+const char* ptyger_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PTYGER_H */

@@ -1,0 +1,247 @@
+"""ctypes binding of libptyger (include/ptyger.h): argument marshalling only.
+
+Every step of the CG iteration runs in the library's CUDA kernels; there is no Python or CPU
+fallback.  If libptyger.so is missing, importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libptyger.so")
+
+PTYGER_OK = 0
+STATUS = {0: "OK", 2: "E_ARG", 3: "E_DATA", 4: "E_NUMERIC", 5: "E_CUDA", 6: "E_NCCL", 7: "E_OOM", 8: "E_STATE"}
+DIR_DY, DIR_DY_REAL, DIR_FR = 0, 1, 2
+
+
+class PtygerError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Config(C.Structure):
+    _fields_ = [("gamma0", C.c_double), ("tau", C.c_double), ("t", C.c_double), ("eps", C.c_double),
+                ("max_shrinks", C.c_int32), ("direction", C.c_int32), ("ls_batch", C.c_int32),
+                ("device", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32), ("nccl_id", C.c_void_p)]
+
+
+class Trace(C.Structure):
+    _fields_ = [("iter", C.c_int32), ("shrinks", C.c_int32), ("restarted", C.c_int32), ("stalled", C.c_int32),
+                ("F", C.c_double), ("gamma", C.c_double), ("alpha_re", C.c_double), ("alpha_im", C.c_double),
+                ("grad_norm", C.c_double), ("step_norm", C.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = C.CDLL(LIB_PATH)
+    P, I32, I64, D = C.c_void_p, C.c_int32, C.c_int64, C.c_double
+    sig = {
+        "ptyger_config_default": (None, [C.POINTER(Config)]),
+        "ptyger_init": (I32, [C.POINTER(P), C.POINTER(Config), P, I64, I64, P, I32, P, I64, P]),
+        "ptyger_cg_iterate": (I32, [P, I32, P]),
+        "ptyger_get_object": (I32, [P, P]),
+        "ptyger_get_gradient": (I32, [P, P]),
+        "ptyger_get_farfield": (I32, [P, P]),
+        "ptyger_get_state": (I32, [P, P, P, P, P, P]),
+        "ptyger_set_state": (I32, [P, P, P, P, I32]),
+        "ptyger_get_ls_partials": (I32, [P, P, I32, P]),
+        "ptyger_partition": (I32, [P, I64, I64, I32, I32, P, P]),
+        "ptyger_round_positions": (I32, [P, I64, P]),
+        "ptyger_fft2": (I32, [P, P, I32, I64, I32, P]),
+        "ptyger_nccl_unique_id": (I32, [P]),
+        "ptyger_last_error": (C.c_char_p, [P]),
+        "ptyger_kernel_launches": (I64, [P]),
+        "ptyger_last_iterate_ms": (C.c_float, [P]),
+        "ptyger_stage_times": (I32, [P, I32, P]),
+        "ptyger_destroy": (None, [P]),
+        "ptyger_version": (C.c_char_p, []),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    return lib
+
+
+lib = _load()
+
+
+def last_error(ctx=None) -> str:
+    s = lib.ptyger_last_error(ctx)
+    return s.decode() if s else ""
+
+
+def _check(status: int, ctx=None):
+    if status != PTYGER_OK:
+        raise PtygerError(status, last_error(ctx))
+
+
+def default_config(**kw) -> Config:
+    c = Config()
+    lib.ptyger_config_default(C.byref(c))
+    for k, v in kw.items():
+        setattr(c, k, v)
+    return c
+
+
+def _ptr(a):
+    """Host numpy array or torch tensor (host or CUDA) -> (pointer, keepalive)."""
+    if a is None:
+        return None, None
+    if hasattr(a, "data_ptr"):           # torch tensor
+        if not a.is_contiguous():
+            a = a.contiguous()
+        return a.data_ptr(), a
+    a = np.ascontiguousarray(a)
+    return a.ctypes.data, a
+
+
+def as_c64(a):
+    """complex array -> interleaved float32 view/buffer; torch tensors pass through."""
+    if hasattr(a, "data_ptr"):
+        import torch
+        if a.is_complex():
+            return torch.view_as_real(a.to(torch.complex64).contiguous())
+        return a.float().contiguous()
+    a = np.asarray(a)
+    if np.iscomplexobj(a):
+        return np.ascontiguousarray(a.astype(np.complex64)).view(np.float32)
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+def partition(scan, H: int, N: int, P: int):
+    scan = np.ascontiguousarray(scan, dtype=np.int32)
+    n = len(scan)
+    rank = np.zeros(n, np.int32)
+    rows = np.zeros((P, 6), np.int64)
+    _check(lib.ptyger_partition(scan.ctypes.data, n, H, N, P, rank.ctypes.data, rows.ctypes.data))
+    return rank, rows
+
+
+def round_positions(raw):
+    raw = np.ascontiguousarray(raw, dtype=np.float32)
+    out = np.zeros(raw.shape, np.int32)
+    _check(lib.ptyger_round_positions(raw.ctypes.data, len(raw), out.ctypes.data))
+    return out
+
+
+def fft2(x, inverse: bool = False, out=None):
+    """Library batched unitary 2-D FFT on a CUDA complex64 tensor (..., N, N)."""
+    import torch
+    assert x.is_cuda and x.dtype == torch.complex64
+    x = x.contiguous()
+    N = x.shape[-1]
+    batch = x.numel() // (N * N)
+    if out is None:
+        out = torch.empty_like(x)
+    stream = torch.cuda.current_stream(x.device).cuda_stream
+    _check(lib.ptyger_fft2(x.data_ptr(), out.data_ptr(), N, batch, int(inverse), stream))
+    return out
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_char * 128)()
+    _check(lib.ptyger_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+class Ptyger:
+    """One reconstruction problem resident on one GPU (or one stripe of it when world > 1).
+
+    Wraps ptyger_init / ptyger_cg_iterate / ptyger_get_object (Alg.1)."""
+
+    def __init__(self, obj, probe, scan, d, config: Config | None = None, **cfg):
+        self.cfg = config if config is not None else default_config(**cfg)
+        self._nccl_buf = None
+        if self.cfg.world > 1 and "nccl_id" in cfg and isinstance(cfg["nccl_id"], (bytes, bytearray)):
+            pass
+        o = as_c64(obj)
+        p = as_c64(probe)
+        self.H, self.W = (o.shape[0], o.shape[1]) if o.ndim == 3 else (obj.shape[0], obj.shape[1])
+        self.N = int(probe.shape[0])
+        sc = np.ascontiguousarray(np.asarray(scan), dtype=np.int32)
+        self.n = len(sc)
+        dd = d if hasattr(d, "data_ptr") else np.ascontiguousarray(d, dtype=np.float32)
+        po, ko = _ptr(o)
+        pp, kp = _ptr(p)
+        pd, kd = _ptr(dd)
+        self.ctx = C.c_void_p()
+        st = lib.ptyger_init(C.byref(self.ctx), C.byref(self.cfg), po, self.H, self.W, pp, self.N,
+                             sc.ctypes.data, self.n, pd)
+        _check(st, None)
+        self.K = self.cfg.ls_batch
+
+    def close(self):
+        if getattr(self, "ctx", None) and self.ctx.value:
+            lib.ptyger_destroy(self.ctx)
+            self.ctx = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def iterate(self, n_iter: int, traces: bool = True):
+        tr = (Trace * max(n_iter, 1))()
+        _check(lib.ptyger_cg_iterate(self.ctx, n_iter, tr if traces else None), self.ctx)
+        return [tr[i].as_dict() for i in range(n_iter)] if traces else None
+
+    def _obj_buf(self):
+        return np.empty((self.H, self.W), np.complex64)
+
+    def get_object(self):
+        out = self._obj_buf()
+        _check(lib.ptyger_get_object(self.ctx, out.ctypes.data), self.ctx)
+        return out
+
+    def get_gradient(self):
+        out = self._obj_buf()
+        _check(lib.ptyger_get_gradient(self.ctx, out.ctypes.data), self.ctx)
+        return out
+
+    def get_farfield(self, n_local: int | None = None):
+        out = np.empty((n_local if n_local is not None else self.n, self.N, self.N), np.complex64)
+        _check(lib.ptyger_get_farfield(self.ctx, out.ctypes.data), self.ctx)
+        return out
+
+    def get_state(self):
+        psi, g, e = self._obj_buf(), self._obj_buf(), self._obj_buf()
+        F = C.c_double()
+        m = C.c_int32()
+        _check(lib.ptyger_get_state(self.ctx, psi.ctypes.data, g.ctypes.data, e.ctypes.data, C.byref(F),
+                                    C.byref(m)), self.ctx)
+        return psi, g, e, F.value, m.value
+
+    def set_state(self, psi, g_prev=None, eta_prev=None, m: int = 0):
+        a = np.ascontiguousarray(psi, dtype=np.complex64)
+        b = None if g_prev is None else np.ascontiguousarray(g_prev, dtype=np.complex64)
+        c = None if eta_prev is None else np.ascontiguousarray(eta_prev, dtype=np.complex64)
+        _check(lib.ptyger_set_state(self.ctx, a.ctypes.data, None if b is None else b.ctypes.data,
+                                    None if c is None else c.ctypes.data, m), self.ctx)
+
+    def get_ls_partials(self, K: int = 64):
+        out = np.empty(K, np.float64)
+        ne = C.c_int32()
+        _check(lib.ptyger_get_ls_partials(self.ctx, out.ctypes.data, K, C.byref(ne)), self.ctx)
+        return out[:ne.value]
+
+    def last_iterate_ms(self) -> float:
+        return float(lib.ptyger_last_iterate_ms(self.ctx))
+
+    def stage_times(self, n_iter: int):
+        ms = np.zeros(7, np.float64)
+        _check(lib.ptyger_stage_times(self.ctx, n_iter, ms.ctypes.data), self.ctx)
+        return ms
+
+    def kernel_launches(self) -> int:
+        return int(lib.ptyger_kernel_launches(self.ctx))

@@ -1,0 +1,762 @@
+// libptyger runtime: context, C ABI entry points, CUDA-graph capture of one CG iteration and
+// the NCCL plumbing for world > 1 (band exchange of partial gradients + fp64 allreduces of the
+// DY and LS scalars).
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "host.h"
+#include "internal.h"
+
+using namespace pty;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+// ---------------- NCCL, loaded on demand (world == 1 never touches it) ----------------------
+struct NcclApi {
+    bool ok = false;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*);
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int);
+    ncclResult_t (*CommDestroy)(ncclComm_t);
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t);
+    ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+    ncclResult_t (*GroupStart)();
+    ncclResult_t (*GroupEnd)();
+    const char* (*GetErrorString)(ncclResult_t);
+};
+
+NcclApi* nccl_api(std::string& err) {
+    static NcclApi api;
+    static bool tried = false;
+    if (tried) {
+        if (!api.ok) err = "NCCL library could not be loaded (set PTYGER_NCCL_LIB)";
+        return api.ok ? &api : nullptr;
+    }
+    tried = true;
+    const char* cands[] = {getenv("PTYGER_NCCL_LIB"), "libnccl.so.2", "libnccl.so"};
+    void* h = nullptr;
+    for (const char* c : cands) {
+        if (!c) continue;
+        h = dlopen(c, RTLD_NOW | RTLD_GLOBAL);
+        if (h) break;
+    }
+    if (!h) {
+        err = "NCCL library could not be loaded (set PTYGER_NCCL_LIB)";
+        return nullptr;
+    }
+#define LD(name, sym)                                                  \
+    api.name = reinterpret_cast<decltype(api.name)>(dlsym(h, sym));   \
+    if (!api.name) {                                                   \
+        err = std::string("NCCL symbol missing: ") + sym;              \
+        return nullptr;                                                \
+    }
+    LD(GetUniqueId, "ncclGetUniqueId");
+    LD(CommInitRank, "ncclCommInitRank");
+    LD(CommDestroy, "ncclCommDestroy");
+    LD(AllReduce, "ncclAllReduce");
+    LD(Broadcast, "ncclBroadcast");
+    LD(Send, "ncclSend");
+    LD(Recv, "ncclRecv");
+    LD(GroupStart, "ncclGroupStart");
+    LD(GroupEnd, "ncclGroupEnd");
+    LD(GetErrorString, "ncclGetErrorString");
+#undef LD
+    api.ok = true;
+    return &api;
+}
+
+template <typename T>
+T* dalloc(size_t count, std::string& err, bool zero = true) {
+    void* p = nullptr;
+    if (count == 0) count = 1;
+    if (cudaMalloc(&p, count * sizeof(T)) != cudaSuccess) {
+        cudaGetLastError();
+        err = "cudaMalloc of " + std::to_string(count * sizeof(T)) + " bytes failed";
+        return nullptr;
+    }
+    if (zero) cudaMemset(p, 0, count * sizeof(T));
+    return static_cast<T*>(p);
+}
+
+}  // namespace
+
+struct ptyger_ctx {
+    ptyger_config cfg{};
+    SolverCfg sc{};
+    int64_t H = 0, W = 0, n = 0;
+    int N = 0;
+    int sms = 148;
+    // partition
+    std::vector<int32_t> frame_rank;
+    std::vector<int64_t> rows;   // P*6
+    int64_t st_lo = 0, st_hi = 0, SH = 0;
+    std::vector<int64_t> local_global;  // storage index -> global frame index
+    Geometry geo{};
+    // device
+    float2 *psi = nullptr, *g[2] = {nullptr, nullptr}, *eta = nullptr, *u = nullptr, *v = nullptr,
+           *probe = nullptr, *full = nullptr, *recv[2] = {nullptr, nullptr};
+    float* d = nullptr;
+    int2* pos = nullptr;
+    int* order = nullptr;
+    int* tile_ptr = nullptr;
+    int* entries = nullptr;
+    int ntx = 0, nty = 0;
+    double *part_adj = nullptr, *part_fr = nullptr, *part_el = nullptr, *scratch = nullptr;
+    int band_grid = 0;
+    DevState* st = nullptr;
+    ptyger_trace* d_tr = nullptr;
+    int tr_cap = 0;
+    cudaStream_t stream = nullptr;
+    cudaGraphExec_t graph[2] = {nullptr, nullptr};
+    cudaEvent_t ev_it[2] = {nullptr, nullptr};
+    float last_ms = 0.f;
+    int grid_fr = 0, grid_el = 0;
+    int m_host = 0;
+    int64_t launches_per_iter = 0, last_launches = 0;
+    bool failed_numeric = false;
+    // bands: [0] with rank-1, [1] with rank+1 (storage-local rows)
+    int64_t band_lo[2] = {0, 0}, band_rows[2] = {0, 0};
+    // nccl
+    NcclApi* nc = nullptr;
+    ncclComm_t comm = nullptr;
+    std::string err;
+};
+
+#define CK(call)                                                                                  \
+    do {                                                                                          \
+        cudaError_t e_ = (call);                                                                  \
+        if (e_ != cudaSuccess) {                                                                  \
+            err = std::string(#call) + ": " + cudaGetErrorString(e_);                            \
+            return PTYGER_E_CUDA;                                                                 \
+        }                                                                                         \
+    } while (0)
+
+#define NK(call)                                                                                  \
+    do {                                                                                          \
+        ncclResult_t r_ = (call);                                                                 \
+        if (r_ != ncclSuccess) {                                                                  \
+            err = std::string(#call) + ": " + c->nc->GetErrorString(r_);                          \
+            return PTYGER_E_NCCL;                                                                 \
+        }                                                                                         \
+    } while (0)
+
+#define LK(call)                                                                                  \
+    do {                                                                                          \
+        if ((call) != 0) {                                                                        \
+            err = std::string("kernel launch failed: ") + #call + ": " +                          \
+                  cudaGetErrorString(cudaGetLastError());                                         \
+            return PTYGER_E_CUDA;                                                                 \
+        }                                                                                         \
+    } while (0)
+
+static ptyger_status set_err(ptyger_ctx* c, ptyger_status s, const std::string& m) {
+    if (c)
+        c->err = m;
+    else
+        g_last_error = m;
+    return s;
+}
+
+// ------------------------------------------------------------------------------------------
+// One iteration as a sequence of launches on c->stream (captured into a graph).
+// parity p: gcur = g[p], gprev = g[1-p].
+// ------------------------------------------------------------------------------------------
+static int enqueue_iteration(ptyger_ctx* c, int p, std::string& err, int64_t& launches,
+                             cudaEvent_t* ev = nullptr) {
+    const bool multi = c->cfg.world > 1;
+#define EV(i) \
+    if (ev) CK(cudaEventRecord(ev[i], c->stream))
+    float2* gcur = c->g[p];
+    float2* gprev = c->g[1 - p];
+    cudaStream_t s = c->stream;
+    const Geometry& g = c->geo;
+    const SolverCfg& sc = c->sc;
+    const float eps = (float)sc.eps;
+    launches = 0;
+    EV(0);
+    LK(launch_begin_iter(c->st, s)); ++launches;
+    EV(1);
+    // GRAD stage (Alg.1 648-649)
+    LK(launch_grad(g, c->u, c->v, c->d, c->probe, c->order, c->st, eps, c->grid_fr, s)); ++launches;
+    EV(2);
+    LK(launch_adj(g, c->v, c->tile_ptr, c->entries, c->ntx, c->nty, gcur, gprev, c->eta, c->part_adj, c->st, s));
+    ++launches;
+    EV(3);
+    int nparts = c->ntx * c->nty;
+    if (multi) {
+        // band exchange of partial gradients with the two neighbours (replaces the paper's
+        // pattern duplication + border exchange, R#15)
+        NK(c->nc->GroupStart());
+        const int peers[2] = {c->cfg.rank - 1, c->cfg.rank + 1};
+        for (int b = 0; b < 2; ++b) {
+            if (c->band_rows[b] <= 0) continue;
+            const size_t cnt = (size_t)(c->band_rows[b] * c->W * 2);
+            NK(c->nc->Send(gcur + c->band_lo[b] * c->W, cnt, ncclFloat32, peers[b], c->comm, s));
+            NK(c->nc->Recv(c->recv[b], cnt, ncclFloat32, peers[b], c->comm, s));
+        }
+        NK(c->nc->GroupEnd());
+        for (int b = 0; b < 2; ++b) {
+            if (c->band_rows[b] <= 0) continue;
+            LK(launch_band_add(gcur, c->recv[b], c->band_lo[b], c->band_rows[b], c->W, gprev, c->eta, g.own_lo, g.own_hi,
+                               c->part_adj + (int64_t)nparts * NDY, c->band_grid, s));
+            ++launches;
+            nparts += c->band_grid;
+        }
+    }
+    LK(launch_reduce(c->part_adj, nparts, NDY, &c->st->dy[0], s)); ++launches;
+    if (multi) NK(c->nc->AllReduce(&c->st->dy[0], &c->st->dy[0], NDY, ncclFloat64, ncclSum, c->comm, s));
+    // DIR stage (Alg.1 651-656)
+    LK(launch_dir(c->st, sc, s)); ++launches;
+    LK(launch_eta(g, gcur, c->eta, c->st, c->part_el, c->grid_el, s)); ++launches;
+    LK(launch_reduce(c->part_el, c->grid_el, 1, &c->st->ls_pass[KMAX], s)); ++launches;
+    EV(4);
+    // LS stage (Alg.1 659-668): first pass computes v = G eta and K trials
+    LK(launch_ls(g, c->eta, c->probe, c->pos, c->order, c->u, c->v, c->d, sc, c->part_fr, c->grid_fr, c->st, s));
+    ++launches;
+    EV(5);
+    LK(launch_reduce(c->part_fr, c->grid_fr, sc.K, &c->st->ls_pass[0], s)); ++launches;
+    const int npass = (sc.max_shrinks + sc.K - 1) / sc.K;
+    if (multi) NK(c->nc->AllReduce(&c->st->ls_pass[0], &c->st->ls_pass[0], KMAX + 1, ncclFloat64, ncclSum, c->comm, s));
+    LK(launch_pick(c->st, sc, 0, npass == 1, s)); ++launches;
+    for (int pass = 1; pass < npass; ++pass) {
+        LK(launch_lsx(g, c->u, c->v, c->d, sc, pass, c->part_el, c->grid_el, c->st, s)); ++launches;
+        LK(launch_reduce(c->part_el, c->grid_el, sc.K, &c->st->ls_pass[0], s)); ++launches;
+        if (multi) NK(c->nc->AllReduce(&c->st->ls_pass[0], &c->st->ls_pass[0], sc.K, ncclFloat64, ncclSum, c->comm, s));
+        LK(launch_pick(c->st, sc, pass, pass == npass - 1, s)); ++launches;
+    }
+    // Update stage (Alg.1 672)
+    LK(launch_upd(g, c->psi, c->eta, c->st, c->grid_el, s)); ++launches;
+    EV(6);
+#undef EV
+    return 0;
+}
+
+static int build_graphs(ptyger_ctx* c, std::string& err) {
+    for (int p = 0; p < 2; ++p) {
+        if (c->graph[p]) {
+            cudaGraphExecDestroy(c->graph[p]);
+            c->graph[p] = nullptr;
+        }
+        cudaGraph_t gr = nullptr;
+        CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        int64_t launches = 0;
+        const int rc = enqueue_iteration(c, p, err, launches);
+        cudaGraph_t tmp = nullptr;
+        const cudaError_t ce = cudaStreamEndCapture(c->stream, &tmp);
+        if (rc) {
+            if (tmp) cudaGraphDestroy(tmp);
+            return rc;
+        }
+        if (ce != cudaSuccess) {
+            err = std::string("cudaStreamEndCapture: ") + cudaGetErrorString(ce);
+            return PTYGER_E_CUDA;
+        }
+        gr = tmp;
+        CK(cudaGraphInstantiate(&c->graph[p], gr, 0));
+        cudaGraphDestroy(gr);
+        c->launches_per_iter = launches;
+    }
+    return 0;
+}
+
+// u = G psi and F(psi) (by definition) -> st->F, gamma = 0
+static int run_forward(ptyger_ctx* c, std::string& err) {
+    const Geometry& g = c->geo;
+    LK(launch_fwd(g, c->psi, c->probe, c->pos, c->order, c->d, c->u, c->part_fr, c->grid_fr, (float)c->sc.eps, c->stream));
+    LK(launch_reduce(c->part_fr, c->grid_fr, 1, c->scratch, c->stream));
+    if (c->cfg.world > 1) {
+        ncclResult_t r = c->nc->AllReduce(c->scratch, c->scratch, 1, ncclFloat64, ncclSum, c->comm, c->stream);
+        if (r != ncclSuccess) {
+            err = std::string("ncclAllReduce(F0): ") + c->nc->GetErrorString(r);
+            return PTYGER_E_NCCL;
+        }
+    }
+    LK(launch_set_F(c->st, c->scratch, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return 0;
+}
+
+static void free_ctx(ptyger_ctx* c) {
+    if (!c) return;
+    for (int p = 0; p < 2; ++p)
+        if (c->graph[p]) cudaGraphExecDestroy(c->graph[p]);
+    void* ptrs[] = {c->psi, c->g[0], c->g[1], c->eta, c->u, c->v, c->probe, c->full, c->recv[0], c->recv[1], c->d,
+                    c->pos, c->order, c->tile_ptr, c->entries, c->part_adj, c->part_fr, c->part_el, c->scratch, c->st,
+                    c->d_tr};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    for (int i = 0; i < 2; ++i)
+        if (c->ev_it[i]) cudaEventDestroy(c->ev_it[i]);
+    if (c->comm && c->nc) c->nc->CommDestroy(c->comm);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+extern "C" {
+
+void ptyger_config_default(ptyger_config* cfg) {
+    if (!cfg) return;
+    cfg->gamma0 = 1.0;
+    cfg->tau = 0.5;
+    cfg->t = 0.0;
+    cfg->eps = 1e-16;
+    cfg->max_shrinks = 32;
+    cfg->direction = PTYGER_DIR_DY;
+    cfg->ls_batch = 16;
+    cfg->device = 0;
+    cfg->rank = 0;
+    cfg->world = 1;
+    cfg->nccl_id = nullptr;
+}
+
+const char* ptyger_version(void) { return "ptyger-b200 0.1 (sm_100a)"; }
+
+const char* ptyger_last_error(const ptyger_ctx* ctx) {
+    return ctx ? ctx->err.c_str() : g_last_error.c_str();
+}
+
+int64_t ptyger_kernel_launches(const ptyger_ctx* ctx) { return ctx ? ctx->last_launches : 0; }
+
+ptyger_status ptyger_round_positions(const float* raw, int64_t n, int32_t* out) {
+    if (!raw || !out || n < 0) return set_err(nullptr, PTYGER_E_ARG, "round_positions: null pointer or n < 0");
+    round_positions(raw, n, out);
+    return PTYGER_OK;
+}
+
+ptyger_status ptyger_partition(const int32_t* scan, int64_t n, int64_t H, int32_t N, int32_t P,
+                               int32_t* frame_rank, int64_t* rows) {
+    if (!scan || !frame_rank || !rows) return set_err(nullptr, PTYGER_E_ARG, "partition: null pointer");
+    std::vector<int32_t> rk;
+    std::vector<int64_t> rw;
+    std::string err;
+    const int rc = partition(scan, n, H, N, P, rk, rw, err);
+    if (rc) return set_err(nullptr, (ptyger_status)rc, err);
+    std::memcpy(frame_rank, rk.data(), sizeof(int32_t) * n);
+    std::memcpy(rows, rw.data(), sizeof(int64_t) * rw.size());
+    return PTYGER_OK;
+}
+
+ptyger_status ptyger_nccl_unique_id(void* out128) {
+    std::string err;
+    NcclApi* api = nccl_api(err);
+    if (!api) return set_err(nullptr, PTYGER_E_NCCL, err);
+    ncclUniqueId id;
+    ncclResult_t r = api->GetUniqueId(&id);
+    if (r != ncclSuccess) return set_err(nullptr, PTYGER_E_NCCL, api->GetErrorString(r));
+    std::memcpy(out128, &id, sizeof(id));
+    return PTYGER_OK;
+}
+
+ptyger_status ptyger_fft2(const float* in, float* out, int32_t N, int64_t batch, int32_t inverse, void* stream) {
+    if (!in || !out || batch < 0) return set_err(nullptr, PTYGER_E_ARG, "fft2: null pointer or batch < 0");
+    if (N != 16 && N != 32 && N != 64 && N != 128)
+        return set_err(nullptr, PTYGER_E_ARG, "fft2: N must be 16, 32, 64 or 128");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return set_err(nullptr, PTYGER_E_CUDA, "fft2: no CUDA device");
+    }
+    if (batch == 0) return PTYGER_OK;
+    const int rc = launch_fft2(reinterpret_cast<const float2*>(in), reinterpret_cast<float2*>(out), N, batch,
+                               inverse != 0, (cudaStream_t)stream);
+    if (rc) return set_err(nullptr, PTYGER_E_CUDA, std::string("fft2 launch: ") + cudaGetErrorString(cudaGetLastError()));
+    return PTYGER_OK;
+}
+
+static ptyger_status init_impl(ptyger_ctx* c, const float* object, const float* probe, const int32_t* scan,
+                               const float* intensities) {
+    std::string& err = c->err;
+    const ptyger_config& cfg = c->cfg;
+    const int N = c->N;
+    const int64_t H = c->H, W = c->W, n = c->n;
+    // ---- partition (host) ----
+    const int rc = partition(scan, n, H, N, cfg.world, c->frame_rank, c->rows, err);
+    if (rc) return (ptyger_status)rc;
+    const int me = cfg.rank;
+    const int64_t* R = &c->rows[6 * me];
+    c->st_lo = R[4];
+    c->st_hi = R[5];
+    c->SH = c->st_hi - c->st_lo;
+    for (int64_t j = 0; j < n; ++j)
+        if (c->frame_rank[j] == me) c->local_global.push_back(j);
+    const int64_t nl = (int64_t)c->local_global.size();
+    // bands (storage-local)
+    if (cfg.world > 1) {
+        if (me > 0) {
+            const int64_t lo = R[2], hi = c->rows[6 * (me - 1) + 3];
+            if (hi > lo) { c->band_lo[0] = lo - c->st_lo; c->band_rows[0] = hi - lo; }
+        }
+        if (me + 1 < cfg.world) {
+            const int64_t lo = c->rows[6 * (me + 1) + 2], hi = R[3];
+            if (hi > lo) { c->band_lo[1] = lo - c->st_lo; c->band_rows[1] = hi - lo; }
+        }
+    }
+    Geometry& g = c->geo;
+    g.N = N;
+    g.W = W;
+    g.SH = c->SH;
+    g.own_lo = R[0] - c->st_lo;
+    g.own_hi = R[1] - c->st_lo;
+    g.band_lo0 = c->band_lo[0];
+    g.band_hi0 = c->band_lo[0] + c->band_rows[0];
+    g.band_lo1 = c->band_lo[1];
+    g.band_hi1 = c->band_lo[1] + c->band_rows[1];
+    g.n_local = nl;
+    // local positions and canonical processing order
+    std::vector<int32_t> lpos(2 * nl);
+    std::vector<int32_t> sub(2 * nl);
+    for (int64_t i = 0; i < nl; ++i) {
+        const int64_t j = c->local_global[i];
+        lpos[2 * i] = (int32_t)(scan[2 * j] - c->st_lo);
+        lpos[2 * i + 1] = scan[2 * j + 1];
+        sub[2 * i] = scan[2 * j];
+        sub[2 * i + 1] = scan[2 * j + 1];
+    }
+    std::vector<int64_t> ord64;
+    canonical_order(sub.data(), nl, N, ord64);
+    std::vector<int32_t> ord(ord64.begin(), ord64.end());
+    std::vector<int32_t> tptr, ent;
+    build_tiles(lpos, ord, N, c->SH, W, c->ntx, c->nty, tptr, ent);
+
+    // ---- device ----
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        err = "no CUDA device (libptyger has no CPU fallback)";
+        return PTYGER_E_CUDA;
+    }
+    if (cfg.device < 0 || cfg.device >= ndev) {
+        err = "config.device out of range";
+        return PTYGER_E_ARG;
+    }
+    CK(cudaSetDevice(cfg.device));
+    CK(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, cfg.device));
+    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    if (cfg.world > 1) {
+        c->nc = nccl_api(err);
+        if (!c->nc) return PTYGER_E_NCCL;
+        ncclUniqueId id;
+        std::memcpy(&id, cfg.nccl_id, sizeof(id));
+        NK(c->nc->CommInitRank(&c->comm, cfg.world, id, cfg.rank));
+    }
+    const int64_t obj = c->SH * W;
+    const int64_t NN = (int64_t)N * N;
+#define AL(ptr, T, cnt)                                  \
+    do {                                                 \
+        ptr = dalloc<T>((size_t)(cnt), err);             \
+        if (!ptr) return PTYGER_E_OOM;                   \
+    } while (0)
+    AL(c->psi, float2, obj);
+    AL(c->g[0], float2, obj);
+    AL(c->g[1], float2, obj);
+    AL(c->eta, float2, obj);
+    AL(c->u, float2, nl * NN);
+    AL(c->v, float2, nl * NN);
+    AL(c->d, float, nl * NN);
+    AL(c->probe, float2, NN);
+    AL(c->pos, int2, nl);
+    AL(c->order, int, nl);
+    AL(c->tile_ptr, int, tptr.size());
+    AL(c->entries, int, ent.size());
+    c->grid_fr = (int)std::max<int64_t>(1, std::min<int64_t>(c->sms, nl));
+    c->grid_el = c->sms * 8;
+    c->band_grid = c->sms * 2;
+    AL(c->part_adj, double, ((int64_t)c->ntx * c->nty + 2 * c->band_grid) * NDY);
+    AL(c->part_fr, double, (int64_t)c->grid_fr * KMAX);
+    AL(c->part_el, double, (int64_t)c->grid_el * KMAX);
+    AL(c->scratch, double, 64);
+    AL(c->st, DevState, 1);
+    for (int b = 0; b < 2; ++b)
+        if (c->band_rows[b] > 0) AL(c->recv[b], float2, c->band_rows[b] * W);
+    if (cfg.world > 1) AL(c->full, float2, H * W);
+#undef AL
+    CK(cudaMemcpy(c->psi, object + 2 * c->st_lo * W, sizeof(float2) * obj, cudaMemcpyDefault));
+    CK(cudaMemcpy(c->probe, probe, sizeof(float2) * NN, cudaMemcpyDefault));
+    // d: contiguous runs of local frames
+    for (int64_t i = 0; i < nl;) {
+        int64_t k = i;
+        while (k + 1 < nl && c->local_global[k + 1] == c->local_global[k] + 1) ++k;
+        const int64_t j0 = c->local_global[i];
+        CK(cudaMemcpy(c->d + i * NN, intensities + j0 * NN, sizeof(float) * NN * (k - i + 1), cudaMemcpyDefault));
+        i = k + 1;
+    }
+    std::vector<int2> p2(nl);
+    for (int64_t i = 0; i < nl; ++i) p2[i] = make_int2(lpos[2 * i], lpos[2 * i + 1]);
+    CK(cudaMemcpy(c->pos, p2.data(), sizeof(int2) * nl, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->order, ord.data(), sizeof(int) * nl, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->tile_ptr, tptr.data(), sizeof(int) * tptr.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->entries, ent.data(), sizeof(int) * ent.size(), cudaMemcpyHostToDevice));
+    // validate d on the device
+    {
+        unsigned long long* bad = dalloc<unsigned long long>(1, err, false);
+        if (!bad) return PTYGER_E_OOM;
+        const unsigned long long init = ~0ull;
+        CK(cudaMemcpy(bad, &init, sizeof(init), cudaMemcpyHostToDevice));
+        LK(launch_validate_d(c->d, nl * NN, NN, bad, c->stream));
+        unsigned long long hb = 0;
+        CK(cudaStreamSynchronize(c->stream));
+        CK(cudaMemcpy(&hb, bad, sizeof(hb), cudaMemcpyDeviceToHost));
+        cudaFree(bad);
+        if (hb != ~0ull) {
+            err = "intensities: frame " + std::to_string(c->local_global[(int64_t)hb]) +
+                  " has a negative or non-finite value";
+            return PTYGER_E_DATA;
+        }
+    }
+    // F(psi_0), u_0
+    DevState hs;
+    std::memset(&hs, 0, sizeof(hs));
+    CK(cudaMemcpy(c->st, &hs, sizeof(hs), cudaMemcpyHostToDevice));
+    int rc2 = run_forward(c, err);
+    if (rc2) return (ptyger_status)rc2;
+    rc2 = build_graphs(c, err);
+    if (rc2) return (ptyger_status)rc2;
+    return PTYGER_OK;
+}
+
+ptyger_status ptyger_init(ptyger_ctx** out, const ptyger_config* cfg_in, const float* object, int64_t H, int64_t W,
+                          const float* probe, int32_t N, const int32_t* scan, int64_t n, const float* intensities) {
+    if (!out) return set_err(nullptr, PTYGER_E_ARG, "init: out is NULL");
+    *out = nullptr;
+    ptyger_config cfg;
+    if (cfg_in)
+        cfg = *cfg_in;
+    else
+        ptyger_config_default(&cfg);
+    if (!object || !probe || !scan || !intensities) return set_err(nullptr, PTYGER_E_ARG, "init: null input array");
+    if (!(cfg.gamma0 > 0) || !(cfg.tau > 0 && cfg.tau < 1) || !(cfg.eps > 0) || cfg.max_shrinks < 1 ||
+        cfg.max_shrinks > SMAX || (cfg.ls_batch != 8 && cfg.ls_batch != 16) || cfg.direction < 0 ||
+        cfg.direction > 2 || cfg.world < 1 || cfg.rank < 0 || cfg.rank >= cfg.world ||
+        (cfg.world > 1 && !cfg.nccl_id) || !std::isfinite(cfg.t))
+        return set_err(nullptr, PTYGER_E_ARG,
+                       "init: bad config (need gamma0>0, 0<tau<1, eps>0, 1<=max_shrinks<=64, ls_batch in {8,16}, "
+                       "direction in {0,1,2}, 0<=rank<world, nccl_id when world>1)");
+    if (N != 16 && N != 32 && N != 64 && N != 128)
+        return set_err(nullptr, PTYGER_E_ARG, "init: N must be 16, 32, 64 or 128");
+    if (H < N || W < N) return set_err(nullptr, PTYGER_E_DATA, "init: object smaller than the probe");
+    if (n < 1) return set_err(nullptr, PTYGER_E_DATA, "init: need at least one scan position");
+    for (int64_t j = 0; j < n; ++j) {
+        const int64_t r = scan[2 * j], cc = scan[2 * j + 1];
+        if (r < 0 || r > H - N || cc < 0 || cc > W - N)
+            return set_err(nullptr, PTYGER_E_DATA,
+                           "init: scan position of frame " + std::to_string(j) + " (" + std::to_string(r) + ", " +
+                               std::to_string(cc) + ") puts the window outside the object");
+    }
+    ptyger_ctx* c = new ptyger_ctx();
+    c->cfg = cfg;
+    c->sc.gamma0 = cfg.gamma0;
+    c->sc.tau = cfg.tau;
+    c->sc.t = cfg.t;
+    c->sc.eps = cfg.eps;
+    c->sc.max_shrinks = cfg.max_shrinks;
+    c->sc.direction = cfg.direction;
+    c->sc.K = cfg.ls_batch;
+    c->H = H;
+    c->W = W;
+    c->N = N;
+    c->n = n;
+    const ptyger_status s = init_impl(c, object, probe, scan, intensities);
+    if (s != PTYGER_OK) {
+        g_last_error = c->err;
+        free_ctx(c);
+        return s;
+    }
+    *out = c;
+    return PTYGER_OK;
+}
+
+static ptyger_status check_numeric(ptyger_ctx* c) {
+    DevState hs;
+    std::string& err = c->err;
+    CK(cudaMemcpy(&hs, c->st, sizeof(hs), cudaMemcpyDeviceToHost));
+    if (hs.numeric_error) {
+        const char* stage = hs.numeric_error == 1 ? "DIR (non-finite ||grad||^2)"
+                            : hs.numeric_error == 2 ? "LS (non-finite DeltaF)"
+                                                    : "LS (non-finite F)";
+        c->failed_numeric = true;
+        return set_err(c, PTYGER_E_NUMERIC,
+                       "numeric failure at iteration " + std::to_string(hs.err_iter) + " in stage " + stage +
+                           "; psi holds the last good iterate");
+    }
+    return PTYGER_OK;
+}
+
+ptyger_status ptyger_cg_iterate(ptyger_ctx* c, int32_t n_iter, ptyger_trace* traces) {
+    if (!c) return set_err(nullptr, PTYGER_E_ARG, "cg_iterate: ctx is NULL");
+    std::string& err = c->err;
+    if (n_iter < 0) return set_err(c, PTYGER_E_ARG, "cg_iterate: n_iter < 0");
+    if (c->failed_numeric) return set_err(c, PTYGER_E_NUMERIC, "context is in a numeric-failure state; call set_state");
+    if (n_iter == 0) return PTYGER_OK;
+    CK(cudaSetDevice(c->cfg.device));
+    if (c->tr_cap < n_iter) {
+        if (c->d_tr) cudaFree(c->d_tr);
+        c->d_tr = dalloc<ptyger_trace>((size_t)n_iter, err);
+        if (!c->d_tr) return PTYGER_E_OOM;
+        c->tr_cap = n_iter;
+    }
+    struct { int idx, cap; ptyger_trace* p; } hdr = {0, c->tr_cap, c->d_tr};
+    CK(cudaMemcpyAsync(&c->st->trace_idx, &hdr, sizeof(int) * 2, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(&c->st->trace_ptr, &hdr.p, sizeof(hdr.p), cudaMemcpyHostToDevice, c->stream));
+    if (!c->ev_it[0]) {
+        CK(cudaEventCreate(&c->ev_it[0]));
+        CK(cudaEventCreate(&c->ev_it[1]));
+    }
+    CK(cudaEventRecord(c->ev_it[0], c->stream));
+    for (int i = 0; i < n_iter; ++i) {
+        CK(cudaGraphLaunch(c->graph[c->m_host & 1], c->stream));
+        c->m_host += 1;
+    }
+    CK(cudaEventRecord(c->ev_it[1], c->stream));
+    c->last_launches = c->launches_per_iter * n_iter;
+    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaEventElapsedTime(&c->last_ms, c->ev_it[0], c->ev_it[1]));
+    if (traces) CK(cudaMemcpy(traces, c->d_tr, sizeof(ptyger_trace) * n_iter, cudaMemcpyDeviceToHost));
+    return check_numeric(c);
+}
+
+// full H*W array of a per-rank storage buffer (collective when world > 1)
+static ptyger_status gather_rows(ptyger_ctx* c, const float2* src, float* out) {
+    std::string& err = c->err;
+    CK(cudaSetDevice(c->cfg.device));
+    CK(cudaStreamSynchronize(c->stream));
+    if (c->cfg.world == 1) {
+        CK(cudaMemcpy(out, src, sizeof(float2) * c->H * c->W, cudaMemcpyDeviceToHost));
+        return PTYGER_OK;
+    }
+    const int64_t* R = &c->rows[6 * c->cfg.rank];
+    CK(cudaMemcpyAsync(c->full + R[0] * c->W, src + (R[0] - c->st_lo) * c->W, sizeof(float2) * (R[1] - R[0]) * c->W,
+                       cudaMemcpyDeviceToDevice, c->stream));
+    NK(c->nc->GroupStart());
+    for (int r = 0; r < c->cfg.world; ++r) {
+        const int64_t lo = c->rows[6 * r], hi = c->rows[6 * r + 1];
+        if (hi <= lo) continue;
+        NK(c->nc->Broadcast(c->full + lo * c->W, c->full + lo * c->W, (size_t)((hi - lo) * c->W * 2), ncclFloat32, r,
+                            c->comm, c->stream));
+    }
+    NK(c->nc->GroupEnd());
+    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaMemcpy(out, c->full, sizeof(float2) * c->H * c->W, cudaMemcpyDeviceToHost));
+    return PTYGER_OK;
+}
+
+ptyger_status ptyger_get_object(ptyger_ctx* c, float* out) {
+    if (!c || !out) return set_err(c, PTYGER_E_ARG, "get_object: null pointer");
+    return gather_rows(c, c->psi, out);
+}
+
+ptyger_status ptyger_get_gradient(ptyger_ctx* c, float* out) {
+    if (!c || !out) return set_err(c, PTYGER_E_ARG, "get_gradient: null pointer");
+    if (c->m_host == 0) {
+        std::memset(out, 0, sizeof(float2) * c->H * c->W);
+        return PTYGER_OK;
+    }
+    return gather_rows(c, c->g[(c->m_host - 1) & 1], out);
+}
+
+ptyger_status ptyger_get_farfield(ptyger_ctx* c, float* out) {
+    if (!c || !out) return set_err(c, PTYGER_E_ARG, "get_farfield: null pointer");
+    std::string& err = c->err;
+    CK(cudaSetDevice(c->cfg.device));
+    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaMemcpy(out, c->u, sizeof(float2) * c->geo.n_local * c->N * c->N, cudaMemcpyDeviceToHost));
+    return PTYGER_OK;
+}
+
+ptyger_status ptyger_get_state(ptyger_ctx* c, float* psi, float* g_prev, float* eta_prev, double* F, int32_t* m) {
+    if (!c) return set_err(nullptr, PTYGER_E_ARG, "get_state: ctx is NULL");
+    std::string& err = c->err;
+    ptyger_status s;
+    if (psi && (s = ptyger_get_object(c, psi)) != PTYGER_OK) return s;
+    if (g_prev && (s = ptyger_get_gradient(c, g_prev)) != PTYGER_OK) return s;
+    if (eta_prev && (s = gather_rows(c, c->eta, eta_prev)) != PTYGER_OK) return s;
+    DevState hs;
+    CK(cudaMemcpy(&hs, c->st, sizeof(hs), cudaMemcpyDeviceToHost));
+    if (F) *F = hs.F;
+    if (m) *m = c->m_host;
+    return PTYGER_OK;
+}
+
+ptyger_status ptyger_set_state(ptyger_ctx* c, const float* psi, const float* g_prev, const float* eta_prev,
+                               int32_t m) {
+    if (!c || !psi || m < 0) return set_err(c, PTYGER_E_ARG, "set_state: null ctx/psi or m < 0");
+    if (c->cfg.world != 1) return set_err(c, PTYGER_E_STATE, "set_state: only for world == 1");
+    if (m > 0 && (!g_prev || !eta_prev)) return set_err(c, PTYGER_E_ARG, "set_state: m > 0 needs g_prev and eta_prev");
+    std::string& err = c->err;
+    CK(cudaSetDevice(c->cfg.device));
+    CK(cudaStreamSynchronize(c->stream));
+    const size_t bytes = sizeof(float2) * c->H * c->W;
+    CK(cudaMemcpy(c->psi, psi, bytes, cudaMemcpyDefault));
+    if (m > 0) {
+        CK(cudaMemcpy(c->g[(m - 1) & 1], g_prev, bytes, cudaMemcpyDefault));
+        CK(cudaMemcpy(c->eta, eta_prev, bytes, cudaMemcpyDefault));
+    } else {
+        CK(cudaMemset(c->g[0], 0, bytes));
+        CK(cudaMemset(c->g[1], 0, bytes));
+        CK(cudaMemset(c->eta, 0, bytes));
+    }
+    DevState hs;
+    std::memset(&hs, 0, sizeof(hs));
+    hs.m = m;
+    CK(cudaMemcpy(c->st, &hs, sizeof(hs), cudaMemcpyHostToDevice));
+    c->m_host = m;
+    c->failed_numeric = false;
+    const int rc = run_forward(c, err);
+    return (ptyger_status)rc;
+}
+
+ptyger_status ptyger_get_ls_partials(ptyger_ctx* c, double* dF, int32_t K, int32_t* n_eval) {
+    if (!c || !dF || K < 0) return set_err(c, PTYGER_E_ARG, "get_ls_partials: bad arguments");
+    std::string& err = c->err;
+    CK(cudaStreamSynchronize(c->stream));
+    DevState hs;
+    CK(cudaMemcpy(&hs, c->st, sizeof(hs), cudaMemcpyDeviceToHost));
+    for (int k = 0; k < K; ++k) dF[k] = k < SMAX ? hs.ls_hist[k] : NAN;
+    if (n_eval) *n_eval = hs.n_eval;
+    return PTYGER_OK;
+}
+
+float ptyger_last_iterate_ms(const ptyger_ctx* c) { return c ? c->last_ms : 0.f; }
+
+ptyger_status ptyger_stage_times(ptyger_ctx* c, int32_t n_iter, double* ms) {
+    if (!c || !ms || n_iter < 1) return set_err(c, PTYGER_E_ARG, "stage_times: bad arguments");
+    if (c->failed_numeric) return set_err(c, PTYGER_E_NUMERIC, "context is in a numeric-failure state");
+    std::string& err = c->err;
+    CK(cudaSetDevice(c->cfg.device));
+    cudaEvent_t ev[7];
+    for (int i = 0; i < 7; ++i) CK(cudaEventCreate(&ev[i]));
+    for (int i = 0; i < 7; ++i) ms[i] = 0.0;
+    struct { int idx, cap; } hdr = {0, 0};
+    CK(cudaMemcpyAsync(&c->st->trace_idx, &hdr, sizeof(int) * 2, cudaMemcpyHostToDevice, c->stream));
+    for (int it = 0; it < n_iter; ++it) {
+        int64_t launches = 0;
+        const int rc = enqueue_iteration(c, c->m_host & 1, err, launches, ev);
+        if (rc) return (ptyger_status)rc;
+        c->m_host += 1;
+        CK(cudaStreamSynchronize(c->stream));
+        float t;
+        for (int i = 0; i < 6; ++i) {
+            CK(cudaEventElapsedTime(&t, ev[i], ev[i + 1]));
+            ms[i] += t;
+        }
+        CK(cudaEventElapsedTime(&t, ev[0], ev[6]));
+        ms[6] += t;
+    }
+    for (int i = 0; i < 7; ++i) cudaEventDestroy(ev[i]);
+    return check_numeric(c);
+}
+
+void ptyger_destroy(ptyger_ctx* c) { free_ctx(c); }
+
+}  // extern "C"

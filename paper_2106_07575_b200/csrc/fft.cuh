@@ -1,0 +1,235 @@
+// Shared-memory batched unitary 2-D FFT for detector-sized frames (N = 16..128), sm_100a.
+//
+// F in Eq.1 and F^H in Eq.3, read as the UNITARY DFT
+// (R#1, R#2): X[k] = (1/N) sum_n x[n] exp(-/+ 2 pi i (k.n)/N), DC at [0,0].
+//
+// Decomposition of one length-N line (N = R*T, R = min(N,16)):
+//   x[n], n = T*n1 + n2 (n1 < R, n2 < T);  X[k], k = k1 + R*k2 (k1 < R, k2 < T)
+//   X[k1 + R k2] = sum_{n2} W_T^{n2 k2} [ W_N^{n2 k1} sum_{n1} x[T n1 + n2] W_R^{n1 k1} ]
+// phase 1: thread n2 holds its R strided inputs in registers -> radix-R DFT (radix-4
+//          stages, compile-time twiddles) -> W_N^{n2 k1} twiddle (table in smem, fp64-built)
+// phase 2: exchange through shared memory, each thread takes R/T values of k1 and runs
+//          T-point DFTs over n2.
+// A 2-D transform = a ROW pass (lines = rows; the T threads of a row sit in one warp and
+// exchange in place with an XOR swizzle, __syncwarp only) followed by a COLUMN pass (warp
+// lanes = 32 consecutive columns of one row, so every smem access is conflict-free; the
+// T sub-threads of a column sit in T different warps and exchange through __syncthreads).
+// Frame rows live in smem with stride LD = N + 8 complex so the two rows a half-warp
+// touches in the row pass fall in disjoint bank halves.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace pty {
+
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+// a * b
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+    return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
+// a * conj(b)
+__device__ __forceinline__ float2 cmulc(float2 a, float2 b) {
+    return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -a.x * b.y));
+}
+// conj(a) * b
+__device__ __forceinline__ float2 cconjmul(float2 a, float2 b) {
+    return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.x, b.y, -a.y * b.x));
+}
+
+// cos / sin of 2 pi q / 16 for q in [0, 16) (compile-time after unrolling)
+__host__ __device__ constexpr float cos16_0_8(int q) {
+    return q == 0 ? 1.0f : q == 1 ? 0.92387953251128674f : q == 2 ? 0.70710678118654752f
+         : q == 3 ? 0.38268343236508977f : q == 4 ? 0.0f : q == 5 ? -0.38268343236508977f
+         : q == 6 ? -0.70710678118654752f : q == 7 ? -0.92387953251128674f : -1.0f;
+}
+__host__ __device__ constexpr float sin16_0_8(int q) {
+    return q == 0 ? 0.0f : q == 1 ? 0.38268343236508977f : q == 2 ? 0.70710678118654752f
+         : q == 3 ? 0.92387953251128674f : q == 4 ? 1.0f : q == 5 ? 0.92387953251128674f
+         : q == 6 ? 0.70710678118654752f : q == 7 ? 0.38268343236508977f : 0.0f;
+}
+__host__ __device__ constexpr float cos16(int q) { return q <= 8 ? cos16_0_8(q) : cos16_0_8(16 - q); }
+__host__ __device__ constexpr float sin16(int q) { return q <= 8 ? sin16_0_8(q) : -sin16_0_8(16 - q); }
+
+// x * W_R^m, W_R = exp(-2 pi i / R) (forward) or exp(+2 pi i / R) (INV); R divides 16.
+template <int R, bool INV>
+__device__ __forceinline__ float2 twr(float2 x, int m) {
+    const int q = (m % R) * (16 / R);
+    if (q == 0) return x;
+    if (q == 8) return make_float2(-x.x, -x.y);
+    if (q == 4) return INV ? make_float2(-x.y, x.x) : make_float2(x.y, -x.x);
+    if (q == 12) return INV ? make_float2(x.y, -x.x) : make_float2(-x.y, x.x);
+    const float c = cos16(q);
+    const float s = INV ? sin16(q) : -sin16(q);
+    return make_float2(fmaf(x.x, c, -x.y * s), fmaf(x.x, s, x.y * c));
+}
+
+template <int R, bool INV> struct DFT;
+
+template <bool INV> struct DFT<1, INV> {
+    __device__ __forceinline__ static void run(float2 (&)[1]) {}
+};
+template <bool INV> struct DFT<2, INV> {
+    __device__ __forceinline__ static void run(float2 (&x)[2]) {
+        const float2 t = x[0];
+        x[0] = cadd(t, x[1]);
+        x[1] = csub(t, x[1]);
+    }
+};
+template <bool INV> struct DFT<4, INV> {
+    __device__ __forceinline__ static void run(float2 (&x)[4]) {
+        const float2 t0 = cadd(x[0], x[2]), t1 = csub(x[0], x[2]);
+        const float2 t2 = cadd(x[1], x[3]), t3 = twr<4, INV>(csub(x[1], x[3]), 1);
+        x[0] = cadd(t0, t2);
+        x[2] = csub(t0, t2);
+        x[1] = cadd(t1, t3);
+        x[3] = csub(t1, t3);
+    }
+};
+
+// R = R1*R2 with n = R2*n1 + n2, k = k1 + R1*k2 (same split as the line decomposition).
+template <int R1, int R2, bool INV>
+__device__ __forceinline__ void dft_2level(float2 (&x)[R1 * R2]) {
+    constexpr int R = R1 * R2;
+#pragma unroll
+    for (int n2 = 0; n2 < R2; ++n2) {
+        float2 a[R1];
+#pragma unroll
+        for (int n1 = 0; n1 < R1; ++n1) a[n1] = x[R2 * n1 + n2];
+        DFT<R1, INV>::run(a);
+#pragma unroll
+        for (int k1 = 0; k1 < R1; ++k1) x[R2 * k1 + n2] = twr<R, INV>(a[k1], n2 * k1);
+    }
+    float2 y[R];
+#pragma unroll
+    for (int k1 = 0; k1 < R1; ++k1) {
+        float2 b[R2];
+#pragma unroll
+        for (int n2 = 0; n2 < R2; ++n2) b[n2] = x[R2 * k1 + n2];
+        DFT<R2, INV>::run(b);
+#pragma unroll
+        for (int k2 = 0; k2 < R2; ++k2) y[k1 + R1 * k2] = b[k2];
+    }
+#pragma unroll
+    for (int i = 0; i < R; ++i) x[i] = y[i];
+}
+
+template <bool INV> struct DFT<8, INV> {
+    __device__ __forceinline__ static void run(float2 (&x)[8]) { dft_2level<4, 2, INV>(x); }
+};
+template <bool INV> struct DFT<16, INV> {
+    __device__ __forceinline__ static void run(float2 (&x)[16]) { dft_2level<4, 4, INV>(x); }
+};
+
+// ------------------------------------------------------------------------------------
+// Line FFTs over a frame held in shared memory.
+// ------------------------------------------------------------------------------------
+template <int N>
+struct FFTCfg {
+    static constexpr int R = N < 16 ? N : 16;    // radix of phase 1 (registers)
+    static constexpr int T = N / R;              // threads per line / radix of phase 2
+    static constexpr int LD = N + 8;             // smem row stride (complex), LD % 16 == 8
+    static constexpr int NT = 512;               // threads per CTA
+    static constexpr int FPB = (NT / (N * T)) > 0 ? (NT / (N * T)) : 1;  // frames per CTA step
+    static constexpr int LINES = FPB * N;        // lines per pass
+    static constexpr int LPR = NT / T;           // lines per round
+    static constexpr int ROUNDS = LINES / LPR;   // rounds per pass
+    static constexpr int FRAME_ELEMS = N * LD;
+    static constexpr size_t SMEM_BYTES = (size_t)(FPB * FRAME_ELEMS + N) * sizeof(float2);
+    static_assert(N * T * FPB % NT == 0 || FPB == 1, "bad config");
+    static_assert(LINES % LPR == 0, "bad rounds");
+};
+
+// Twiddle table tw[m] = exp(-2 pi i m / N), built in double precision.
+template <int N>
+__device__ __forceinline__ void build_twiddles(float2* tw) {
+    for (int m = threadIdx.x; m < N; m += blockDim.x) {
+        double s, c;
+        sincospi(2.0 * (double)m / (double)N, &s, &c);
+        tw[m] = make_float2((float)c, (float)(-s));
+    }
+}
+
+template <bool INV>
+__device__ __forceinline__ float2 twmul(float2 x, float2 w) { return INV ? cmulc(x, w) : cmul(x, w); }
+
+// ROW pass for one row: x[n1] = input element at column T*n1 + t.  Leaves the row's DFT
+// (unnormalised) in srow[0..N) in natural order.  The T threads of the row must be
+// consecutive lanes of one warp and all 32 lanes must call this together.
+template <int N, bool INV>
+__device__ __forceinline__ void row_fft(float2 (&x)[FFTCfg<N>::R], float2* srow, int t, const float2* tw) {
+    constexpr int R = FFTCfg<N>::R, T = FFTCfg<N>::T;
+    DFT<R, INV>::run(x);
+    if constexpr (T == 1) {
+#pragma unroll
+        for (int k = 0; k < R; ++k) srow[k] = x[k];
+    } else {
+#pragma unroll
+        for (int k1 = 1; k1 < R; ++k1) x[k1] = twmul<INV>(x[k1], tw[t * k1]);
+#pragma unroll
+        for (int k1 = 0; k1 < R; ++k1) srow[T * k1 + (t ^ (k1 & (T - 1)))] = x[k1];
+        __syncwarp();
+        float2 y[R];
+#pragma unroll
+        for (int j = 0; j < R / T; ++j) {
+            const int k1 = j * T + t;
+#pragma unroll
+            for (int n2 = 0; n2 < T; ++n2) y[j * T + n2] = srow[T * k1 + (n2 ^ t)];
+        }
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < R / T; ++j) {
+            float2 b[T];
+#pragma unroll
+            for (int n2 = 0; n2 < T; ++n2) b[n2] = y[j * T + n2];
+            DFT<T, INV>::run(b);
+            const int k1 = j * T + t;
+#pragma unroll
+            for (int k2 = 0; k2 < T; ++k2) srow[k1 + R * k2] = b[k2];
+        }
+    }
+}
+
+// COLUMN pass phase 1 for column scol (pointer to element [0][c]); sub-thread t.
+// Reads rows T*n1 + t, writes the twiddled radix-R outputs back to rows T*k1 + t.
+template <int N, bool INV>
+__device__ __forceinline__ void col_fft_phase1(float2* scol, int t, const float2* tw) {
+    constexpr int R = FFTCfg<N>::R, T = FFTCfg<N>::T, LD = FFTCfg<N>::LD;
+    float2 x[R];
+#pragma unroll
+    for (int n1 = 0; n1 < R; ++n1) x[n1] = scol[(T * n1 + t) * LD];
+    DFT<R, INV>::run(x);
+    if constexpr (T > 1) {
+#pragma unroll
+        for (int k1 = 1; k1 < R; ++k1) x[k1] = twmul<INV>(x[k1], tw[t * k1]);
+    }
+#pragma unroll
+    for (int k1 = 0; k1 < R; ++k1) scol[(T * k1 + t) * LD] = x[k1];
+}
+
+// COLUMN pass phase 2 (after a block barrier): X[j*T + k2] is output row k1 + R*k2 with
+// k1 = j*T + t.  Results stay in registers (the caller's epilogue consumes them).
+template <int N, bool INV>
+__device__ __forceinline__ void col_fft_phase2(const float2* scol, int t, float2 (&X)[FFTCfg<N>::R]) {
+    constexpr int R = FFTCfg<N>::R, T = FFTCfg<N>::T, LD = FFTCfg<N>::LD;
+#pragma unroll
+    for (int j = 0; j < R / T; ++j) {
+        const int k1 = j * T + t;
+        float2 b[T];
+#pragma unroll
+        for (int n2 = 0; n2 < T; ++n2) b[n2] = scol[(T * k1 + n2) * LD];
+        DFT<T, INV>::run(b);
+#pragma unroll
+        for (int k2 = 0; k2 < T; ++k2) X[j * T + k2] = b[k2];
+    }
+}
+
+template <int N>
+__device__ __forceinline__ int col_out_row(int idx, int t) {
+    constexpr int R = FFTCfg<N>::R, T = FFTCfg<N>::T;
+    const int j = idx / T, k2 = idx % T;
+    return (j * T + t) + R * k2;
+}
+
+}  // namespace pty

@@ -1,0 +1,82 @@
+// Internal declarations shared by the kernels (kernels.cu) and the host runtime (ctx.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "ptyger.h"
+
+namespace pty {
+
+constexpr int KMAX = 32;     // max LS trials per pass
+constexpr int SMAX = 64;     // max trials per iteration (max_shrinks bound)
+constexpr int NDY = 6;       // DY partial sums per tile
+
+// Device-resident scalar state of the iteration (all decisions are taken on the device).
+struct DevState {
+    double F;                // F(psi_m) (cached accepted value, R#11)
+    double gamma;            // gamma of the last accepted step (u <- u + gamma v in k_grad)
+    double alpha_re, alpha_im;
+    double dy[NDY];          // reduced: |g|^2, Re/Im <eta,g-g_prev>, |g_prev|^2, Re/Im <eta,g>
+    double ls_pass[KMAX + 1];// reduced LS partials of the current pass (+ ||eta||^2 slot)
+    double ls_hist[SMAX];    // DeltaF_k of every trial evaluated this iteration
+    double eta2;             // ||eta_m||^2 over owned rows (global after reduction)
+    double F_init_part;      // scratch for k_fwd reductions
+    int m;                   // iteration counter
+    int accepted;            // 1 once a trial was accepted in this iteration
+    int kstar;               // accepted trial index
+    int n_eval;              // trials evaluated this iteration
+    int restarted;
+    int stalled;
+    int numeric_error;       // 0 = ok; else stage code (1 DIR, 2 LS, 3 F)
+    int err_iter;
+    int trace_idx;           // slot of the current iteration in the trace buffer
+    int trace_cap;           // capacity of trace_ptr
+    ptyger_trace* trace_ptr; // device trace buffer of the current ptyger_cg_iterate call
+};
+
+struct Geometry {
+    int N;
+    int64_t W;               // object width (all ranks store full-width rows)
+    int64_t SH;              // storage rows on this rank
+    int64_t own_lo, own_hi;  // owned rows, storage-local coordinates (for reductions)
+    int64_t band_lo0, band_hi0, band_lo1, band_hi1;  // storage-local band rows excluded from k_adj partials
+    int64_t n_local;         // frames stored on this rank
+};
+
+struct SolverCfg {
+    double gamma0, tau, t, eps;
+    int max_shrinks, direction, K;
+};
+
+// -------- kernel launchers (kernels.cu) ------------------------------------------------
+int launch_fft2(const float2* in, float2* out, int N, int64_t batch, bool inverse, cudaStream_t s);
+int launch_fwd(const Geometry& g, const float2* psi, const float2* probe, const int2* pos,
+               const int* order, const float* d, float2* u, double* part, int grid, float eps,
+               cudaStream_t s);
+int launch_grad(const Geometry& g, float2* u, float2* v, const float* d, const float2* probe,
+                const int* order, const DevState* st, float eps, int grid, cudaStream_t s);
+int launch_adj(const Geometry& g, const float2* y, const int* tile_ptr, const int* tile_frames,
+               int ntx, int nty, float2* gcur, const float2* gprev, const float2* eta, double* part,
+               const DevState* st, cudaStream_t s);
+int launch_ls(const Geometry& g, const float2* eta, const float2* probe, const int2* pos,
+              const int* order, const float2* u, float2* v, const float* d, const SolverCfg& c,
+              double* part, int grid, const DevState* st, cudaStream_t s);
+int launch_lsx(const Geometry& g, const float2* u, const float2* v, const float* d,
+               const SolverCfg& c, int pass, double* part, int grid, const DevState* st,
+               cudaStream_t s);
+int launch_reduce(const double* part, int nblocks, int width, double* dst, cudaStream_t s);
+int launch_dir(DevState* st, const SolverCfg& c, cudaStream_t s);
+int launch_eta(const Geometry& g, const float2* gcur, float2* eta, const DevState* st,
+               double* part, int grid, cudaStream_t s);
+int launch_pick(DevState* st, const SolverCfg& c, int pass, int last_pass, cudaStream_t s);
+int launch_upd(const Geometry& g, float2* psi, const float2* eta, const DevState* st, int grid,
+               cudaStream_t s);
+int launch_begin_iter(DevState* st, cudaStream_t s);
+int launch_validate_d(const float* d, int64_t count, int64_t frame_elems, unsigned long long* bad,
+                      cudaStream_t s);
+int launch_set_F(DevState* st, const double* src, cudaStream_t s);
+int launch_band_add(float2* gcur, const float2* recv, int64_t row_lo, int64_t rows, int64_t W,
+                    const float2* gprev, const float2* eta, int64_t own_lo, int64_t own_hi,
+                    double* part, int grid, cudaStream_t s);
+
+}  // namespace pty

@@ -1,0 +1,231 @@
+"""GPU parity of the CUDA path (through the C ABI) against the float64 oracle.
+
+Tolerances:
+  * FFT / u = G psi: rel L2 <= 2e-6 (fp32 radix-16 x radix-T FFT, fp64-built twiddles)
+  * F: rel <= 2e-6 (fp32 per-pixel terms, fp64 sums)
+  * teacher-forced gradient: rel L2 <= max(1e-4, 4 e32), e32 = error of a plain float32
+    NumPy evaluation of the same formula on the same state (oracle.gradient_f32)
+  * LS partials DeltaF_k: |GPU - oracle| <= 1e-5 * sum|terms|; same accepted k unless
+    ambiguous
+  * warm-start 20-iteration trajectory: object rel L2 <= 1e-3, equal shrink sequences
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import ptycho as O  # noqa: E402
+from paper_2106_07575_b200 import inputs as I  # noqa: E402
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(np.asarray(b)), 1e-300))
+
+
+@pytest.fixture(scope="module")
+def L():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2106_07575_b200 import _lib
+    return _lib
+
+
+def problem(H, N, k, step, jitter=0, seed=0, photons=1.0, noisy=False):
+    psi_true = I.make_object(I.siemens_star(H, H))
+    p = I.make_probe(N)
+    scan = I.make_scan(H, H, N, k, step, jitter, seed)
+    mean = photons * np.abs(O.forward_G(psi_true, p, scan)) ** 2
+    d = I.poisson_counts(mean, seed) if noisy else mean
+    return psi_true, p, scan, np.asarray(d, np.float32)
+
+
+FIXTURES = {
+    # name: (H, N, k, step, jitter, seed, photons, noisy)
+    "tiny": (64, 16, 7, 8, 0, 23, 1.0, False),
+    "n32": (96, 32, 9, 8, 1, 3, 1e3, True),        # 81 frames: FPB=8 ragged tail
+    "n64": (192, 64, 9, 16, 2, 4, 1e3, True),      # 81 frames: FPB=2 ragged tail, 36 tiles
+    "n128": (320, 128, 7, 32, 2, 5, 1e3, True),    # 49 frames, 100 tiles
+}
+
+
+def get_fixture(name):
+    H, N, k, step, jit, seed, ph, noisy = FIXTURES[name]
+    return problem(H, N, k, step, jit, seed, ph, noisy)
+
+
+# ------------------------------------------------------------------ FFT library
+
+@pytest.mark.parametrize("N", [16, 32, 64, 128])
+@pytest.mark.parametrize("inverse", [False, True])
+def test_fft2_matches_oracle_and_cufft(L, N, inverse):
+    batch = 37
+    x = I.random_complex((batch, N, N), seed=N)
+    xt = torch.from_numpy(x.astype(np.complex64)).cuda()
+    y = L.fft2(xt, inverse=inverse).cpu().numpy()
+    ref = O.uifft2(x) if inverse else O.ufft2(x)
+    assert rel(y, ref) < 2e-6
+    cu = (torch.fft.ifft2 if inverse else torch.fft.fft2)(xt, norm="ortho").cpu().numpy()
+    assert rel(y, cu) < 2e-6
+    back = L.fft2(L.fft2(xt, inverse=inverse), inverse=not inverse).cpu().numpy()
+    assert rel(back, x) < 3e-6
+
+
+# ------------------------------------------------------------------ forward / objective
+
+@pytest.mark.parametrize("name", list(FIXTURES))
+def test_forward_and_objective(L, name):
+    psi_true, p, scan, d = get_fixture(name)
+    psi0 = np.ones_like(psi_true) * (0.8 + 0.3j) + 0.05 * I.random_complex(psi_true.shape, seed=1)
+    pt = L.Ptyger(psi0, p, scan, d)
+    psi0c = psi0.astype(np.complex64).astype(np.complex128)
+    u_ref = O.forward_G(psi0c, p.astype(np.complex64).astype(np.complex128), scan)
+    assert rel(pt.get_farfield(), u_ref) < 2e-6
+    _, _, _, F, m = pt.get_state()
+    Fref = O.objective_F(u_ref, d.astype(np.float64))
+    assert m == 0 and abs(F - Fref) <= 2e-6 * abs(Fref)
+    pt.close()
+
+
+# ------------------------------------------------------------------ teacher-forced iterations
+
+def c128(a):
+    return np.asarray(a, np.complex64).astype(np.complex128)
+
+
+@pytest.mark.parametrize("name", list(FIXTURES))
+@pytest.mark.parametrize("direction", [0, 2])
+def test_teacher_forced_iterations(L, name, direction):
+    psi_true, p, scan, d = get_fixture(name)
+    d64 = d.astype(np.float64)
+    p64 = c128(p)
+    pt = L.Ptyger(np.ones_like(psi_true), p, scan, d, direction=direction)
+    n_checked_ls = 0
+    for m in range(6):
+        psi_m, g_prev, eta_prev, F_m, mm = pt.get_state()
+        assert mm == m
+        psi64 = c128(psi_m)
+        g_ref, alpha_ref, eta_ref, rs_ref, u_ref = O.grad_at(psi64, c128(g_prev), c128(eta_prev), m, p64, scan, d64,
+                                                            variant=direction)
+        tr = pt.iterate(1)[0]
+        g_gpu = pt.get_gradient()
+        e32 = rel(O.gradient_f32(psi_m, p, scan, d), g_ref)
+        tol = max(1e-4, 4 * e32)
+        assert rel(g_gpu, g_ref) <= tol, (m, rel(g_gpu, g_ref), e32)
+        # alpha (Eq.8) from the oracle's sums on the GPU state
+        if m > 0 and not rs_ref:
+            assert abs(complex(tr["alpha_re"], tr["alpha_im"]) - alpha_ref) <= 1e-3 * abs(alpha_ref) + 1e-12
+        assert tr["iter"] == m
+        # LS partials on the GPU's eta_m (fp64 oracle, difference form)
+        _, _, eta_m, _, _ = pt.get_state()
+        v_ref = O.forward_G(c128(eta_m), p64, scan)
+        dF = pt.get_ls_partials()
+        assert len(dF) == (tr["shrinks"] + 1 if not tr["stalled"] else 32) or len(dF) >= tr["shrinks"] + 1
+        a_terms = np.abs(u_ref) ** 2
+        for k, val in enumerate(dF):
+            gk = 0.5 ** k
+            ref = O.ls_delta(u_ref, v_ref, d64, gk)
+            scale = np.sum(np.abs(u_ref + gk * v_ref) ** 2) + np.sum(a_terms) + 2 * np.sum(np.abs(d64 * np.log(np.maximum(np.abs(u_ref), 1e-30))))
+            assert abs(val - ref) <= 1e-5 * scale, (m, k, val, ref, scale)
+            n_checked_ls += 1
+        # decision: first k with DeltaF_k <= 0 (t = 0), unless ambiguous
+        refs = [O.ls_delta(u_ref, v_ref, d64, 0.5 ** k) for k in range(len(dF))]
+        kref = next((k for k, r in enumerate(refs) if r <= 0), None)
+        if kref is not None and not tr["stalled"]:
+            margins = [abs(r) for r in refs[:kref + 1]]
+            scale = np.sum(np.abs(u_ref) ** 2) + np.sum(d64)
+            if min(margins) > 1e-5 * scale:
+                assert tr["shrinks"] == kref
+        assert np.isfinite(tr["F"]) and tr["gamma"] in [0.5 ** k for k in range(32)] + [0.0]
+    assert n_checked_ls > 0
+    pt.close()
+
+
+# ------------------------------------------------------------------ trajectories
+
+def test_warm_start_trajectory_tiny(L):
+    psi_true, p, scan, d = get_fixture("tiny")
+    d64 = d.astype(np.float64)
+    st, _ = O.run_cg(np.ones_like(psi_true), c128(p), scan, d64, 100)
+    psi_w = c128(st.psi)
+    ost, otr = O.run_cg(psi_w, c128(p), scan, d64, 20)
+    pt = L.Ptyger(psi_w, p, scan, d)
+    gtr = pt.iterate(20)
+    assert [t["shrinks"] for t in gtr] == [t.shrinks for t in otr]
+    assert rel(pt.get_object(), ost.psi) <= 1e-3
+    F = [t["F"] for t in gtr]
+    assert all(F[i + 1] <= F[i] for i in range(len(F) - 1))
+    pt.close()
+
+
+def test_monotone_and_deterministic(L):
+    psi_true, p, scan, d = get_fixture("n64")
+    outs = []
+    for _ in range(2):
+        pt = L.Ptyger(np.ones_like(psi_true), p, scan, d)
+        tr = pt.iterate(12)
+        F = [t["F"] for t in tr]
+        assert all(F[i + 1] <= F[i] for i in range(len(F) - 1))
+        outs.append((pt.get_object(), [t["F"] for t in tr]))
+        pt.close()
+    assert np.array_equal(outs[0][0], outs[1][0]) and outs[0][1] == outs[1][1]   # bitwise reproducible
+
+
+# ------------------------------------------------------------------ degenerate cases
+
+def test_d_zero_gradient_closed_form(L):
+    psi_true, p, scan, d = get_fixture("n64")
+    x = (0.9 + 0.2j) * np.ones_like(psi_true)
+    pt = L.Ptyger(x, p, scan, np.zeros_like(d))
+    pt.iterate(1)
+    Ill = O.illumination(c128(p), scan, x.shape)
+    assert rel(pt.get_gradient(), Ill * c128(x)) < 2e-6
+    pt.close()
+
+
+def test_stationary_at_noiseless_truth(L):
+    psi_true, p, scan, _ = get_fixture("n64")
+    d = np.abs(O.forward_G(c128(psi_true), c128(p), scan)) ** 2
+    pt = L.Ptyger(psi_true, p, scan, d.astype(np.float32))
+    tr = pt.iterate(1)[0]
+    g = pt.get_gradient()
+    assert np.linalg.norm(g) <= 1e-4 * np.linalg.norm(O.illumination(c128(p), scan, psi_true.shape) * psi_true)
+    assert tr["gamma"] == 1.0
+    pt.close()
+
+
+def test_stall_then_restart(L):
+    """t = -1e30: no trial can satisfy Eq.7 -> gamma = 0, stalled; the next iteration sees
+    g == g_prev bitwise, so <eta, g - g_prev> = 0 and DY restarts (R#9)."""
+    psi_true, p, scan, d = get_fixture("tiny")
+    pt = L.Ptyger(np.ones_like(psi_true), p, scan, d, t=-1e30)
+    tr = pt.iterate(2)
+    assert tr[0]["stalled"] == 1 and tr[0]["gamma"] == 0.0 and tr[0]["shrinks"] == 32
+    assert tr[1]["stalled"] == 1 and tr[1]["restarted"] == 1
+    assert np.array_equal(pt.get_object(), np.ones_like(psi_true).astype(np.complex64))
+    pt.close()
+
+
+def test_bad_data_is_rejected(L):
+    psi_true, p, scan, d = get_fixture("tiny")
+    d = d.copy()
+    d[13, 2, 3] = -1.0
+    with pytest.raises(L.PtygerError) as ei:
+        L.Ptyger(psi_true, p, scan, d)
+    assert ei.value.status == 3 and "frame 13" in str(ei.value)
+    d[13, 2, 3] = np.nan
+    with pytest.raises(L.PtygerError):
+        L.Ptyger(psi_true, p, scan, d)
+
+
+def test_single_frame_and_device_inputs(L):
+    """n = 1 (degenerate scan) and device-resident inputs through the same C ABI."""
+    psi_true, p, scan, d = get_fixture("n128")
+    sc = scan[:1].copy()
+    dd = d[:1]
+    pt = L.Ptyger(torch.from_numpy(np.ones_like(psi_true).astype(np.complex64)).cuda(),
+                  torch.from_numpy(p.astype(np.complex64)).cuda(), sc, torch.from_numpy(dd).cuda())
+    tr = pt.iterate(2)
+    g_ref, _ = O.gradient(np.ones_like(psi_true), c128(p), sc, dd.astype(np.float64))
+    assert tr[0]["iter"] == 0 and np.isfinite(tr[1]["F"])
+    pt.close()
