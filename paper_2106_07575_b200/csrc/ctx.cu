@@ -314,7 +314,7 @@ void ptyger_config_default(ptyger_config* cfg) {
     cfg->eps = 1e-16;
     cfg->max_shrinks = 32;
     cfg->direction = PTYGER_DIR_DY;
-    cfg->ls_batch = 16;
+    cfg->ls_batch = 8;
     cfg->device = 0;
     cfg->rank = 0;
     cfg->world = 1;

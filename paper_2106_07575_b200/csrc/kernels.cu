@@ -70,35 +70,70 @@ __device__ __forceinline__ double warp_reduce_scatter(double (&v)[K], int lane) 
     return r;
 }
 
-// Accurate float log1p (|rel err| ~ 3 ulp) for z > -1: w = 1 + z rounded, the rounding
-// error delta = z - (w - 1) restores the lost low bits, log(w) by exponent split and the
-// atanh series in s = (m - 1)/(m + 1), |s| <= 0.1716.
-__device__ __forceinline__ float log1p_acc(float z) {
+// Accurate, branch-free float log1p for z > -1 (max rel err 1.4e-7 measured in fp32 over the
+// reduced range): w = 1 + z = m 2^e with m in [sqrt(1/2), sqrt(2)); when e = 0 the polynomial is
+// evaluated on z itself (no rounding of 1 + z is ever used), otherwise on m - 1 (the rounding
+// of 1 + z is then below 2e-7 of the result).  log1p(x) = x + x^2 P(x), P a degree-8 Chebyshev
+// fit on [sqrt(1/2)-1, sqrt(2)-1] (fp64 fit, coefficients rounded to fp32).  No MUFU, no branch.
+__device__ __forceinline__ float log1p_poly(float z) {
     const float w = 1.0f + z;
-    const float delta = z - (w - 1.0f);
     const int iw = __float_as_int(w);
     const int e = (iw - 0x3f3504f3) >> 23;
     const float m = __int_as_float(iw - (e << 23));
-    const float s = __fdividef(m - 1.0f, m + 1.0f);
-    const float s2 = s * s;
-    const float p = s2 * fmaf(s2, fmaf(s2, fmaf(s2, 0.11111111f, 0.14285715f), 0.2f), 0.33333334f);
-    const float lm = 2.0f * fmaf(s, p, s);
-    const float corr = __fdividef(delta, w);
-    return fmaf((float)e, 0.693147182464599609375f, lm + corr) + (float)e * -1.904654323148236e-09f;
+    const float x = (e == 0) ? z : (m - 1.0f);
+    float P = -0.07764425f;
+    P = fmaf(P, x, 0.12656558f);
+    P = fmaf(P, x, -0.13065042f);
+    P = fmaf(P, x, 0.14209557f);
+    P = fmaf(P, x, -0.1663307f);
+    P = fmaf(P, x, 0.20001242f);
+    P = fmaf(P, x, -0.25000605f);
+    P = fmaf(P, x, 0.33333328f);
+    P = fmaf(P, x, -0.49999997f);
+    const float ef = __int_as_float(e + 0x4B400000) - 12582912.0f;   // (float)e on the FMA pipe
+    return fmaf(ef, 0.693147182464599609375f, fmaf(x * x, P, x));
 }
 
-// Per-pixel LS term  F_pixel(u + gamma v) - F_pixel(u)  (difference form of Eq.2 along eta,
-// oracle ls_delta):  q - d log1p(q / c),  q = gamma (a + gamma b),  with the guarded
-// definition where |u| or |u + gamma v| < eps (R#4).
-__device__ __forceinline__ float ls_term(float a, float b, float c, float rc, float dd, float gam,
-                                         float eps2, bool okc) {
+// Guarded definition of the per-pixel LS term (R#4): used only when |u| < eps or
+// |u + gamma v| < eps or 1 + z underflows (warp-uniform slow path).
+__device__ __noinline__ float ls_term_slow(float a, float b, float c, float dd, float gam, float eps2) {
     const float q = gam * fmaf(gam, b, a);
     const float cn = c + q;
-    const float z = q * rc;
-    if (okc && cn >= eps2 && z > -0.999999f) {
-        return fmaf(-dd, log1p_acc(z), q);
+    if (c >= eps2 && cn >= eps2) {
+        const float z = q / c;
+        if (z > -0.999f) return fmaf(-dd, log1p_poly(z), q);
     }
     return (cn - c) - dd * (logf(fmaxf(cn, eps2)) - logf(fmaxf(c, eps2)));
+}
+
+// Per-pixel difference-form LS terms for K trials (oracle ls_delta):  t_k = q_k - d log1p(q_k/c),
+// q_k = gamma_k (a + gamma_k b), a = 2 Re(u* v), b = |v|^2, c = |u|^2.  Branch-free fast path;
+// any lane needing the guarded definition sends its warp through ls_term_slow.
+template <int K>
+__device__ __forceinline__ void ls_terms(float2 uu, float2 vv, float dd, const float* sgam, float eps2,
+                                         float (&acc)[K]) {
+    const float a = 2.0f * fmaf(uu.x, vv.x, uu.y * vv.y);
+    const float b = fmaf(vv.x, vv.x, vv.y * vv.y);
+    const float c = fmaf(uu.x, uu.x, uu.y * uu.y);
+    bool bad = !(c >= eps2);
+    const float rc = bad ? 0.0f : 1.0f / c;
+    float t[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const float gam = sgam[k];
+        const float q = gam * fmaf(gam, b, a);
+        const float z = q * rc;
+        bad |= (c + q < eps2) | (z <= -0.999f);
+        t[k] = fmaf(-dd, log1p_poly(fmaxf(z, -0.5f)), q);
+    }
+    if (__any_sync(__activemask(), bad)) {
+        if (bad) {
+#pragma unroll 1
+            for (int k = 0; k < K; ++k) t[k] = ls_term_slow(a, b, c, dd, sgam[k], eps2);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) acc[k] += t[k];
 }
 
 __device__ __forceinline__ float2 ldg2(const float2* p) { return __ldg(p); }
@@ -647,15 +682,7 @@ __global__ void __launch_bounds__(512, 1) k_ls(Geometry g, const float2* __restr
                     const int64_t o = j * N * N + (int64_t)k * N + c;
                     const float2 vv = cscale(X[q], scale);
                     v[o] = vv;
-                    const float2 uu = u[o];
-                    const float dd = __ldg(d + o);
-                    const float a = 2.0f * (uu.x * vv.x + uu.y * vv.y);
-                    const float b = vv.x * vv.x + vv.y * vv.y;
-                    const float cc = uu.x * uu.x + uu.y * uu.y;
-                    const bool okc = cc >= eps2;
-                    const float rc = okc ? 1.0f / cc : 0.0f;
-#pragma unroll
-                    for (int kk = 0; kk < K; ++kk) acc[kk] += ls_term(a, b, cc, rc, dd, sgam[kk], eps2, okc);
+                    ls_terms<K>(u[o], vv, __ldg(d + o), sgam, eps2, acc);
                 }
             }
             double dv[K];
@@ -698,15 +725,7 @@ __global__ void __launch_bounds__(256) k_lsx(int64_t count, const float2* __rest
     if (!skip) {
         int cnt = 0;
         for (int64_t o = (int64_t)blockIdx.x * blockDim.x + tid; o < count; o += (int64_t)gridDim.x * blockDim.x) {
-            const float2 uu = u[o], vv = v[o];
-            const float dd = __ldg(d + o);
-            const float a = 2.0f * (uu.x * vv.x + uu.y * vv.y);
-            const float b = vv.x * vv.x + vv.y * vv.y;
-            const float cc = uu.x * uu.x + uu.y * uu.y;
-            const bool okc = cc >= eps2;
-            const float rc = okc ? 1.0f / cc : 0.0f;
-#pragma unroll
-            for (int kk = 0; kk < K; ++kk) acc[kk] += ls_term(a, b, cc, rc, dd, sgam[kk], eps2, okc);
+            ls_terms<K>(u[o], v[o], __ldg(d + o), sgam, eps2, acc);
             if (++cnt == 16) {  // bounded fp32 run length, then fp64
 #pragma unroll
                 for (int k = 0; k < K; ++k) { acc64[k] += (double)acc[k]; acc[k] = 0.f; }
