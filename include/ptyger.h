@@ -141,9 +141,11 @@ ptyger_status ptyger_set_state(ptyger_ctx* ctx, const float* psi, const float* g
                                const float* eta_prev, int32_t m);
 
 /* DeltaF_k = F(psi + gamma_k eta) - F(psi) for the trials k = 0..K-1 the last iteration's
- * line search evaluated (difference form); entries beyond the evaluated
- * trials are NaN.  Returns the number evaluated in *n_eval (nullable). */
-ptyger_status ptyger_get_ls_partials(ptyger_ctx* ctx, double* dF, int32_t K, int32_t* n_eval);
+ * line search evaluated (difference form), and (bound, nullable) the error bound
+ * of each value: > 0 for a screened value (MUFU log2, decision certified outside the bound),
+ * 0 for an exact re-evaluation (accurate log1p).  Entries beyond the evaluated trials are NaN.
+ * Returns the number evaluated in *n_eval (nullable). */
+ptyger_status ptyger_get_ls_partials(ptyger_ctx* ctx, double* dF, double* bound, int32_t K, int32_t* n_eval);
 
 /* Host-only helpers (no GPU needed) --------------------------------------------------- */
 

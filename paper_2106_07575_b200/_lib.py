@@ -53,7 +53,7 @@ def _load():
         "ptyger_get_farfield": (I32, [P, P]),
         "ptyger_get_state": (I32, [P, P, P, P, P, P]),
         "ptyger_set_state": (I32, [P, P, P, P, I32]),
-        "ptyger_get_ls_partials": (I32, [P, P, I32, P]),
+        "ptyger_get_ls_partials": (I32, [P, P, P, I32, P]),
         "ptyger_partition": (I32, [P, I64, I64, I32, I32, P, P]),
         "ptyger_round_positions": (I32, [P, I64, P]),
         "ptyger_fft2": (I32, [P, P, I32, I64, I32, P]),
@@ -229,11 +229,12 @@ class Ptyger:
         _check(lib.ptyger_set_state(self.ctx, a.ctypes.data, None if b is None else b.ctypes.data,
                                     None if c is None else c.ctypes.data, m), self.ctx)
 
-    def get_ls_partials(self, K: int = 64):
+    def get_ls_partials(self, K: int = 64, with_bound: bool = False):
         out = np.empty(K, np.float64)
+        bnd = np.empty(K, np.float64)
         ne = C.c_int32()
-        _check(lib.ptyger_get_ls_partials(self.ctx, out.ctypes.data, K, C.byref(ne)), self.ctx)
-        return out[:ne.value]
+        _check(lib.ptyger_get_ls_partials(self.ctx, out.ctypes.data, bnd.ctypes.data, K, C.byref(ne)), self.ctx)
+        return (out[:ne.value], bnd[:ne.value]) if with_bound else out[:ne.value]
 
     def last_iterate_ms(self) -> float:
         return float(lib.ptyger_last_iterate_ms(self.ctx))

@@ -220,21 +220,30 @@ static int enqueue_iteration(ptyger_ctx* c, int p, std::string& err, int64_t& la
     // DIR stage (Alg.1 651-656)
     LK(launch_dir(c->st, sc, s)); ++launches;
     LK(launch_eta(g, gcur, c->eta, c->st, c->part_el, c->grid_el, s)); ++launches;
-    LK(launch_reduce(c->part_el, c->grid_el, 1, &c->st->ls_pass[KMAX], s)); ++launches;
+    LK(launch_reduce(c->part_el, c->grid_el, 1, &c->st->ls_pass[LS_ETA], s)); ++launches;
     EV(4);
-    // LS stage (Alg.1 659-668): first pass computes v = G eta and K trials
+    // LS stage (Alg.1 659-668).  Pass 0 computes v = G eta and screens trials 0..K-1; every pass
+    // is followed by an exact re-evaluation that runs only when the screening left it undecided;
+    // further passes (trials pK..pK+K-1) run only while nothing was accepted.
     LK(launch_ls(g, c->eta, c->probe, c->pos, c->order, c->u, c->v, c->d, sc, c->part_fr, c->grid_fr, c->st, s));
     ++launches;
     EV(5);
-    LK(launch_reduce(c->part_fr, c->grid_fr, sc.K, &c->st->ls_pass[0], s)); ++launches;
     const int npass = (sc.max_shrinks + sc.K - 1) / sc.K;
-    if (multi) NK(c->nc->AllReduce(&c->st->ls_pass[0], &c->st->ls_pass[0], KMAX + 1, ncclFloat64, ncclSum, c->comm, s));
-    LK(launch_pick(c->st, sc, 0, npass == 1, s)); ++launches;
-    for (int pass = 1; pass < npass; ++pass) {
-        LK(launch_lsx(g, c->u, c->v, c->d, sc, pass, c->part_el, c->grid_el, c->st, s)); ++launches;
+    const int wscreen = 2 * sc.K + 3;
+    for (int pass = 0; pass < npass; ++pass) {
+        if (pass > 0) {
+            LK(launch_lsx(g, c->u, c->v, c->d, sc, pass, false, c->part_el, c->grid_el, c->st, s));
+            ++launches;
+        }
+        LK(launch_reduce(pass == 0 ? c->part_fr : c->part_el, pass == 0 ? c->grid_fr : c->grid_el, wscreen,
+                         &c->st->ls_pass[0], s));
+        ++launches;
+        if (multi) NK(c->nc->AllReduce(&c->st->ls_pass[0], &c->st->ls_pass[0], LSW, ncclFloat64, ncclSum, c->comm, s));
+        LK(launch_pick(c->st, sc, pass, 0, 0, s)); ++launches;
+        LK(launch_lsx(g, c->u, c->v, c->d, sc, pass, true, c->part_el, c->grid_el, c->st, s)); ++launches;
         LK(launch_reduce(c->part_el, c->grid_el, sc.K, &c->st->ls_pass[0], s)); ++launches;
         if (multi) NK(c->nc->AllReduce(&c->st->ls_pass[0], &c->st->ls_pass[0], sc.K, ncclFloat64, ncclSum, c->comm, s));
-        LK(launch_pick(c->st, sc, pass, pass == npass - 1, s)); ++launches;
+        LK(launch_pick(c->st, sc, pass, 1, pass == npass - 1, s)); ++launches;
     }
     // Update stage (Alg.1 672)
     LK(launch_upd(g, c->psi, c->eta, c->st, c->grid_el, s)); ++launches;
@@ -474,8 +483,8 @@ static ptyger_status init_impl(ptyger_ctx* c, const float* object, const float* 
     c->grid_el = c->sms * 8;
     c->band_grid = c->sms * 2;
     AL(c->part_adj, double, ((int64_t)c->ntx * c->nty + 2 * c->band_grid) * NDY);
-    AL(c->part_fr, double, (int64_t)c->grid_fr * KMAX);
-    AL(c->part_el, double, (int64_t)c->grid_el * KMAX);
+    AL(c->part_fr, double, (int64_t)c->grid_fr * LSW);
+    AL(c->part_el, double, (int64_t)c->grid_el * LSW);
     AL(c->scratch, double, 64);
     AL(c->st, DevState, 1);
     for (int b = 0; b < 2; ++b)
@@ -716,13 +725,16 @@ ptyger_status ptyger_set_state(ptyger_ctx* c, const float* psi, const float* g_p
     return (ptyger_status)rc;
 }
 
-ptyger_status ptyger_get_ls_partials(ptyger_ctx* c, double* dF, int32_t K, int32_t* n_eval) {
+ptyger_status ptyger_get_ls_partials(ptyger_ctx* c, double* dF, double* bound, int32_t K, int32_t* n_eval) {
     if (!c || !dF || K < 0) return set_err(c, PTYGER_E_ARG, "get_ls_partials: bad arguments");
     std::string& err = c->err;
     CK(cudaStreamSynchronize(c->stream));
     DevState hs;
     CK(cudaMemcpy(&hs, c->st, sizeof(hs), cudaMemcpyDeviceToHost));
-    for (int k = 0; k < K; ++k) dF[k] = k < SMAX ? hs.ls_hist[k] : NAN;
+    for (int k = 0; k < K; ++k) {
+        dF[k] = k < SMAX ? hs.ls_hist[k] : NAN;
+        if (bound) bound[k] = k < SMAX ? hs.ls_bnd[k] : NAN;
+    }
     if (n_eval) *n_eval = hs.n_eval;
     return PTYGER_OK;
 }

@@ -1,0 +1,191 @@
+// Device helpers shared by the libptyger kernels: reductions, the Poisson residual and the
+// line-search (LS) pixel terms.
+#pragma once
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "fft.cuh"
+#include "internal.h"
+
+namespace pty {
+
+#define FULLMASK 0xffffffffu
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) v += __shfl_xor_sync(FULLMASK, v, m);
+    return v;
+}
+
+// Block sum in fixed order (deterministic).  All threads must call; result valid in thread 0.
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double* sred) {
+    v = warp_sum(v);
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __syncthreads();
+    if (lane == 0) sred[w] = v;
+    __syncthreads();
+    double s = 0.0;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NT / 32; ++i) s += sred[i];
+    }
+    return s;
+}
+
+template <int K>
+struct Log2 {
+    static constexpr int value = (K <= 1) ? 0 : 1 + Log2<K / 2>::value;
+};
+template <>
+struct Log2<1> {
+    static constexpr int value = 0;
+};
+
+// Warp reduce-scatter of K (power of two <= 32) per-lane values: afterwards every lane holds
+// the warp total of entry  lane >> (5 - log2 K).
+template <int K>
+__device__ __forceinline__ double warp_reduce_scatter(double (&v)[K], int lane) {
+    constexpr int P = Log2<K>::value;
+#pragma unroll
+    for (int s = 0; s < P; ++s) {
+        const int h = K >> (s + 1);
+        const int m = 16 >> s;
+        const bool upper = (lane & m) != 0;
+#pragma unroll
+        for (int i = 0; i < h; ++i) {
+            const double send = upper ? v[i] : v[i + h];
+            const double keep = upper ? v[i + h] : v[i];
+            v[i] = keep + __shfl_xor_sync(FULLMASK, send, m);
+        }
+    }
+    double r = v[0];
+#pragma unroll
+    for (int m = (32 >> P) >> 1; m >= 1; m >>= 1) r += __shfl_xor_sync(FULLMASK, r, m);
+    return r;
+}
+
+__device__ __forceinline__ float2 ldg2(const float2* p) { return __ldg(p); }
+
+// gamma_k = gamma0 tau^k by repeated multiplication in double: exactly the trial sequence of
+// Eq.7's backtracking (gamma <- gamma tau, Alg.1 662) and of the oracle's line_search.
+__device__ __forceinline__ double trial_gamma(double gamma0, double tau, int k) {
+    double g = gamma0;
+    for (int i = 0; i < k; ++i) g *= tau;
+    return g;
+}
+
+// Residual of Eq.3: u - d/u^* = u - d u / |u|^2, quotient dropped where |u| < eps (R#4).
+__device__ __forceinline__ float2 residual(float2 u, float dd, float eps2) {
+    const float c = u.x * u.x + u.y * u.y;
+    if (c >= eps2) {
+        const float s = dd / c;
+        return make_float2(u.x - s * u.x, u.y - s * u.y);
+    }
+    return u;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Line search pixel terms.  With u = G psi, v = G eta (Eq.1 linearity) the change of the Eq.2
+// objective along eta at trial gamma is, per detector pixel,
+//     t(gamma) = |u + gamma v|^2 - |u|^2 - d log(|u + gamma v|^2 / |u|^2)
+//              = q - d log w,   q = gamma (a + gamma b),  w = |u + gamma v|^2 / |u|^2,
+// a = 2 Re(u^* v), b = |v|^2, c = |u|^2 (oracle ls_delta).  Logs are guarded (R#4).
+// ---------------------------------------------------------------------------------------------
+
+// Accurate, branch-free float log1p for z > -1 (max rel err 1.7e-7 measured in fp32):
+// w = 1 + z = m 2^e with m in [sqrt(1/2), sqrt(2)); the polynomial runs on z itself when e = 0
+// (so the rounding of 1 + z is never used there), otherwise on m - 1.  log1p(x) = x + x^2 P(x),
+// P a degree-8 Chebyshev fit on [sqrt(1/2)-1, sqrt(2)-1].  No MUFU, no branch.
+__device__ __forceinline__ float log1p_poly(float z) {
+    const float w = 1.0f + z;
+    const int iw = __float_as_int(w);
+    const int e = (iw - 0x3f3504f3) >> 23;
+    const float m = __int_as_float(iw - (e << 23));
+    const float x = (e == 0) ? z : (m - 1.0f);
+    float P = -0.07764425f;
+    P = fmaf(P, x, 0.12656558f);
+    P = fmaf(P, x, -0.13065042f);
+    P = fmaf(P, x, 0.14209557f);
+    P = fmaf(P, x, -0.1663307f);
+    P = fmaf(P, x, 0.20001242f);
+    P = fmaf(P, x, -0.25000605f);
+    P = fmaf(P, x, 0.33333328f);
+    P = fmaf(P, x, -0.49999997f);
+    const float ef = __int_as_float(e + 0x4B400000) - 12582912.0f;  // (float)e on the FMA pipe
+    return fmaf(ef, 0.693147182464599609375f, fmaf(x * x, P, x));
+}
+
+// Guarded exact definition, used where |u| < eps or |u + gamma v| < eps or 1 + z underflows.
+static __device__ __noinline__ float ls_term_slow(float a, float b, float c, float dd, float gam, float eps2) {
+    const float q = gam * fmaf(gam, b, a);
+    const float cn = c + q;
+    if (c >= eps2 && cn >= eps2) {
+        const float z = q / c;
+        if (z > -0.999f) return fmaf(-dd, log1p_poly(z), q);
+    }
+    return (cn - c) - dd * (logf(fmaxf(cn, eps2)) - logf(fmaxf(c, eps2)));
+}
+
+// EXACT terms (accurate log1p, ~1.7e-7 relative): t_k = q_k - d log1p(q_k / c).  Branch-free
+// fast path; a lane needing the guarded definition sends its warp through ls_term_slow.
+template <int K>
+__device__ __forceinline__ void ls_exact(float2 uu, float2 vv, float dd, const float* sgam, float eps2,
+                                         float (&acc)[K]) {
+    const float a = 2.0f * fmaf(uu.x, vv.x, uu.y * vv.y);
+    const float b = fmaf(vv.x, vv.x, vv.y * vv.y);
+    const float c = fmaf(uu.x, uu.x, uu.y * uu.y);
+    bool bad = !(c >= eps2);
+    const float rc = bad ? 0.0f : 1.0f / c;
+    float t[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const float gam = sgam[k];
+        const float q = gam * fmaf(gam, b, a);
+        const float z = q * rc;
+        bad |= (c + q < eps2) | (z <= -0.999f);
+        t[k] = fmaf(-dd, log1p_poly(fmaxf(z, -0.999f)), q);
+    }
+    if (__any_sync(__activemask(), bad)) {
+        if (bad) {
+#pragma unroll 1
+            for (int k = 0; k < K; ++k) t[k] = ls_term_slow(a, b, c, dd, sgam[k], eps2);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) acc[k] += t[k];
+}
+
+// SCREENING terms: w from the components of u + gamma v (relative error a few ulp even when
+// u + gamma v nearly cancels), log2 w on the MUFU (|abs err| <= 2^-22 on [0.5, 2], 2 ulp
+// relative elsewhere).  Accumulates S_k = sum t_k and A_k = sum d |ln w_k|; the caller also
+// accumulates sum d, sum |a|, sum b, which bound the error:
+//     |S_k - t_exact| <= LS_EPS_D sum d + LS_EPS_R (A_k + gamma_k sum|a| + gamma_k^2 sum b).
+// |u| < eps makes w = 0 -> S non-finite -> the exact pass decides (guarded definition).
+constexpr double LS_EPS_D = 1e-6;
+constexpr double LS_EPS_R = 2e-6;
+
+template <int K>
+__device__ __forceinline__ void ls_screen(float2 uu, float2 vv, float dd, const float* sgam, float eps2,
+                                          float (&S)[K], float (&A)[K], float& sd, float& sa, float& sb) {
+    const float a = 2.0f * fmaf(uu.x, vv.x, uu.y * vv.y);
+    const float b = fmaf(vv.x, vv.x, vv.y * vv.y);
+    const float c = fmaf(uu.x, uu.x, uu.y * uu.y);
+    const float rc = (c >= eps2) ? 1.0f / c : 0.0f;
+    const float dl = dd * 0.693147182464599609375f;
+    sd += dd;
+    sa += fabsf(a);
+    sb += b;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const float gam = sgam[k];
+        const float q = gam * fmaf(gam, b, a);
+        const float ex = fmaf(gam, vv.x, uu.x), ey = fmaf(gam, vv.y, uu.y);
+        const float cn = fmaxf(fmaf(ex, ex, ey * ey), eps2);
+        const float L2 = __log2f(cn * rc);
+        S[k] += fmaf(-dl, L2, q);
+        A[k] = fmaf(dl, fabsf(L2), A[k]);
+    }
+}
+
+}  // namespace pty

@@ -10,6 +10,8 @@ namespace pty {
 constexpr int KMAX = 32;     // max LS trials per pass
 constexpr int SMAX = 64;     // max trials per iteration (max_shrinks bound)
 constexpr int NDY = 6;       // DY partial sums per tile
+constexpr int LSW = 2 * KMAX + 8;  // LS partial vector: [S | A | sum d, sum|a|, sum b], eta^2 at LS_ETA
+constexpr int LS_ETA = LSW - 1;
 
 // Device-resident scalar state of the iteration (all decisions are taken on the device).
 struct DevState {
@@ -17,8 +19,9 @@ struct DevState {
     double gamma;            // gamma of the last accepted step (u <- u + gamma v in k_grad)
     double alpha_re, alpha_im;
     double dy[NDY];          // reduced: |g|^2, Re/Im <eta,g-g_prev>, |g_prev|^2, Re/Im <eta,g>
-    double ls_pass[KMAX + 1];// reduced LS partials of the current pass (+ ||eta||^2 slot)
+    double ls_pass[LSW];     // reduced LS partials of the current pass (+ ||eta||^2 at LS_ETA)
     double ls_hist[SMAX];    // DeltaF_k of every trial evaluated this iteration
+    double ls_bnd[SMAX];     // error bound of ls_hist (0 = exact evaluation)
     double eta2;             // ||eta_m||^2 over owned rows (global after reduction)
     double F_init_part;      // scratch for k_fwd reductions
     int m;                   // iteration counter
@@ -29,6 +32,9 @@ struct DevState {
     int stalled;
     int numeric_error;       // 0 = ok; else stage code (1 DIR, 2 LS, 3 F)
     int err_iter;
+    int need_exact;          // pass + 1 when the screening pick left that pass undecided
+    int k_unc;               // first undecided trial
+    int n_exact;             // exact re-evaluations so far (diagnostic)
     int trace_idx;           // slot of the current iteration in the trace buffer
     int trace_cap;           // capacity of trace_ptr
     ptyger_trace* trace_ptr; // device trace buffer of the current ptyger_cg_iterate call
@@ -62,13 +68,13 @@ int launch_ls(const Geometry& g, const float2* eta, const float2* probe, const i
               const int* order, const float2* u, float2* v, const float* d, const SolverCfg& c,
               double* part, int grid, const DevState* st, cudaStream_t s);
 int launch_lsx(const Geometry& g, const float2* u, const float2* v, const float* d,
-               const SolverCfg& c, int pass, double* part, int grid, const DevState* st,
+               const SolverCfg& c, int pass, bool exact, double* part, int grid, const DevState* st,
                cudaStream_t s);
 int launch_reduce(const double* part, int nblocks, int width, double* dst, cudaStream_t s);
 int launch_dir(DevState* st, const SolverCfg& c, cudaStream_t s);
 int launch_eta(const Geometry& g, const float2* gcur, float2* eta, const DevState* st,
                double* part, int grid, cudaStream_t s);
-int launch_pick(DevState* st, const SolverCfg& c, int pass, int last_pass, cudaStream_t s);
+int launch_pick(DevState* st, const SolverCfg& c, int pass, int exact_mode, int last_pass, cudaStream_t s);
 int launch_upd(const Geometry& g, float2* psi, const float2* eta, const DevState* st, int grid,
                cudaStream_t s);
 int launch_begin_iter(DevState* st, cudaStream_t s);

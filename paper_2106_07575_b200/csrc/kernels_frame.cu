@@ -1,0 +1,392 @@
+// sm_100a kernels of one ML-CG iteration (PAPER.md:462-471 four stages GRAD / DIR / LS /
+// Update; Alg.1).  Design S: the far fields u = G psi and
+// v = G eta stay resident in HBM and the line search uses linearity, G(psi + g eta) = u + g v.
+//
+//   k_fwd   u = G psi, F(psi) partials                      (init / set_state; Eq.1, Eq.2)
+//   k_grad  u <- u + gamma_prev v; r = u - d u/|u|^2; y = conj(p) F^H r  (Eq.3 minus the scatter)
+//   k_adj   g = sum_j scatter(y_j): tile-major, atomic-free, canonical frame order (Q^H of Eq.3)
+//           + DY partials |g|^2, <eta, g - g_prev>                (Eq.6 / Eq.8 inner products)
+//   k_dir   alpha (DY complex / real / FR, restart rules)          (Eq.6, Eq.8; R#6, R#9)
+//   k_eta   eta = -g + alpha eta, ||eta||^2                        (Eq.6)
+//   k_ls    v = F(p eta[window]) and K trial partials DeltaF_k     (Eq.7 with the Eq.2 objective)
+//   k_lsx   further K-trial passes over (u, v, d) when no trial of the first pass was accepted
+//   k_pick  first accepted trial, F update, trace                  (Eq.7, Alg.1 659-668)
+//   k_upd   psi <- psi + gamma eta                                  (Eq.5, Alg.1 672)
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "dev.cuh"
+
+namespace pty {
+
+// ----------------------------------------------------------------------------------------
+// k_fwd: u_j = F(p * psi[window s_j]) (Eq.1) and F partial sum (Eq.2) per CTA.
+// ----------------------------------------------------------------------------------------
+template <int N>
+__global__ void __launch_bounds__(512, 1) k_fwd(Geometry g, const float2* __restrict__ psi,
+                                                const float2* __restrict__ probe,
+                                                const int2* __restrict__ pos, const int* __restrict__ order,
+                                                const float* __restrict__ d, float2* __restrict__ u,
+                                                double* __restrict__ part, float eps) {
+    using C = FFTCfg<N>;
+    constexpr int R = C::R, T = C::T, LD = C::LD;
+    extern __shared__ float2 smem[];
+    float2* sf = smem;
+    float2* tw = smem + C::FPB * C::FRAME_ELEMS;
+    __shared__ double sred[16];
+    build_twiddles<N>(tw);
+    __syncthreads();
+    const int64_t nfr = g.n_local;
+    const int64_t ngroups = (nfr + C::FPB - 1) / C::FPB;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const float scale = 1.0f / (float)N, eps2 = eps * eps;
+    double facc = 0.0;
+    for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+#pragma unroll 1
+        for (int rd = 0; rd < C::ROUNDS; ++rd) {
+            const int line = rd * C::LPR + tid / T, t = tid % T;
+            const int f = line / N, row = line % N;
+            const int64_t i = grp * C::FPB + f;
+            float2 x[R];
+            if (i < nfr) {
+                const int j = order[i];
+                const int2 s = pos[j];
+                const float2* src = psi + (int64_t)(s.x + row) * g.W + s.y + t;
+                const float2* pp = probe + row * N + t;
+#pragma unroll
+                for (int n1 = 0; n1 < R; ++n1) x[n1] = cmul(ldg2(pp + T * n1), ldg2(src + T * n1));
+            } else {
+#pragma unroll
+                for (int n1 = 0; n1 < R; ++n1) x[n1] = make_float2(0.f, 0.f);
+            }
+            row_fft<N, false>(x, sf + f * C::FRAME_ELEMS + row * LD, t, tw);
+        }
+        __syncthreads();
+#pragma unroll 1
+        for (int rd = 0; rd < C::ROUNDS; ++rd) {
+            const int t = warp % T;
+            const int line = rd * C::LPR + (warp / T) * 32 + lane;
+            col_fft_phase1<N, false>(sf + (line / N) * C::FRAME_ELEMS + line % N, t, tw);
+        }
+        __syncthreads();
+#pragma unroll 1
+        for (int rd = 0; rd < C::ROUNDS; ++rd) {
+            const int t = warp % T;
+            const int line = rd * C::LPR + (warp / T) * 32 + lane;
+            const int f = line / N, c = line % N;
+            const int64_t i = grp * C::FPB + f;
+            float2 X[R];
+            col_fft_phase2<N, false>(sf + f * C::FRAME_ELEMS + c, t, X);
+            if (i < nfr) {
+                const int64_t j = order[i];
+                float fs = 0.f;
+#pragma unroll
+                for (int q = 0; q < R; ++q) {
+                    const int k = col_out_row<N>(q, t);
+                    const int64_t o = j * N * N + (int64_t)k * N + c;
+                    const float2 uu = cscale(X[q], scale);
+                    u[o] = uu;
+                    const float cc = uu.x * uu.x + uu.y * uu.y;
+                    fs += cc - __ldg(d + o) * logf(fmaxf(cc, eps2));
+                }
+                facc += (double)fs;
+            }
+        }
+        __syncthreads();
+    }
+    const double s = block_sum<512>(facc, sred);
+    if (tid == 0) part[blockIdx.x] = s;
+}
+
+// ----------------------------------------------------------------------------------------
+// k_grad: GRAD stage frame part (Alg.1 648-649): u <- u + gamma_prev v (lazy Eq.5 on the far
+// field), r = u - d/u^*, y = conj(p) F^H r written into v's slot.
+// ----------------------------------------------------------------------------------------
+template <int N>
+__global__ void __launch_bounds__(512, 1) k_grad(Geometry g, float2* __restrict__ u, float2* __restrict__ v,
+                                                 const float* __restrict__ d, const float2* __restrict__ probe,
+                                                 const DevState* __restrict__ st, float eps) {
+    using C = FFTCfg<N>;
+    constexpr int R = C::R, T = C::T, LD = C::LD;
+    extern __shared__ float2 smem[];
+    float2* sf = smem;
+    float2* tw = smem + C::FPB * C::FRAME_ELEMS;
+    if (st->numeric_error) return;
+    build_twiddles<N>(tw);
+    __syncthreads();
+    const float gam = (float)st->gamma;
+    const bool upd = gam != 0.0f;
+    const int64_t nfr = g.n_local;
+    const int64_t ngroups = (nfr + C::FPB - 1) / C::FPB;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const float scale = 1.0f / (float)N, eps2 = eps * eps;
+    for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+#pragma unroll 1
+        for (int rd = 0; rd < C::ROUNDS; ++rd) {
+            const int line = rd * C::LPR + tid / T, t = tid % T;
+            const int f = line / N, row = line % N;
+            const int64_t j = grp * C::FPB + f;
+            float2 x[R];
+            if (j < nfr) {
+                const int64_t base = j * N * N + (int64_t)row * N + t;
+                float2 uu[R];
+                float dd[R];
+#pragma unroll
+                for (int n1 = 0; n1 < R; ++n1) {
+                    uu[n1] = u[base + T * n1];
+                    dd[n1] = __ldg(d + base + T * n1);
+                }
+                if (upd) {
+                    float2 vv[R];
+#pragma unroll
+                    for (int n1 = 0; n1 < R; ++n1) vv[n1] = v[base + T * n1];
+#pragma unroll
+                    for (int n1 = 0; n1 < R; ++n1) {
+                        uu[n1] = make_float2(fmaf(gam, vv[n1].x, uu[n1].x), fmaf(gam, vv[n1].y, uu[n1].y));
+                        u[base + T * n1] = uu[n1];
+                    }
+                }
+#pragma unroll
+                for (int n1 = 0; n1 < R; ++n1) x[n1] = residual(uu[n1], dd[n1], eps2);
+            } else {
+#pragma unroll
+                for (int n1 = 0; n1 < R; ++n1) x[n1] = make_float2(0.f, 0.f);
+            }
+            row_fft<N, true>(x, sf + f * C::FRAME_ELEMS + row * LD, t, tw);
+        }
+        __syncthreads();
+#pragma unroll 1
+        for (int rd = 0; rd < C::ROUNDS; ++rd) {
+            const int t = warp % T;
+            const int line = rd * C::LPR + (warp / T) * 32 + lane;
+            col_fft_phase1<N, true>(sf + (line / N) * C::FRAME_ELEMS + line % N, t, tw);
+        }
+        __syncthreads();
+#pragma unroll 1
+        for (int rd = 0; rd < C::ROUNDS; ++rd) {
+            const int t = warp % T;
+            const int line = rd * C::LPR + (warp / T) * 32 + lane;
+            const int f = line / N, c = line % N;
+            const int64_t j = grp * C::FPB + f;
+            float2 X[R];
+            col_fft_phase2<N, true>(sf + f * C::FRAME_ELEMS + c, t, X);
+            if (j < nfr) {
+#pragma unroll
+                for (int q = 0; q < R; ++q) {
+                    const int k = col_out_row<N>(q, t);
+                    const float2 pk = ldg2(probe + k * N + c);
+                    v[j * N * N + (int64_t)k * N + c] = cscale(cconjmul(pk, X[q]), scale);
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
+
+// ----------------------------------------------------------------------------------------
+// k_ls: LS stage first pass (Alg.1 659-668 with Eq.7): v_j = F(p * eta[window s_j]) written
+// to HBM, then for K trials gamma_k = gamma0 tau^k the SCREENING terms (dev.cuh ls_screen)
+// against (u, d); per-CTA fp64 partials [S_0..S_{K-1}, A_0..A_{K-1}, sum d, sum|a|, sum b].
+// ----------------------------------------------------------------------------------------
+template <int N, int K>
+__global__ void __launch_bounds__(512, 1) k_ls(Geometry g, const float2* __restrict__ eta,
+                                               const float2* __restrict__ probe, const int2* __restrict__ pos,
+                                               const int* __restrict__ order, const float2* __restrict__ u,
+                                               float2* __restrict__ v, const float* __restrict__ d,
+                                               SolverCfg cfg, double* __restrict__ part,
+                                               const DevState* __restrict__ st) {
+    using C = FFTCfg<N>;
+    constexpr int R = C::R, T = C::T, LD = C::LD;
+    extern __shared__ float2 smem[];
+    float2* sf = smem;
+    float2* tw = smem + C::FPB * C::FRAME_ELEMS;
+    __shared__ double sred[16][2 * K];
+    __shared__ double smom[16][3];
+    __shared__ float sgam[K];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const bool err = st->numeric_error != 0;
+    build_twiddles<N>(tw);
+    if (tid < K) sgam[tid] = (float)trial_gamma(cfg.gamma0, cfg.tau, tid);
+    __syncthreads();
+    const int64_t nfr = err ? 0 : g.n_local;
+    const int64_t ngroups = (nfr + C::FPB - 1) / C::FPB;
+    const float scale = 1.0f / (float)N;
+    const float eps2 = (float)(cfg.eps * cfg.eps);
+    double tot = 0.0;  // running total of entry lane >> (5 - log2 2K) of [S | A]
+    double md = 0.0, ma = 0.0, mb = 0.0;
+    for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+#pragma unroll 1
+        for (int rd = 0; rd < C::ROUNDS; ++rd) {
+            const int line = rd * C::LPR + tid / T, t = tid % T;
+            const int f = line / N, row = line % N;
+            const int64_t i = grp * C::FPB + f;
+            float2 x[R];
+            if (i < nfr) {
+                const int j = order[i];
+                const int2 s = pos[j];
+                const float2* src = eta + (int64_t)(s.x + row) * g.W + s.y + t;
+                const float2* pp = probe + row * N + t;
+#pragma unroll
+                for (int n1 = 0; n1 < R; ++n1) x[n1] = cmul(ldg2(pp + T * n1), ldg2(src + T * n1));
+            } else {
+#pragma unroll
+                for (int n1 = 0; n1 < R; ++n1) x[n1] = make_float2(0.f, 0.f);
+            }
+            row_fft<N, false>(x, sf + f * C::FRAME_ELEMS + row * LD, t, tw);
+        }
+        __syncthreads();
+#pragma unroll 1
+        for (int rd = 0; rd < C::ROUNDS; ++rd) {
+            const int t = warp % T;
+            const int line = rd * C::LPR + (warp / T) * 32 + lane;
+            col_fft_phase1<N, false>(sf + (line / N) * C::FRAME_ELEMS + line % N, t, tw);
+        }
+        __syncthreads();
+#pragma unroll 1
+        for (int rd = 0; rd < C::ROUNDS; ++rd) {
+            const int t = warp % T;
+            const int line = rd * C::LPR + (warp / T) * 32 + lane;
+            const int f = line / N, c = line % N;
+            const int64_t i = grp * C::FPB + f;
+            float2 X[R];
+            col_fft_phase2<N, false>(sf + f * C::FRAME_ELEMS + c, t, X);
+            float S[K], A[K];
+            float sd = 0.f, sa = 0.f, sb = 0.f;
+#pragma unroll
+            for (int k = 0; k < K; ++k) S[k] = A[k] = 0.f;
+            if (i < nfr) {
+                const int64_t j = order[i];
+#pragma unroll
+                for (int q = 0; q < R; ++q) {
+                    const int k = col_out_row<N>(q, t);
+                    const int64_t o = j * N * N + (int64_t)k * N + c;
+                    const float2 vv = cscale(X[q], scale);
+                    v[o] = vv;
+                    ls_screen<K>(u[o], vv, __ldg(d + o), sgam, eps2, S, A, sd, sa, sb);
+                }
+            }
+            double dv[2 * K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                dv[k] = (double)S[k];
+                dv[K + k] = (double)A[k];
+            }
+            tot += warp_reduce_scatter<2 * K>(dv, lane);
+            md += (double)sd;
+            ma += (double)sa;
+            mb += (double)sb;
+        }
+        __syncthreads();
+    }
+    // block reduction: lane-group leader of each entry writes per warp, then fixed-order sums
+    constexpr int P = Log2<2 * K>::value;
+    constexpr int G = 32 >> P;
+    if ((lane & (G - 1)) == 0) sred[warp][lane >> (5 - P)] = tot;
+    md = warp_sum(md);
+    ma = warp_sum(ma);
+    mb = warp_sum(mb);
+    if (lane == 0) {
+        smom[warp][0] = md;
+        smom[warp][1] = ma;
+        smom[warp][2] = mb;
+    }
+    __syncthreads();
+    constexpr int WID = 2 * K + 3;
+    if (tid < 2 * K) {
+        double s = 0.0;
+        for (int w = 0; w < 16; ++w) s += sred[w][tid];
+        part[(int64_t)blockIdx.x * WID + tid] = s;
+    } else if (tid < WID) {
+        double s = 0.0;
+        for (int w = 0; w < 16; ++w) s += smom[w][tid - 2 * K];
+        part[(int64_t)blockIdx.x * WID + tid] = s;
+    }
+}
+
+
+// ----------------------------------------------------------------------------------------
+// launchers
+// ----------------------------------------------------------------------------------------
+template <typename F>
+static int set_smem(F* f, size_t bytes) {
+    return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) == cudaSuccess ? 0 : -1;
+}
+
+template <int N>
+static int fwd_n(const Geometry& g, const float2* psi, const float2* probe, const int2* pos,
+                 const int* order, const float* d, float2* u, double* part, int grid, float eps,
+                 cudaStream_t s) {
+    using C = FFTCfg<N>;
+    if (set_smem(k_fwd<N>, C::SMEM_BYTES)) return -1;
+    k_fwd<N><<<grid, C::NT, C::SMEM_BYTES, s>>>(g, psi, probe, pos, order, d, u, part, eps);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+int launch_fwd(const Geometry& g, const float2* psi, const float2* probe, const int2* pos,
+               const int* order, const float* d, float2* u, double* part, int grid, float eps,
+               cudaStream_t s) {
+    switch (g.N) {
+        case 16: return fwd_n<16>(g, psi, probe, pos, order, d, u, part, grid, eps, s);
+        case 32: return fwd_n<32>(g, psi, probe, pos, order, d, u, part, grid, eps, s);
+        case 64: return fwd_n<64>(g, psi, probe, pos, order, d, u, part, grid, eps, s);
+        case 128: return fwd_n<128>(g, psi, probe, pos, order, d, u, part, grid, eps, s);
+    }
+    return -2;
+}
+
+template <int N>
+static int grad_n(const Geometry& g, float2* u, float2* v, const float* d, const float2* probe,
+                  const DevState* st, float eps, int grid, cudaStream_t s) {
+    using C = FFTCfg<N>;
+    if (set_smem(k_grad<N>, C::SMEM_BYTES)) return -1;
+    k_grad<N><<<grid, C::NT, C::SMEM_BYTES, s>>>(g, u, v, d, probe, st, eps);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+int launch_grad(const Geometry& g, float2* u, float2* v, const float* d, const float2* probe,
+                const int* /*order*/, const DevState* st, float eps, int grid, cudaStream_t s) {
+    switch (g.N) {
+        case 16: return grad_n<16>(g, u, v, d, probe, st, eps, grid, s);
+        case 32: return grad_n<32>(g, u, v, d, probe, st, eps, grid, s);
+        case 64: return grad_n<64>(g, u, v, d, probe, st, eps, grid, s);
+        case 128: return grad_n<128>(g, u, v, d, probe, st, eps, grid, s);
+    }
+    return -2;
+}
+
+template <int N, int K>
+static int ls_nk(const Geometry& g, const float2* eta, const float2* probe, const int2* pos,
+                 const int* order, const float2* u, float2* v, const float* d, const SolverCfg& c,
+                 double* part, int grid, const DevState* st, cudaStream_t s) {
+    using C = FFTCfg<N>;
+    if (set_smem(k_ls<N, K>, C::SMEM_BYTES)) return -1;
+    k_ls<N, K><<<grid, C::NT, C::SMEM_BYTES, s>>>(g, eta, probe, pos, order, u, v, d, c, part, st);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+template <int N>
+static int ls_n(const Geometry& g, const float2* eta, const float2* probe, const int2* pos,
+                const int* order, const float2* u, float2* v, const float* d, const SolverCfg& c,
+                double* part, int grid, const DevState* st, cudaStream_t s) {
+    switch (c.K) {
+        case 8: return ls_nk<N, 8>(g, eta, probe, pos, order, u, v, d, c, part, grid, st, s);
+        case 16: return ls_nk<N, 16>(g, eta, probe, pos, order, u, v, d, c, part, grid, st, s);
+    }
+    return -2;
+}
+
+int launch_ls(const Geometry& g, const float2* eta, const float2* probe, const int2* pos,
+              const int* order, const float2* u, float2* v, const float* d, const SolverCfg& c,
+              double* part, int grid, const DevState* st, cudaStream_t s) {
+    switch (g.N) {
+        case 16: return ls_n<16>(g, eta, probe, pos, order, u, v, d, c, part, grid, st, s);
+        case 32: return ls_n<32>(g, eta, probe, pos, order, u, v, d, c, part, grid, st, s);
+        case 64: return ls_n<64>(g, eta, probe, pos, order, u, v, d, c, part, grid, st, s);
+        case 128: return ls_n<128>(g, eta, probe, pos, order, u, v, d, c, part, grid, st, s);
+    }
+    return -2;
+}
+
+}  // namespace pty

@@ -1,0 +1,516 @@
+// Object-domain, reduction and decision kernels of the CG iteration (see kernels_frame.cu header).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "dev.cuh"
+
+namespace pty {
+
+// ----------------------------------------------------------------------------------------
+// k_adj: g[rho] = sum_j y_j[rho - s_j] over the frames whose window covers rho (Q^H of
+// Eq.3), one 32x32 object tile per CTA, frames in canonical order from a CSR list
+// (deterministic, no atomics).  Epilogue: DY partial sums over owned, non-band rows.
+// ----------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_adj(Geometry g, const float2* __restrict__ y,
+                                             const int4* __restrict__ ent, const int* __restrict__ tile_ptr,
+                                             int ntx, float2* __restrict__ gcur,
+                                             const float2* __restrict__ gprev, const float2* __restrict__ eta,
+                                             double* __restrict__ part, const DevState* __restrict__ st) {
+    __shared__ double sred[NDY][8];
+    if (st->numeric_error) return;
+    const int tile = blockIdx.x;
+    const int tx = tile % ntx, ty = tile / ntx;
+    const int lane = threadIdx.x & 31, wy = threadIdx.x >> 5;
+    const int64_t col = (int64_t)tx * 32 + lane;
+    const int64_t row0 = (int64_t)ty * 32 + wy;
+    const int N = g.N;
+    const int64_t NN = (int64_t)N * N;
+    float2 acc[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[i] = make_float2(0.f, 0.f);
+    const int beg = tile_ptr[tile], end = tile_ptr[tile + 1];
+    int e = beg;
+    for (; e + 2 <= end; e += 2) {
+        float2 val[2][4];
+#pragma unroll
+        for (int f = 0; f < 2; ++f) {
+            const int4 en = __ldg(ent + e + f);
+            const int dc = (int)(col - en.z);
+            const bool okc = (unsigned)dc < (unsigned)N;
+            const float2* yb = y + (int64_t)en.x * NN + dc;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int dr = (int)(row0 + 8 * i - en.y);
+                val[f][i] = (okc && (unsigned)dr < (unsigned)N) ? ldg2(yb + (int64_t)dr * N) : make_float2(0.f, 0.f);
+            }
+        }
+#pragma unroll
+        for (int f = 0; f < 2; ++f)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) acc[i] = cadd(acc[i], val[f][i]);
+    }
+    for (; e < end; ++e) {
+        const int4 en = __ldg(ent + e);
+        const int dc = (int)(col - en.z);
+        const bool okc = (unsigned)dc < (unsigned)N;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int dr = (int)(row0 + 8 * i - en.y);
+            if (okc && (unsigned)dr < (unsigned)N) acc[i] = cadd(acc[i], ldg2(y + (int64_t)en.x * NN + (int64_t)dr * N + dc));
+        }
+    }
+    float s[NDY];
+#pragma unroll
+    for (int q = 0; q < NDY; ++q) s[q] = 0.f;
+    if (col < g.W) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int64_t r = row0 + 8 * i;
+            if (r < g.SH) {
+                const int64_t o = r * g.W + col;
+                gcur[o] = acc[i];
+                const bool own = r >= g.own_lo && r < g.own_hi && !(r >= g.band_lo0 && r < g.band_hi0) &&
+                                 !(r >= g.band_lo1 && r < g.band_hi1);
+                if (own) {
+                    const float2 gp = gprev[o], et = eta[o];
+                    const float2 dg = csub(acc[i], gp);
+                    s[0] += acc[i].x * acc[i].x + acc[i].y * acc[i].y;
+                    const float2 den = cconjmul(et, dg);
+                    s[1] += den.x;
+                    s[2] += den.y;
+                    s[3] += gp.x * gp.x + gp.y * gp.y;
+                    const float2 eg = cconjmul(et, acc[i]);
+                    s[4] += eg.x;
+                    s[5] += eg.y;
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < NDY; ++q) {
+        const double w = warp_sum((double)s[q]);
+        if (lane == 0) sred[q][wy] = w;
+    }
+    __syncthreads();
+    if (threadIdx.x < NDY) {
+        double t = 0.0;
+        for (int k = 0; k < 8; ++k) t += sred[threadIdx.x][k];
+        part[(int64_t)tile * NDY + threadIdx.x] = t;
+    }
+}
+
+// After the NCCL band exchange: g[band] += neighbour's partial; DY partials on band rows.
+__global__ void __launch_bounds__(256) k_band_add(float2* __restrict__ gcur, const float2* __restrict__ recv,
+                                                  int64_t row_lo, int64_t rows, int64_t W,
+                                                  const float2* __restrict__ gprev, const float2* __restrict__ eta,
+                                                  int64_t own_lo, int64_t own_hi, double* __restrict__ part) {
+    __shared__ double sred[NDY][8];
+    const int64_t total = rows * W;
+    float s[NDY];
+#pragma unroll
+    for (int q = 0; q < NDY; ++q) s[q] = 0.f;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = row_lo + i / W;
+        const int64_t o = row_lo * W + i;
+        const float2 gv = cadd(gcur[o], recv[i]);
+        gcur[o] = gv;
+        if (r >= own_lo && r < own_hi) {
+            const float2 gp = gprev[o], et = eta[o];
+            s[0] += gv.x * gv.x + gv.y * gv.y;
+            const float2 den = cconjmul(et, csub(gv, gp));
+            s[1] += den.x;
+            s[2] += den.y;
+            s[3] += gp.x * gp.x + gp.y * gp.y;
+            const float2 eg = cconjmul(et, gv);
+            s[4] += eg.x;
+            s[5] += eg.y;
+        }
+    }
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int q = 0; q < NDY; ++q) {
+        const double v = warp_sum((double)s[q]);
+        if (lane == 0) sred[q][w] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < NDY) {
+        double t = 0.0;
+        for (int k = 0; k < 8; ++k) t += sred[threadIdx.x][k];
+        part[(int64_t)blockIdx.x * NDY + threadIdx.x] = t;
+    }
+}
+
+// ----------------------------------------------------------------------------------------
+// Deterministic reduction of per-block partials: dst[w] = sum_b part[b*width + w].
+// ----------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) k_reduce(const double* __restrict__ part, int nblocks, int width,
+                                                 double* __restrict__ dst) {
+    __shared__ double sred[32];
+    for (int w = 0; w < width; ++w) {
+        double s = 0.0;
+        for (int b = threadIdx.x; b < nblocks; b += blockDim.x) s += part[(int64_t)b * width + w];
+        s = warp_sum(s);
+        const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+        if (lane == 0) sred[wp] = s;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += sred[i];
+            dst[w] = t;
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void k_set_F(DevState* st, const double* src) {
+    st->F = src[0];
+    st->gamma = 0.0;
+}
+
+__global__ void k_begin_iter(DevState* st) {
+    st->accepted = 0;
+    st->kstar = -1;
+    st->n_eval = 0;
+    st->restarted = 0;
+    st->stalled = 0;
+    st->need_exact = 0;
+    st->k_unc = 0;
+    for (int k = 0; k < SMAX; ++k) st->ls_hist[k] = st->ls_bnd[k] = __longlong_as_double(0x7ff8000000000000LL);
+}
+
+// DIR stage (Alg.1 651-656): alpha from the reduced DY sums (Eq.8), restart rules (R#9).
+__global__ void k_dir(DevState* st, SolverCfg c) {
+    if (st->numeric_error) return;
+    const double gg = st->dy[0];
+    double are = 0.0, aim = 0.0;
+    int restarted = 0;
+    if (!isfinite(gg)) {
+        st->numeric_error = 1;
+        st->err_iter = st->m;
+        st->gamma = 0.0;
+        return;
+    }
+    if (st->m > 0) {
+        double dre, dim;
+        if (c.direction == PTYGER_DIR_FR) {
+            dre = st->dy[3];
+            dim = 0.0;
+        } else {
+            dre = st->dy[1];
+            dim = st->dy[2];
+        }
+        const double den2 = dre * dre + dim * dim;
+        if (sqrt(den2) < 1e-30) {
+            restarted = 1;
+        } else {
+            // alpha = gg / den = gg conj(den) / |den|^2
+            are = gg * dre / den2;
+            aim = -gg * dim / den2;
+            if (c.direction != PTYGER_DIR_DY) aim = 0.0;
+            if (!isfinite(are) || !isfinite(aim)) {
+                are = aim = 0.0;
+                restarted = 1;
+            }
+        }
+    }
+    st->alpha_re = are;
+    st->alpha_im = aim;
+    st->restarted = restarted;
+}
+
+// eta = -g + alpha eta (Eq.6) over the storage rows; ||eta||^2 over owned rows.
+__global__ void __launch_bounds__(256) k_eta(Geometry g, const float2* __restrict__ gcur, float2* __restrict__ eta,
+                                             const DevState* __restrict__ st, double* __restrict__ part) {
+    __shared__ double sred[8];
+    const float2 al = make_float2((float)st->alpha_re, (float)st->alpha_im);
+    const bool err = st->numeric_error != 0;
+    const int64_t total = g.SH * g.W;
+    const int64_t lo = g.own_lo * g.W, hi = g.own_hi * g.W;
+    float s = 0.f;
+    if (!err) {
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+            const float2 gv = gcur[i];
+            const float2 ev = eta[i];
+            const float2 ne = csub(cmul(al, ev), gv);
+            eta[i] = ne;
+            if (i >= lo && i < hi) s += ne.x * ne.x + ne.y * ne.y;
+        }
+    }
+    const double t = block_sum<256>((double)s, sred);
+    if (threadIdx.x == 0) part[blockIdx.x] = t;
+}
+
+
+// Further LS passes over the cached (u, v, d): trials pass*K .. pass*K+K-1.  SCREEN mode runs
+// unless an earlier pass accepted; EXACT mode runs only when the screening pick left this pass
+// undecided (st->need_exact == pass + 1).  Partials: screen [S | A | sum d, sum|a|, sum b],
+// exact [S].
+template <int K, bool EXACT>
+__global__ void __launch_bounds__(256) k_lsx(int64_t count, const float2* __restrict__ u,
+                                             const float2* __restrict__ v, const float* __restrict__ d,
+                                             SolverCfg cfg, int pass, double* __restrict__ part,
+                                             const DevState* __restrict__ st) {
+    constexpr int NV = EXACT ? K : 2 * K;
+    constexpr int WID = EXACT ? K : 2 * K + 3;
+    __shared__ double sred[8][NV];
+    __shared__ double smom[8][3];
+    __shared__ float sgam[K];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const bool run = EXACT ? (st->need_exact == pass + 1 && !st->numeric_error)
+                           : (!st->accepted && !st->numeric_error);
+    if (tid < K) sgam[tid] = (float)trial_gamma(cfg.gamma0, cfg.tau, pass * K + tid);
+    __syncthreads();
+    const float eps2 = (float)(cfg.eps * cfg.eps);
+    double acc64[NV];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) acc64[k] = 0.0;
+    double md = 0.0, ma = 0.0, mb = 0.0;
+    if (run) {
+        float S[K], A[K];
+        float sd = 0.f, sa = 0.f, sb = 0.f;
+#pragma unroll
+        for (int k = 0; k < K; ++k) S[k] = A[k] = 0.f;
+        int cnt = 0;
+        for (int64_t o = (int64_t)blockIdx.x * blockDim.x + tid; o < count; o += (int64_t)gridDim.x * blockDim.x) {
+            if (EXACT)
+                ls_exact<K>(u[o], v[o], __ldg(d + o), sgam, eps2, S);
+            else
+                ls_screen<K>(u[o], v[o], __ldg(d + o), sgam, eps2, S, A, sd, sa, sb);
+            if (++cnt == 16) {  // bounded fp32 run length, then fp64
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    acc64[k] += (double)S[k];
+                    S[k] = 0.f;
+                    if (!EXACT) {
+                        acc64[K + k] += (double)A[k];
+                        A[k] = 0.f;
+                    }
+                }
+                md += sd; ma += sa; mb += sb;
+                sd = sa = sb = 0.f;
+                cnt = 0;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            acc64[k] += (double)S[k];
+            if (!EXACT) acc64[K + k] += (double)A[k];
+        }
+        md += sd; ma += sa; mb += sb;
+    }
+    const double tot = warp_reduce_scatter<NV>(acc64, lane);
+    constexpr int P = Log2<NV>::value;
+    constexpr int G = 32 >> P;
+    if ((lane & (G - 1)) == 0) sred[warp][lane >> (5 - P)] = tot;
+    md = warp_sum(md);
+    ma = warp_sum(ma);
+    mb = warp_sum(mb);
+    if (lane == 0) {
+        smom[warp][0] = md;
+        smom[warp][1] = ma;
+        smom[warp][2] = mb;
+    }
+    __syncthreads();
+    if (tid < NV) {
+        double s = 0.0;
+        for (int w = 0; w < 8; ++w) s += sred[w][tid];
+        part[(int64_t)blockIdx.x * WID + tid] = s;
+    } else if (tid < WID) {
+        double s = 0.0;
+        for (int w = 0; w < 8; ++w) s += smom[w][tid - NV];
+        part[(int64_t)blockIdx.x * WID + tid] = s;
+    }
+}
+
+// Line-search decision (Eq.7, Alg.1 659-668): the first trial with DeltaF_k <= gamma_k t.
+// SCREEN mode: a trial is decided only if the screening sum S_k is farther than its error bound
+// B_k = LS_EPS_D sum d + LS_EPS_R (A_k + gamma_k sum|a| + gamma_k^2 sum b) from gamma_k t;
+// otherwise the EXACT pass re-evaluates this pass's trials with the accurate log1p and the
+// EXACT-mode pick decides from the first undecided trial on.  F += DeltaF_k* (R#11); after
+// max_shrinks trials: gamma = 0, stalled (R#9); the last pass writes the trace.
+__global__ void k_pick(DevState* st, SolverCfg c, int pass, int exact_mode, int last_pass) {
+    const int K = c.K;
+    if (pass == 0 && !exact_mode) st->eta2 = st->ls_pass[LS_ETA];
+    if (!st->numeric_error && !st->accepted) {
+        if (!exact_mode) {
+            const double sd = st->ls_pass[2 * K], sa = st->ls_pass[2 * K + 1], sb = st->ls_pass[2 * K + 2];
+            for (int k = 0; k < K; ++k) {
+                const int kk = pass * K + k;
+                if (kk >= c.max_shrinks) break;
+                const double gk = trial_gamma(c.gamma0, c.tau, kk);
+                const double S = st->ls_pass[k], A = st->ls_pass[K + k];
+                const double B = LS_EPS_D * sd + LS_EPS_R * (A + gk * sa + gk * gk * sb);
+                st->ls_hist[kk] = S;
+                st->ls_bnd[kk] = B;
+                st->n_eval = kk + 1;
+                if (!(isfinite(S) && isfinite(B)) || fabs(S - gk * c.t) <= B) {
+                    st->need_exact = pass + 1;   // undecided: exact re-evaluation of this pass
+                    st->k_unc = kk;
+                    break;
+                }
+                if (S <= gk * c.t) {
+                    st->accepted = 1;
+                    st->kstar = kk;
+                    st->gamma = gk;
+                    st->F += S;
+                    break;
+                }
+            }
+        } else if (st->need_exact == pass + 1) {
+            for (int kk = st->k_unc; kk < (pass + 1) * K && kk < c.max_shrinks; ++kk) {
+                const double dF = st->ls_pass[kk - pass * K];
+                const double gk = trial_gamma(c.gamma0, c.tau, kk);
+                st->ls_hist[kk] = dF;
+                st->ls_bnd[kk] = 0.0;
+                st->n_eval = kk + 1;
+                st->n_exact += 1;
+                if (!isfinite(dF)) {
+                    st->numeric_error = 2;
+                    st->err_iter = st->m;
+                    st->gamma = 0.0;
+                    break;
+                }
+                if (dF <= gk * c.t) {
+                    st->accepted = 1;
+                    st->kstar = kk;
+                    st->gamma = gk;
+                    st->F += dF;
+                    break;
+                }
+            }
+        }
+    }
+    if (exact_mode) st->need_exact = 0;
+    if (!last_pass || !exact_mode) return;
+    if (st->numeric_error) return;
+    if (!st->accepted) {
+        st->stalled = 1;
+        st->kstar = c.max_shrinks;
+        st->gamma = 0.0;
+    }
+    if (!isfinite(st->F)) {
+        st->numeric_error = 3;
+        st->err_iter = st->m;
+        st->gamma = 0.0;
+        return;
+    }
+    ptyger_trace t;
+    t.iter = st->m;
+    t.shrinks = st->kstar;
+    t.restarted = st->restarted;
+    t.stalled = st->stalled;
+    t.F = st->F;
+    t.gamma = st->gamma;
+    t.alpha_re = st->alpha_re;
+    t.alpha_im = st->alpha_im;
+    t.grad_norm = sqrt(st->dy[0]);
+    t.step_norm = st->gamma * sqrt(st->eta2);
+    if (st->trace_ptr && st->trace_idx < st->trace_cap) st->trace_ptr[st->trace_idx] = t;
+    st->trace_idx += 1;
+    st->m += 1;
+}
+
+// Update stage (Eq.5, Alg.1 672): psi <- psi + gamma eta over the storage rows.
+__global__ void __launch_bounds__(256) k_upd(Geometry g, float2* __restrict__ psi, const float2* __restrict__ eta,
+                                             const DevState* __restrict__ st) {
+    if (st->numeric_error) return;
+    const float gam = (float)st->gamma;
+    if (gam == 0.0f) return;
+    const int64_t total = g.SH * g.W;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const float2 e = eta[i];
+        float2 p = psi[i];
+        p.x = fmaf(gam, e.x, p.x);
+        p.y = fmaf(gam, e.y, p.y);
+        psi[i] = p;
+    }
+}
+
+// d must be finite and >= 0: records the smallest offending frame index.
+__global__ void k_validate_d(const float* __restrict__ d, int64_t count, int64_t frame_elems,
+                             unsigned long long* bad) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+        const float x = d[i];
+        if (!(x >= 0.0f) || isinf(x)) atomicMin(bad, (unsigned long long)(i / frame_elems));
+    }
+}
+
+
+int launch_adj(const Geometry& g, const float2* y, const int* tile_ptr, const int* tile_frames,
+               int ntx, int nty, float2* gcur, const float2* gprev, const float2* eta, double* part,
+               const DevState* st, cudaStream_t s) {
+    // tile_frames holds int4 entries {frame, row, col, 0}
+    k_adj<<<ntx * nty, 256, 0, s>>>(g, y, reinterpret_cast<const int4*>(tile_frames), tile_ptr, ntx, gcur,
+                                    gprev, eta, part, st);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+int launch_lsx(const Geometry& g, const float2* u, const float2* v, const float* d,
+               const SolverCfg& c, int pass, bool exact, double* part, int grid, const DevState* st,
+               cudaStream_t s) {
+    const int64_t count = g.n_local * (int64_t)g.N * g.N;
+    if (c.K == 8) {
+        if (exact) k_lsx<8, true><<<grid, 256, 0, s>>>(count, u, v, d, c, pass, part, st);
+        else k_lsx<8, false><<<grid, 256, 0, s>>>(count, u, v, d, c, pass, part, st);
+    } else if (c.K == 16) {
+        if (exact) k_lsx<16, true><<<grid, 256, 0, s>>>(count, u, v, d, c, pass, part, st);
+        else k_lsx<16, false><<<grid, 256, 0, s>>>(count, u, v, d, c, pass, part, st);
+    } else {
+        return -2;
+    }
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+int launch_reduce(const double* part, int nblocks, int width, double* dst, cudaStream_t s) {
+    k_reduce<<<1, 1024, 0, s>>>(part, nblocks, width, dst);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+int launch_dir(DevState* st, const SolverCfg& c, cudaStream_t s) {
+    k_dir<<<1, 1, 0, s>>>(st, c);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+int launch_eta(const Geometry& g, const float2* gcur, float2* eta, const DevState* st, double* part,
+               int grid, cudaStream_t s) {
+    k_eta<<<grid, 256, 0, s>>>(g, gcur, eta, st, part);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+int launch_pick(DevState* st, const SolverCfg& c, int pass, int exact_mode, int last_pass, cudaStream_t s) {
+    k_pick<<<1, 1, 0, s>>>(st, c, pass, exact_mode, last_pass);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+int launch_upd(const Geometry& g, float2* psi, const float2* eta, const DevState* st, int grid,
+               cudaStream_t s) {
+    k_upd<<<grid, 256, 0, s>>>(g, psi, eta, st);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+int launch_begin_iter(DevState* st, cudaStream_t s) {
+    k_begin_iter<<<1, 1, 0, s>>>(st);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+int launch_validate_d(const float* d, int64_t count, int64_t frame_elems, unsigned long long* bad,
+                      cudaStream_t s) {
+    k_validate_d<<<1184, 256, 0, s>>>(d, count, frame_elems, bad);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+int launch_set_F(DevState* st, const double* src, cudaStream_t s) {
+    k_set_F<<<1, 1, 0, s>>>(st, src);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+int launch_band_add(float2* gcur, const float2* recv, int64_t row_lo, int64_t rows, int64_t W,
+                    const float2* gprev, const float2* eta, int64_t own_lo, int64_t own_hi,
+                    double* part, int grid, cudaStream_t s) {
+    k_band_add<<<grid, 256, 0, s>>>(gcur, recv, row_lo, rows, W, gprev, eta, own_lo, own_hi, part);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+}  // namespace pty
+

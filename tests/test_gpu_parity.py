@@ -119,14 +119,17 @@ def test_teacher_forced_iterations(L, name, direction):
         # LS partials on the GPU's eta_m (fp64 oracle, difference form)
         _, _, eta_m, _, _ = pt.get_state()
         v_ref = O.forward_G(c128(eta_m), p64, scan)
-        dF = pt.get_ls_partials()
-        assert len(dF) == (tr["shrinks"] + 1 if not tr["stalled"] else 32) or len(dF) >= tr["shrinks"] + 1
+        dF, bnd = pt.get_ls_partials(with_bound=True)
+        assert len(dF) == (tr["shrinks"] + 1 if not tr["stalled"] else 32)
         a_terms = np.abs(u_ref) ** 2
         for k, val in enumerate(dF):
             gk = 0.5 ** k
             ref = O.ls_delta(u_ref, v_ref, d64, gk)
             scale = np.sum(np.abs(u_ref + gk * v_ref) ** 2) + np.sum(a_terms) + 2 * np.sum(np.abs(d64 * np.log(np.maximum(np.abs(u_ref), 1e-30))))
-            assert abs(val - ref) <= 1e-5 * scale, (m, k, val, ref, scale)
+            # screened values carry their own error bound (exact re-evaluations report 0)
+            assert abs(val - ref) <= max(1e-5 * scale, 2 * bnd[k]), (m, k, val, ref, scale, bnd[k])
+            if bnd[k] > 0:
+                assert bnd[k] <= 1e-4 * scale          # the screening bound stays tight
             n_checked_ls += 1
         # decision: first k with DeltaF_k <= 0 (t = 0), unless ambiguous
         refs = [O.ls_delta(u_ref, v_ref, d64, 0.5 ** k) for k in range(len(dF))]
@@ -190,7 +193,9 @@ def test_stationary_at_noiseless_truth(L):
     tr = pt.iterate(1)[0]
     g = pt.get_gradient()
     assert np.linalg.norm(g) <= 1e-4 * np.linalg.norm(O.illumination(c128(p), scan, psi_true.shape) * psi_true)
-    assert tr["gamma"] == 1.0
+    # at the fixed point DeltaF(gamma) is below fp32 resolution, so which tiny step is accepted is
+    # rounding noise (the fp64 oracle accepts gamma = 1); the step itself must be negligible
+    assert tr["step_norm"] <= 1e-5 * np.linalg.norm(psi_true) and not tr["stalled"]
     pt.close()
 
 
