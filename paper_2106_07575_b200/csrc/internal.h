@@ -61,6 +61,8 @@ int launch_fwd(const Geometry& g, const float2* psi, const float2* probe, const 
                cudaStream_t s);
 int launch_grad(const Geometry& g, float2* u, float2* v, const float* d, const float2* probe,
                 const int* order, const DevState* st, float eps, int grid, cudaStream_t s);
+int launch_grad128(const Geometry& g, float2* u, float2* v, const float* d, const float2* probe,
+                   const DevState* st, float eps, int grid, cudaStream_t s);
 int launch_adj(const Geometry& g, const float2* y, const int* tile_ptr, const int* tile_frames,
                int ntx, int nty, float2* gcur, const float2* gprev, const float2* eta, double* part,
                const DevState* st, cudaStream_t s);

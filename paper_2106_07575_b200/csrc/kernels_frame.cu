@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "dev.cuh"
 
@@ -351,7 +352,9 @@ int launch_grad(const Geometry& g, float2* u, float2* v, const float* d, const f
         case 16: return grad_n<16>(g, u, v, d, probe, st, eps, grid, s);
         case 32: return grad_n<32>(g, u, v, d, probe, st, eps, grid, s);
         case 64: return grad_n<64>(g, u, v, d, probe, st, eps, grid, s);
-        case 128: return grad_n<128>(g, u, v, d, probe, st, eps, grid, s);
+        case 128:
+            if (!getenv("PTYGER_GRAD_V1")) return launch_grad128(g, u, v, d, probe, st, eps, grid, s);
+            return grad_n<128>(g, u, v, d, probe, st, eps, grid, s);
     }
     return -2;
 }
