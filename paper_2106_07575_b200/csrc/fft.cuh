@@ -191,6 +191,31 @@ __device__ __forceinline__ void row_fft(float2 (&x)[FFTCfg<N>::R], float2* srow,
     }
 }
 
+// ROW pass whose results stay in registers: X[j*T + k2] is column (j*T + t) + R*k2 of the row
+// (same arithmetic as row_fft; srow is used only for the exchange and is clobbered).
+template <int N, bool INV>
+__device__ __forceinline__ void row_fft_regs(float2 (&x)[FFTCfg<N>::R], float2* srow, int t, const float2* tw) {
+    constexpr int R = FFTCfg<N>::R, T = FFTCfg<N>::T;
+    static_assert(T > 1, "row_fft_regs needs T > 1");
+    DFT<R, INV>::run(x);
+#pragma unroll
+    for (int k1 = 1; k1 < R; ++k1) x[k1] = twmul<INV>(x[k1], tw[t * k1]);
+    __syncwarp();
+#pragma unroll
+    for (int k1 = 0; k1 < R; ++k1) srow[T * k1 + (t ^ (k1 & (T - 1)))] = x[k1];
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < R / T; ++j) {
+        const int k1 = j * T + t;
+        float2 b[T];
+#pragma unroll
+        for (int n2 = 0; n2 < T; ++n2) b[n2] = srow[T * k1 + (n2 ^ t)];
+        DFT<T, INV>::run(b);
+#pragma unroll
+        for (int k2 = 0; k2 < T; ++k2) x[j * T + k2] = b[k2];
+    }
+}
+
 // COLUMN pass phase 1 for column scol (pointer to element [0][c]); sub-thread t.
 // Reads rows T*n1 + t, writes the twiddled radix-R outputs back to rows T*k1 + t.
 template <int N, bool INV>

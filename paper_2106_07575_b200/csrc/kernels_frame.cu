@@ -383,6 +383,8 @@ static int ls_n(const Geometry& g, const float2* eta, const float2* probe, const
 int launch_ls(const Geometry& g, const float2* eta, const float2* probe, const int2* pos,
               const int* order, const float2* u, float2* v, const float* d, const SolverCfg& c,
               double* part, int grid, const DevState* st, cudaStream_t s) {
+    if (g.N == 128 && !getenv("PTYGER_LS_V1"))
+        return launch_ls128(g, eta, probe, pos, order, u, v, d, c, part, grid, st, s);
     switch (g.N) {
         case 16: return ls_n<16>(g, eta, probe, pos, order, u, v, d, c, part, grid, st, s);
         case 32: return ls_n<32>(g, eta, probe, pos, order, u, v, d, c, part, grid, st, s);
