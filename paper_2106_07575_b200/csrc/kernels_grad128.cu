@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(512, 1) k_grad128(Geometry g, float2* __restri
         const int q = (int)(c % CHUNKS);
         const int64_t j = (int64_t)blockIdx.x + fi * gridDim.x;
         unsigned char* slot = ring + (c & 1) * SLOT_BYTES;
-        uint64_t* b = bar + (c & 1);
+        uint64_t* b = bar + (c & 3);
         mbar_arrive_expect_tx(b, chunk_bytes);
         const int64_t off = j * N * N + (int64_t)q * ROWS * N;
         for (int r = 0; r < ROWS; ++r) {
@@ -71,8 +71,7 @@ __global__ void __launch_bounds__(512, 1) k_grad128(Geometry g, float2* __restri
 
     build_twiddles<N>(tw);
     if (tid == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
+        for (int i = 0; i < 4; ++i) mbar_init(&bar[i], 1);
         fence_mbar_init();
     }
     __syncthreads();
@@ -88,7 +87,10 @@ __global__ void __launch_bounds__(512, 1) k_grad128(Geometry g, float2* __restri
             const int q = rd * 4 + grp;
             const int64_t cc = fi * CHUNKS + q;
             const int sid = (int)(cc & 1);
-            mbar_wait(&bar[sid], (uint32_t)((cc >> 1) & 1));
+            // barrier cc % 4: its previous use (chunk cc - 4) was consumed by this same group, so
+            // the parity wait cannot be satisfied by a stale phase (a per-slot barrier could be,
+            // when this group runs two phases ahead of the slot)
+            mbar_wait(&bar[cc & 3], (uint32_t)((cc >> 2) & 1));
             const unsigned char* slot = ring + sid * SLOT_BYTES;
             const int rloc = gtid >> 3, t = gtid & 7;
             const int row = q * ROWS + rloc;

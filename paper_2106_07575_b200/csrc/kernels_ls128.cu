@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(512, 1) k_ls128(Geometry g, const float2* __re
         const int64_t j = order[(int64_t)blockIdx.x + fi * gridDim.x];
         const int sid = (int)(c % NSLOT);
         unsigned char* slot = ring + sid * SLOT_BYTES;
-        uint64_t* b = bar + sid;
+        uint64_t* b = bar + (c & 3);
         mbar_arrive_expect_tx(b, ROWS * (1024u + 512u));
         for (int r = 0; r < ROWS; ++r) {
             const int64_t off = j * N * N + (int64_t)logical_row(q * ROWS + r) * N;
@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(512, 1) k_ls128(Geometry g, const float2* __re
     build_twiddles<N>(tw);
     if (tid < K) sgam[tid] = (float)trial_gamma(cfg.gamma0, cfg.tau, tid);
     if (tid == 0) {
-        for (int i = 0; i < NSLOT; ++i) mbar_init(&bar[i], 1);
+        for (int i = 0; i < 4; ++i) mbar_init(&bar[i], 1);
         fence_mbar_init();
     }
     __syncthreads();
@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(512, 1) k_ls128(Geometry g, const float2* __re
             row_fft_regs<N, false>(X, sr, t, tw);
             const int64_t cc = fi * CHUNKS + q;
             const int sid = (int)(cc % NSLOT);
-            mbar_wait(&bar[sid], (uint32_t)((cc / NSLOT) & 1));
+            mbar_wait(&bar[cc & 3], (uint32_t)((cc >> 2) & 1));   // see k_grad128: one barrier per group
             const unsigned char* slot = ring + sid * SLOT_BYTES;
             const float2* su = reinterpret_cast<const float2*>(slot + SLOT_U + (srow & 15) * UST);
             const float* sd = reinterpret_cast<const float*>(slot + SLOT_D + (srow & 15) * DST);
