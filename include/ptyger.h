@@ -95,7 +95,7 @@ void ptyger_config_default(ptyger_config* cfg);
 /*
  * Create a context and upload one problem (Alg.1).
  *   object       psi_0: H*W complex64 (2*H*W floats), row-major, host or device.
- *   probe        p: N*N complex64, host or device; N even, N in {16, 32, 64, 128}.
+ *   probe        p: N*N complex64, host or device; N in {16, 32, 64, 128, 256}.
  *   scan         n*(row, col) int32 top-left corners, 0<=row<=H-N, 0<=col<=W-N, host.
  *   intensities  d: n*N*N float32 >= 0 and finite, frame j at offset j*N*N, detector pixel
  *                (k1, k2) at k1*N + k2 in DFT order (DC at [0,0]); host or device.
@@ -165,7 +165,7 @@ ptyger_status ptyger_round_positions(const float* raw, int64_t n, int32_t* out);
 
 /* The library's batched unitary 2-D FFT on DEVICE buffers (cross-check against cuFFT):
  * batch frames of N*N complex64, forward (inverse = 0, e^{-i}) or inverse (e^{+i}), 1/N scale.
- * stream is a cudaStream_t (NULL = default stream).  N in {16, 32, 64, 128}. */
+ * stream is a cudaStream_t (NULL = default stream).  N in {16, 32, 64, 128, 256}. */
 ptyger_status ptyger_fft2(const float* in, float* out, int32_t N, int64_t batch, int32_t inverse,
                           void* stream);
 

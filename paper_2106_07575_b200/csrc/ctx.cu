@@ -370,8 +370,8 @@ ptyger_status ptyger_nccl_unique_id(void* out128) {
 
 ptyger_status ptyger_fft2(const float* in, float* out, int32_t N, int64_t batch, int32_t inverse, void* stream) {
     if (!in || !out || batch < 0) return set_err(nullptr, PTYGER_E_ARG, "fft2: null pointer or batch < 0");
-    if (N != 16 && N != 32 && N != 64 && N != 128)
-        return set_err(nullptr, PTYGER_E_ARG, "fft2: N must be 16, 32, 64 or 128");
+    if (N != 16 && N != 32 && N != 64 && N != 128 && N != 256)
+        return set_err(nullptr, PTYGER_E_ARG, "fft2: N must be 16, 32, 64, 128 or 256");
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
         cudaGetLastError();
@@ -552,8 +552,8 @@ ptyger_status ptyger_init(ptyger_ctx** out, const ptyger_config* cfg_in, const f
         return set_err(nullptr, PTYGER_E_ARG,
                        "init: bad config (need gamma0>0, 0<tau<1, eps>0, 1<=max_shrinks<=64, ls_batch in {8,16}, "
                        "direction in {0,1,2}, 0<=rank<world, nccl_id when world>1)");
-    if (N != 16 && N != 32 && N != 64 && N != 128)
-        return set_err(nullptr, PTYGER_E_ARG, "init: N must be 16, 32, 64 or 128");
+    if (N != 16 && N != 32 && N != 64 && N != 128 && N != 256)
+        return set_err(nullptr, PTYGER_E_ARG, "init: N must be 16, 32, 64, 128 or 256");
     if (H < N || W < N) return set_err(nullptr, PTYGER_E_DATA, "init: object smaller than the probe");
     if (n < 1) return set_err(nullptr, PTYGER_E_DATA, "init: need at least one scan position");
     for (int64_t j = 0; j < n; ++j) {

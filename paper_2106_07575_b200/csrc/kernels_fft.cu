@@ -98,6 +98,7 @@ int launch_fft2(const float2* in, float2* out, int N, int64_t batch, bool inv, c
         case 32: return inv ? fft2_n<32, true>(in, out, batch, s) : fft2_n<32, false>(in, out, batch, s);
         case 64: return inv ? fft2_n<64, true>(in, out, batch, s) : fft2_n<64, false>(in, out, batch, s);
         case 128: return inv ? fft2_n<128, true>(in, out, batch, s) : fft2_n<128, false>(in, out, batch, s);
+        case 256: return launch_fft2_256(in, out, batch, inv, s);
     }
     return -2;
 }

@@ -333,6 +333,7 @@ int launch_fwd(const Geometry& g, const float2* psi, const float2* probe, const 
         case 32: return fwd_n<32>(g, psi, probe, pos, order, d, u, part, grid, eps, s);
         case 64: return fwd_n<64>(g, psi, probe, pos, order, d, u, part, grid, eps, s);
         case 128: return fwd_n<128>(g, psi, probe, pos, order, d, u, part, grid, eps, s);
+        case 256: return launch_fwd256(g, psi, probe, pos, order, d, u, part, grid, eps, s);
     }
     return -2;
 }
@@ -355,6 +356,7 @@ int launch_grad(const Geometry& g, float2* u, float2* v, const float* d, const f
         case 128:
             if (!getenv("PTYGER_GRAD_V1")) return launch_grad128(g, u, v, d, probe, st, eps, grid, s);
             return grad_n<128>(g, u, v, d, probe, st, eps, grid, s);
+        case 256: return launch_grad256(g, u, v, d, probe, st, eps, grid, s);
     }
     return -2;
 }
@@ -390,6 +392,7 @@ int launch_ls(const Geometry& g, const float2* eta, const float2* probe, const i
         case 32: return ls_n<32>(g, eta, probe, pos, order, u, v, d, c, part, grid, st, s);
         case 64: return ls_n<64>(g, eta, probe, pos, order, u, v, d, c, part, grid, st, s);
         case 128: return ls_n<128>(g, eta, probe, pos, order, u, v, d, c, part, grid, st, s);
+        case 256: return launch_ls256(g, eta, probe, pos, order, u, v, d, c, part, grid, st, s);
     }
     return -2;
 }

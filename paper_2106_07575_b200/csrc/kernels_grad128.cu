@@ -87,9 +87,9 @@ __global__ void __launch_bounds__(512, 1) k_grad128(Geometry g, float2* __restri
             const int q = rd * 4 + grp;
             const int64_t cc = fi * CHUNKS + q;
             const int sid = (int)(cc & 1);
-            // barrier cc % 4: its previous use (chunk cc - 4) was consumed by this same group, so
-            // the parity wait cannot be satisfied by a stale phase (a per-slot barrier could be,
-            // when this group runs two phases ahead of the slot)
+            // barrier cc % 4 = lcm(issue distance 2, 4 groups): its previous use, chunk cc - 4, was
+            // consumed by this same group (no stale-parity match), and it landed before chunk
+            // cc - 2 was issued (so the issuer of cc, which consumed cc - 2, arms a closed phase)
             mbar_wait(&bar[cc & 3], (uint32_t)((cc >> 2) & 1));
             const unsigned char* slot = ring + sid * SLOT_BYTES;
             const int rloc = gtid >> 3, t = gtid & 7;

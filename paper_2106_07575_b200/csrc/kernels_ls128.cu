@@ -30,7 +30,12 @@ constexpr int NSLOT = 3;
 constexpr int FRAME_BYTES = N * LD * 8;
 constexpr int RING_OFF = FRAME_BYTES + N * 8;
 constexpr int BAR_OFF = RING_OFF + NSLOT * SLOT_BYTES;
-constexpr size_t SMEM = BAR_OFF + 64;
+// Chunk c waits on barrier c % NBAR.  NBAR = lcm(issue distance NSLOT = 3, 4 consumer groups):
+// the barrier's previous use, chunk c - 12, was consumed by the waiting group itself (so a parity
+// wait cannot match a stale phase), and it landed before chunk c - 9, c - 6, c - 3 were issued in
+// turn (so the issuer of c, which consumed c - 3, never arms a barrier whose phase is still open).
+constexpr int NBAR = 12;
+constexpr size_t SMEM = BAR_OFF + NBAR * 8;
 static_assert(SMEM <= 232448, "exceeds the 227 KB per-CTA shared memory");
 __device__ __forceinline__ int logical_row(int s) { return (s >> 3) + 16 * (s & 7); }
 }  // namespace l128
@@ -66,7 +71,7 @@ __global__ void __launch_bounds__(512, 1) k_ls128(Geometry g, const float2* __re
         const int64_t j = order[(int64_t)blockIdx.x + fi * gridDim.x];
         const int sid = (int)(c % NSLOT);
         unsigned char* slot = ring + sid * SLOT_BYTES;
-        uint64_t* b = bar + (c & 3);
+        uint64_t* b = bar + (c % NBAR);
         mbar_arrive_expect_tx(b, ROWS * (1024u + 512u));
         for (int r = 0; r < ROWS; ++r) {
             const int64_t off = j * N * N + (int64_t)logical_row(q * ROWS + r) * N;
@@ -78,7 +83,7 @@ __global__ void __launch_bounds__(512, 1) k_ls128(Geometry g, const float2* __re
     build_twiddles<N>(tw);
     if (tid < K) sgam[tid] = (float)trial_gamma(cfg.gamma0, cfg.tau, tid);
     if (tid == 0) {
-        for (int i = 0; i < 4; ++i) mbar_init(&bar[i], 1);
+        for (int i = 0; i < NBAR; ++i) mbar_init(&bar[i], 1);
         fence_mbar_init();
     }
     __syncthreads();
@@ -136,7 +141,7 @@ __global__ void __launch_bounds__(512, 1) k_ls128(Geometry g, const float2* __re
             row_fft_regs<N, false>(X, sr, t, tw);
             const int64_t cc = fi * CHUNKS + q;
             const int sid = (int)(cc % NSLOT);
-            mbar_wait(&bar[cc & 3], (uint32_t)((cc >> 2) & 1));   // see k_grad128: one barrier per group
+            mbar_wait(&bar[cc % NBAR], (uint32_t)((cc / NBAR) & 1));
             const unsigned char* slot = ring + sid * SLOT_BYTES;
             const float2* su = reinterpret_cast<const float2*>(slot + SLOT_U + (srow & 15) * UST);
             const float* sd = reinterpret_cast<const float*>(slot + SLOT_D + (srow & 15) * DST);

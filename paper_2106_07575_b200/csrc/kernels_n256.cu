@@ -1,0 +1,348 @@
+// Frame kernels for N = 256 (BASELINE "large" view: 8192^2 object, 256^2 detector).
+//
+// A 256x256 complex64 frame is 512 KB: it does not fit one SM (228 KB shared memory), so each
+// 2-D FFT runs as TWO passes of one CTA over the frame, with the frame's OWN far-field slot in
+// HBM (v, which is dead at that point in both kernels) as the transpose buffer:
+//   pass 1: 32-row batches; a row is 16 threads x 16 elements (N = 16 x 16: radix-16 in
+//           registers, W_256 twiddle, XOR-swizzled exchange, radix-16 across the 16 lanes);
+//           results go from registers to the slot's rows (coalesced 128-B segments);
+//   pass 2: 32-column batches; lanes = 32 consecutive columns, the 16 sub-threads of a column in
+//           16 warps; phase 1 reads the slot (L2-resident: written microseconds earlier by this
+//           CTA), phase 2 produces whole columns and runs the epilogue (y = conj(p) X / N for
+//           k_grad; v = X/N plus the LS screening terms against u, d for k_ls).
+// The intermediate lines are overwritten by the final values while still in L2, so HBM traffic
+// stays at the design-S bytes (36 B/px k_grad, 20 B/px k_ls); L2 carries +16 B/px.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "dev.cuh"
+
+namespace pty {
+
+namespace n256 {
+constexpr int N = 256, R = 16, T = 16, LD = N + 8;
+constexpr int NT = 512;
+constexpr int ROWB = NT / T;      // 32 rows per pass-1 batch
+constexpr int COLB = 32;          // 32 columns per pass-2 batch
+constexpr int BUF = ROWB * LD;    // complex elements of the batch buffer (>= N * COLB)
+static_assert(BUF >= N * COLB, "buffer too small for a column batch");
+constexpr size_t SMEM = (size_t)(BUF + N) * sizeof(float2);   // + twiddle table
+}  // namespace n256
+
+// pass 2 of a 2-D transform: column batch cb (columns cb*32 .. +31) of slot (frame base `src`,
+// row-major N x N); returns X[k2] = output row t + 16 k2 of column c (unnormalised).
+template <bool INV>
+__device__ __forceinline__ void n256_column(const float2* __restrict__ src, int cb, float2* buf, const float2* tw,
+                                            float2 (&X)[16], int& c) {
+    using namespace n256;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int t = warp;  // 16 warps = 16 sub-threads of every column
+    c = cb * COLB + lane;
+    float2 x[R];
+#pragma unroll
+    for (int n1 = 0; n1 < R; ++n1) x[n1] = src[(int64_t)(T * n1 + t) * N + c];
+    DFT<R, INV>::run(x);
+#pragma unroll
+    for (int k1 = 1; k1 < R; ++k1) x[k1] = twmul<INV>(x[k1], tw[t * k1]);
+    __syncthreads();  // previous batch's readers are done with buf
+#pragma unroll
+    for (int k1 = 0; k1 < R; ++k1) buf[(T * k1 + t) * COLB + lane] = x[k1];
+    __syncthreads();
+    // phase 2: k1 = t (R / T = 1), inputs rows T*t + n2
+#pragma unroll
+    for (int n2 = 0; n2 < T; ++n2) X[n2] = buf[(T * t + n2) * COLB + lane];
+    DFT<T, INV>::run(X);
+}
+
+// ---------------------------------------------------------------------------------------------
+// k_grad (N = 256): u <- u + gamma v, r = u - d/u^*, y = conj(p) F^H r into v's slot.
+// ---------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(512, 1) k_grad256(Geometry g, float2* __restrict__ u, float2* __restrict__ v,
+                                                    const float* __restrict__ d, const float2* __restrict__ probe,
+                                                    const DevState* __restrict__ st, float eps) {
+    using namespace n256;
+    extern __shared__ float2 smem[];
+    float2* buf = smem;
+    float2* tw = smem + BUF;
+    if (st->numeric_error) return;
+    build_twiddles<N>(tw);
+    __syncthreads();
+    const float gam = (float)st->gamma;
+    const bool upd = gam != 0.0f;
+    const float eps2 = eps * eps, scale = 1.0f / (float)N;
+    const int tid = threadIdx.x;
+    for (int64_t j = blockIdx.x; j < g.n_local; j += gridDim.x) {
+        float2* vj = v + j * N * N;
+        // pass 1: rows
+#pragma unroll 1
+        for (int rb = 0; rb < N / ROWB; ++rb) {
+            const int row = rb * ROWB + tid / T, t = tid % T;
+            const int64_t base = j * N * N + (int64_t)row * N + t;
+            float2 uu[R];
+            float dd[R];
+#pragma unroll
+            for (int n1 = 0; n1 < R; ++n1) {
+                uu[n1] = u[base + T * n1];
+                dd[n1] = __ldg(d + base + T * n1);
+            }
+            if (upd) {
+                float2 vv[R];
+#pragma unroll
+                for (int n1 = 0; n1 < R; ++n1) vv[n1] = v[base + T * n1];
+#pragma unroll
+                for (int n1 = 0; n1 < R; ++n1) {
+                    uu[n1] = make_float2(fmaf(gam, vv[n1].x, uu[n1].x), fmaf(gam, vv[n1].y, uu[n1].y));
+                    u[base + T * n1] = uu[n1];
+                }
+            }
+            float2 x[R];
+#pragma unroll
+            for (int n1 = 0; n1 < R; ++n1) x[n1] = residual(uu[n1], dd[n1], eps2);
+            float2* srow = buf + (tid / T) * LD;
+            __syncwarp();
+            row_fft_regs<N, true>(x, srow, t, tw);
+            // x[k2] is column t + 16 k2; v of this row was consumed above, so the slot row is free
+            float2* dst = vj + (int64_t)row * N + t;
+#pragma unroll
+            for (int k2 = 0; k2 < T; ++k2) dst[R * k2] = x[k2];
+        }
+        __syncthreads();
+        // pass 2: columns, epilogue y = conj(p) X / N
+#pragma unroll 1
+        for (int cb = 0; cb < N / COLB; ++cb) {
+            float2 X[16];
+            int c;
+            n256_column<true>(vj, cb, buf, tw, X, c);
+            const int t = tid >> 5;
+#pragma unroll
+            for (int k2 = 0; k2 < T; ++k2) {
+                const int k = t + R * k2;
+                vj[(int64_t)k * N + c] = cscale(cconjmul(ldg2(probe + k * N + c), X[k2]), scale);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// k_ls (N = 256): v = F(p * eta[window]) (pass 1 rows -> v slot, pass 2 columns), then the LS
+// screening terms against (u, d); per-CTA partials [S | A | sum d, sum|a|, sum b].
+// k_fwd (N = 256) shares the structure: u = F(p * psi[window]) and the Eq.2 objective.
+// ---------------------------------------------------------------------------------------------
+template <int K, bool FWD>
+__global__ void __launch_bounds__(512, 1) k_lsfwd256(Geometry g, const float2* __restrict__ obj,
+                                                     const float2* __restrict__ probe, const int2* __restrict__ pos,
+                                                     const int* __restrict__ order, float2* __restrict__ u,
+                                                     float2* __restrict__ v, const float* __restrict__ d, SolverCfg cfg,
+                                                     double* __restrict__ part, const DevState* __restrict__ st) {
+    using namespace n256;
+    extern __shared__ float2 smem[];
+    float2* buf = smem;
+    float2* tw = smem + BUF;
+    constexpr int NV = FWD ? 1 : 2 * K;
+    __shared__ double sred[16][NV];
+    __shared__ double smom[16][3];
+    __shared__ float sgam[K];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const bool err = !FWD && st->numeric_error != 0;
+    build_twiddles<N>(tw);
+    if (tid < K) sgam[tid] = (float)trial_gamma(cfg.gamma0, cfg.tau, tid);
+    __syncthreads();
+    const int64_t nfr = err ? 0 : g.n_local;
+    const float eps2 = (float)(cfg.eps * cfg.eps), scale = 1.0f / (float)N;
+    float2* out = FWD ? u : v;
+    double tot = 0.0, md = 0.0, ma = 0.0, mb = 0.0, facc = 0.0;
+    for (int64_t i = blockIdx.x; i < nfr; i += gridDim.x) {
+        const int64_t j = order[i];
+        const int2 s = pos[j];
+        float2* oj = out + j * N * N;
+#pragma unroll 1
+        for (int rb = 0; rb < N / ROWB; ++rb) {
+            const int row = rb * ROWB + tid / T, t = tid % T;
+            const float2* src = obj + (int64_t)(s.x + row) * g.W + s.y + t;
+            const float2* pp = probe + row * N + t;
+            float2 x[R];
+#pragma unroll
+            for (int n1 = 0; n1 < R; ++n1) x[n1] = cmul(ldg2(pp + T * n1), ldg2(src + T * n1));
+            float2* srow = buf + (tid / T) * LD;
+            __syncwarp();
+            row_fft_regs<N, false>(x, srow, t, tw);
+            float2* dst = oj + (int64_t)row * N + t;
+#pragma unroll
+            for (int k2 = 0; k2 < T; ++k2) dst[R * k2] = x[k2];
+        }
+        __syncthreads();
+#pragma unroll 1
+        for (int cb = 0; cb < N / COLB; ++cb) {
+            float2 X[16];
+            int c;
+            n256_column<false>(oj, cb, buf, tw, X, c);
+            const int t = tid >> 5;
+            if (FWD) {
+                float fs = 0.f;
+#pragma unroll
+                for (int k2 = 0; k2 < T; ++k2) {
+                    const int64_t o = j * N * N + (int64_t)(t + R * k2) * N + c;
+                    const float2 uu = cscale(X[k2], scale);
+                    u[o] = uu;
+                    const float cc = uu.x * uu.x + uu.y * uu.y;
+                    fs += cc - __ldg(d + o) * logf(fmaxf(cc, eps2));
+                }
+                facc += (double)fs;
+            } else {
+                float S[K], A[K];
+                float sd_ = 0.f, sa_ = 0.f, sb_ = 0.f;
+#pragma unroll
+                for (int kk = 0; kk < K; ++kk) S[kk] = A[kk] = 0.f;
+#pragma unroll
+                for (int k2 = 0; k2 < T; ++k2) {
+                    const int64_t o = j * N * N + (int64_t)(t + R * k2) * N + c;
+                    const float2 vv = cscale(X[k2], scale);
+                    v[o] = vv;
+                    ls_screen<K>(u[o], vv, __ldg(d + o), sgam, eps2, S, A, sd_, sa_, sb_);
+                }
+                double dv[NV];
+#pragma unroll
+                for (int kk = 0; kk < K; ++kk) {
+                    dv[kk] = (double)S[kk];
+                    dv[K + kk] = (double)A[kk];
+                }
+                tot += warp_reduce_scatter<NV>(dv, lane);
+                md += (double)sd_;
+                ma += (double)sa_;
+                mb += (double)sb_;
+            }
+        }
+        __syncthreads();
+    }
+    if (FWD) {
+        const double s2 = block_sum<512>(facc, &sred[0][0]);
+        if (tid == 0) part[blockIdx.x] = s2;
+        return;
+    }
+    constexpr int P = Log2<NV>::value;
+    constexpr int G = 32 >> P;
+    if ((lane & (G - 1)) == 0) sred[warp][lane >> (5 - P)] = tot;
+    md = warp_sum(md);
+    ma = warp_sum(ma);
+    mb = warp_sum(mb);
+    if (lane == 0) {
+        smom[warp][0] = md;
+        smom[warp][1] = ma;
+        smom[warp][2] = mb;
+    }
+    __syncthreads();
+    constexpr int WID = 2 * K + 3;
+    if (tid < NV) {
+        double a = 0.0;
+        for (int w = 0; w < 16; ++w) a += sred[w][tid];
+        part[(int64_t)blockIdx.x * WID + tid] = a;
+    } else if (tid < WID) {
+        double a = 0.0;
+        for (int w = 0; w < 16; ++w) a += smom[w][tid - NV];
+        part[(int64_t)blockIdx.x * WID + tid] = a;
+    }
+}
+
+// Batched 2-D FFT (ptyger_fft2, N = 256): pass 1 writes row transforms into `out`, pass 2 reads
+// them back column-wise and writes the final values in place.
+template <bool INV>
+__global__ void __launch_bounds__(512, 1) k_fft2_256(const float2* __restrict__ in, float2* __restrict__ out,
+                                                     int64_t batch) {
+    using namespace n256;
+    extern __shared__ float2 smem[];
+    float2* buf = smem;
+    float2* tw = smem + BUF;
+    build_twiddles<N>(tw);
+    __syncthreads();
+    const int tid = threadIdx.x;
+    const float scale = 1.0f / (float)N;
+    for (int64_t j = blockIdx.x; j < batch; j += gridDim.x) {
+        float2* oj = out + j * N * N;
+#pragma unroll 1
+        for (int rb = 0; rb < N / ROWB; ++rb) {
+            const int row = rb * ROWB + tid / T, t = tid % T;
+            const float2* src = in + j * N * N + (int64_t)row * N + t;
+            float2 x[R];
+#pragma unroll
+            for (int n1 = 0; n1 < R; ++n1) x[n1] = ldg2(src + T * n1);
+            float2* srow = buf + (tid / T) * LD;
+            __syncwarp();
+            row_fft_regs<N, INV>(x, srow, t, tw);
+            float2* dst = oj + (int64_t)row * N + t;
+#pragma unroll
+            for (int k2 = 0; k2 < T; ++k2) dst[R * k2] = x[k2];
+        }
+        __syncthreads();
+#pragma unroll 1
+        for (int cb = 0; cb < N / COLB; ++cb) {
+            float2 X[16];
+            int c;
+            n256_column<INV>(oj, cb, buf, tw, X, c);
+            const int t = tid >> 5;
+#pragma unroll
+            for (int k2 = 0; k2 < T; ++k2) oj[(int64_t)(t + R * k2) * N + c] = cscale(X[k2], scale);
+        }
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------------------------ launchers
+template <typename F>
+static int n256_smem(F* f) {
+    return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)n256::SMEM) == cudaSuccess ? 0
+                                                                                                              : -1;
+}
+
+int launch_grad256(const Geometry& g, float2* u, float2* v, const float* d, const float2* probe, const DevState* st,
+                   float eps, int grid, cudaStream_t s) {
+    if (n256_smem(k_grad256)) return -1;
+    k_grad256<<<grid, 512, n256::SMEM, s>>>(g, u, v, d, probe, st, eps);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+int launch_ls256(const Geometry& g, const float2* eta, const float2* probe, const int2* pos, const int* order,
+                 const float2* u, float2* v, const float* d, const SolverCfg& c, double* part, int grid,
+                 const DevState* st, cudaStream_t s) {
+    float2* uu = const_cast<float2*>(u);
+    if (c.K == 8) {
+        if (n256_smem(k_lsfwd256<8, false>)) return -1;
+        k_lsfwd256<8, false><<<grid, 512, n256::SMEM, s>>>(g, eta, probe, pos, order, uu, v, d, c, part, st);
+    } else if (c.K == 16) {
+        if (n256_smem(k_lsfwd256<16, false>)) return -1;
+        k_lsfwd256<16, false><<<grid, 512, n256::SMEM, s>>>(g, eta, probe, pos, order, uu, v, d, c, part, st);
+    } else {
+        return -2;
+    }
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+int launch_fwd256(const Geometry& g, const float2* psi, const float2* probe, const int2* pos, const int* order,
+                  const float* d, float2* u, double* part, int grid, float eps, cudaStream_t s) {
+    SolverCfg c{};
+    c.eps = eps;
+    c.gamma0 = 1.0;
+    c.tau = 0.5;
+    c.K = 1;
+    if (n256_smem(k_lsfwd256<1, true>)) return -1;
+    k_lsfwd256<1, true><<<grid, 512, n256::SMEM, s>>>(g, psi, probe, pos, order, u, nullptr, d, c, part, nullptr);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+int launch_fft2_256(const float2* in, float2* out, int64_t batch, bool inv, cudaStream_t s) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int grid = (int)(batch < sms ? batch : sms);
+    if (grid <= 0) return 0;
+    if (inv) {
+        if (n256_smem(k_fft2_256<true>)) return -1;
+        k_fft2_256<true><<<grid, 512, n256::SMEM, s>>>(in, out, batch);
+    } else {
+        if (n256_smem(k_fft2_256<false>)) return -1;
+        k_fft2_256<false><<<grid, 512, n256::SMEM, s>>>(in, out, batch);
+    }
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+}  // namespace pty

@@ -37,8 +37,11 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t phase) {
     return ok != 0;
 }
 
+// Bounded wait: a protocol bug becomes a launch failure (trap) after ~seconds, never a hung GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    uint32_t spins = 0;
     while (!mbar_try_wait(bar, phase)) {
+        if (++spins == (1u << 26)) __trap();
     }
 }
 

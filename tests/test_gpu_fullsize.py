@@ -1,0 +1,99 @@
+"""Parity at BASELINE.json's paper-scale view (4096^2 object, 128^2 detector, 24 964 frames), in
+the launch configuration bench.py times, on outputs the float64 oracle can compute one by one:
+
+* u = G psi_0 on sampled frames (rel L2 <= 2e-6);
+* grad F at sampled object pixels, each recomputed from only the frames whose window covers it
+  (|error| <= 1e-4 of the RMS of the sampled gradient values);
+* the first iteration's line-search partials DeltaF_k over ALL frames (oracle evaluated frame
+  chunk by frame chunk on the GPU's eta): within max(1e-5 sum|terms|, 2 x the screening bound),
+  and the same accepted trial.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import ptycho as O  # noqa: E402
+from paper_2106_07575_b200 import inputs as I  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def paper_run():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import bench
+    from paper_2106_07575_b200 import _lib as L
+    w = I.WORKLOADS["paper"]
+    dev = torch.device("cuda", 0)
+    psi_true, p, scan, d = bench.synth_device(w, dev)
+    psi0 = torch.ones((w.H, w.W), dtype=torch.complex64, device=dev)
+    pt = L.Ptyger(psi0, torch.from_numpy(p.astype(np.complex64)).to(dev), scan, d)
+    u0 = pt.get_farfield()
+    tr = pt.iterate(1)[0]
+    g = pt.get_gradient()
+    _, _, eta, _, _ = pt.get_state()
+    dF, bnd = pt.get_ls_partials(with_bound=True)
+    dh = d.cpu().numpy()
+    pt.close()
+    return dict(w=w, p=p.astype(np.complex64).astype(np.complex128), scan=scan, d=dh, u0=u0, tr=tr, g=g, eta=eta,
+                dF=dF, bnd=bnd)
+
+
+def test_farfield_sampled_frames(paper_run):
+    r = paper_run
+    rng = np.random.default_rng(0)
+    idx = rng.choice(len(r["scan"]), 16, replace=False)
+    psi0 = np.ones((r["w"].H, r["w"].W), np.complex128)
+    ref = O.forward_G(psi0, r["p"], r["scan"][idx])
+    got = r["u0"][idx]
+    assert np.linalg.norm(got - ref) <= 2e-6 * np.linalg.norm(ref)
+
+
+def test_gradient_sampled_pixels(paper_run):
+    r = paper_run
+    scan, p, d, N = r["scan"], r["p"], r["d"], r["w"].N
+    rng = np.random.default_rng(1)
+    lo, hi = int(scan[:, 0].min()), int(scan[:, 0].max()) + N
+    pix = np.stack([rng.integers(lo, hi, 48), rng.integers(lo, hi, 48)], 1)
+    pix = np.concatenate([pix, [[lo, lo], [hi - 1, hi - 1], [lo + N // 2, hi - 1]]])
+    psi0 = np.ones((r["w"].H, r["w"].W), np.complex128)
+    refs, gots = [], []
+    for (y, x) in pix:
+        cov = np.where((scan[:, 0] <= y) & (y < scan[:, 0] + N) & (scan[:, 1] <= x) & (x < scan[:, 1] + N))[0]
+        acc = 0j
+        for j in cov:
+            u = O.ufft2(p * O.extract(psi0, scan[j], N))
+            yj = np.conj(p) * O.uifft2(O.residual(u, d[j].astype(np.float64)))
+            acc += yj[y - scan[j, 0], x - scan[j, 1]]
+        refs.append(acc)
+        gots.append(complex(r["g"][y, x]))
+    refs, gots = np.array(refs), np.array(gots)
+    rms = np.sqrt(np.mean(np.abs(refs) ** 2))
+    assert np.max(np.abs(gots - refs)) <= 1e-4 * rms
+
+
+def test_first_line_search_all_frames(paper_run):
+    r = paper_run
+    scan, p, d, N = r["scan"], r["p"], r["d"], r["w"].N
+    eta = r["eta"].astype(np.complex128)
+    K = len(r["dF"])
+    gam = [0.5 ** k for k in range(K)]
+    tot = np.zeros(K)
+    scale = np.zeros(K)
+    psi0 = np.ones((N, N), np.complex128)
+    u = O.ufft2(p * psi0)                       # psi_0 = 1: the same far field for every frame
+    for a in range(0, len(scan), 1024):
+        sc = scan[a:a + 1024]
+        v = O.forward_G(eta, p, sc)
+        dd = d[a:a + 1024].astype(np.float64)
+        uu = np.broadcast_to(u, v.shape)
+        for k in range(K):
+            tot[k] += O.ls_delta(uu, v, dd, gam[k])
+            scale[k] += np.sum(np.abs(uu + gam[k] * v) ** 2) + np.sum(np.abs(uu) ** 2) + \
+                2 * np.sum(np.abs(dd * np.log(np.maximum(np.abs(uu), 1e-30))))
+    for k in range(K):
+        assert abs(r["dF"][k] - tot[k]) <= max(1e-5 * scale[k], 2 * r["bnd"][k]), (k, r["dF"][k], tot[k])
+    kref = next((k for k in range(K) if tot[k] <= 0), None)
+    if kref is not None:
+        assert r["tr"]["shrinks"] == kref

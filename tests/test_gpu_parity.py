@@ -46,6 +46,7 @@ FIXTURES = {
     "n32": (96, 32, 9, 8, 1, 3, 1e3, True),        # 81 frames: FPB=8 ragged tail
     "n64": (192, 64, 9, 16, 2, 4, 1e3, True),      # 81 frames: FPB=2 ragged tail, 36 tiles
     "n128": (320, 128, 7, 32, 2, 5, 1e3, True),    # 49 frames, 100 tiles
+    "n256": (384, 256, 5, 32, 2, 6, 1e3, True),    # 25 frames, two-pass FFT through the v slot
 }
 
 
@@ -56,7 +57,7 @@ def get_fixture(name):
 
 # ------------------------------------------------------------------ FFT library
 
-@pytest.mark.parametrize("N", [16, 32, 64, 128])
+@pytest.mark.parametrize("N", [16, 32, 64, 128, 256])
 @pytest.mark.parametrize("inverse", [False, True])
 def test_fft2_matches_oracle_and_cufft(L, N, inverse):
     batch = 37
