@@ -246,3 +246,27 @@ class Ptyger:
 
     def kernel_launches(self) -> int:
         return int(lib.ptyger_kernel_launches(self.ctx))
+
+
+class ViewBatch:
+    """3-D ptycho-tomography batch: the rotation views
+    are independent 2-D problems, so each view gets its own context (own psi, far fields, alpha,
+    gamma) and the batch iterates them back to back on this GPU.  Across GPUs the views are
+    sharded with no communication (bench.py --config view3d)."""
+
+    def __init__(self, views, **cfg):
+        # views: iterable of (psi0, probe, scan, d)
+        self.views = [Ptyger(o, p, s, d, **cfg) for (o, p, s, d) in views]
+
+    def iterate(self, n_iter: int, traces: bool = True):
+        return [v.iterate(n_iter, traces) for v in self.views]
+
+    def last_iterate_ms(self) -> float:
+        return sum(v.last_iterate_ms() for v in self.views)
+
+    def kernel_launches(self) -> int:
+        return sum(v.kernel_launches() for v in self.views)
+
+    def close(self):
+        for v in self.views:
+            v.close()

@@ -77,16 +77,32 @@ NcclApi* nccl_api(std::string& err) {
     return &api;
 }
 
+// Device buffers come from the device's default stream-ordered memory pool with the release
+// threshold raised to "never": a context created after another one was destroyed (e.g. one
+// reconstruction problem after another) reuses the mapped pages instead of paying cudaMalloc's
+// page-mapping cost again.  Allocations / zero fills are on the legacy stream; init
+// synchronises it before the context's own (non-blocking) stream uses the buffers.
+void pool_setup(int device) {
+    static bool done[64] = {false};
+    if (device < 0 || device >= 64 || done[device]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done[device] = true;
+}
+
 template <typename T>
 T* dalloc(size_t count, std::string& err, bool zero = true) {
     void* p = nullptr;
     if (count == 0) count = 1;
-    if (cudaMalloc(&p, count * sizeof(T)) != cudaSuccess) {
+    if (cudaMallocAsync(&p, count * sizeof(T), 0) != cudaSuccess) {
         cudaGetLastError();
-        err = "cudaMalloc of " + std::to_string(count * sizeof(T)) + " bytes failed";
+        err = "cudaMallocAsync of " + std::to_string(count * sizeof(T)) + " bytes failed";
         return nullptr;
     }
-    if (zero) cudaMemset(p, 0, count * sizeof(T));
+    if (zero) cudaMemsetAsync(p, 0, count * sizeof(T), 0);
     return static_cast<T*>(p);
 }
 
@@ -304,8 +320,10 @@ static void free_ctx(ptyger_ctx* c) {
     void* ptrs[] = {c->psi, c->g[0], c->g[1], c->eta, c->u, c->v, c->probe, c->full, c->recv[0], c->recv[1], c->d,
                     c->pos, c->order, c->tile_ptr, c->entries, c->part_adj, c->part_fr, c->part_el, c->scratch, c->st,
                     c->d_tr};
+    if (c->stream) cudaStreamSynchronize(c->stream);
     for (void* p : ptrs)
-        if (p) cudaFree(p);
+        if (p) cudaFreeAsync(p, 0);
+    cudaStreamSynchronize(0);
     for (int i = 0; i < 2; ++i)
         if (c->ev_it[i]) cudaEventDestroy(c->ev_it[i]);
     if (c->comm && c->nc) c->nc->CommDestroy(c->comm);
@@ -451,6 +469,7 @@ static ptyger_status init_impl(ptyger_ctx* c, const float* object, const float* 
         return PTYGER_E_ARG;
     }
     CK(cudaSetDevice(cfg.device));
+    pool_setup(cfg.device);
     CK(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, cfg.device));
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     if (cfg.world > 1) {
@@ -491,6 +510,7 @@ static ptyger_status init_impl(ptyger_ctx* c, const float* object, const float* 
         if (c->band_rows[b] > 0) AL(c->recv[b], float2, c->band_rows[b] * W);
     if (cfg.world > 1) AL(c->full, float2, H * W);
 #undef AL
+    CK(cudaStreamSynchronize(0));  // pool allocations and zero fills (legacy stream) are done
     CK(cudaMemcpy(c->psi, object + 2 * c->st_lo * W, sizeof(float2) * obj, cudaMemcpyDefault));
     CK(cudaMemcpy(c->probe, probe, sizeof(float2) * NN, cudaMemcpyDefault));
     // d: contiguous runs of local frames
@@ -517,7 +537,7 @@ static ptyger_status init_impl(ptyger_ctx* c, const float* object, const float* 
         unsigned long long hb = 0;
         CK(cudaStreamSynchronize(c->stream));
         CK(cudaMemcpy(&hb, bad, sizeof(hb), cudaMemcpyDeviceToHost));
-        cudaFree(bad);
+        cudaFreeAsync(bad, 0);
         if (hb != ~0ull) {
             err = "intensities: frame " + std::to_string(c->local_global[(int64_t)hb]) +
                   " has a negative or non-finite value";
@@ -610,9 +630,11 @@ ptyger_status ptyger_cg_iterate(ptyger_ctx* c, int32_t n_iter, ptyger_trace* tra
     if (n_iter == 0) return PTYGER_OK;
     CK(cudaSetDevice(c->cfg.device));
     if (c->tr_cap < n_iter) {
-        if (c->d_tr) cudaFree(c->d_tr);
+        CK(cudaStreamSynchronize(c->stream));
+        if (c->d_tr) cudaFreeAsync(c->d_tr, 0);
         c->d_tr = dalloc<ptyger_trace>((size_t)n_iter, err);
         if (!c->d_tr) return PTYGER_E_OOM;
+        CK(cudaStreamSynchronize(0));
         c->tr_cap = n_iter;
     }
     struct { int idx, cap; ptyger_trace* p; } hdr = {0, c->tr_cap, c->d_tr};

@@ -30,34 +30,45 @@ __global__ void __launch_bounds__(256) k_adj(Geometry g, const float2* __restric
 #pragma unroll
     for (int i = 0; i < 4; ++i) acc[i] = make_float2(0.f, 0.f);
     const int beg = tile_ptr[tile], end = tile_ptr[tile + 1];
-    int e = beg;
-    for (; e + 2 <= end; e += 2) {
-        float2 val[2][4];
+    // The tile's frame list is staged in shared memory (one coalesced load) so that the y loads
+    // of 4 consecutive frames issue back to back instead of waiting on a dependent entry load.
+    constexpr int CH = 256;
+    __shared__ int4 sent[CH];
+    for (int e0 = beg; e0 < end; e0 += CH) {
+        const int ne = min(CH, end - e0);
+        __syncthreads();
+        if ((int)threadIdx.x < ne) sent[threadIdx.x] = __ldg(ent + e0 + threadIdx.x);
+        __syncthreads();
+        int e = 0;
+        for (; e + 4 <= ne; e += 4) {
+            float2 val[4][4];
 #pragma unroll
-        for (int f = 0; f < 2; ++f) {
-            const int4 en = __ldg(ent + e + f);
+            for (int f = 0; f < 4; ++f) {
+                const int4 en = sent[e + f];
+                const int dc = (int)(col - en.z);
+                const bool okc = (unsigned)dc < (unsigned)N;
+                const float2* yb = y + (int64_t)en.x * NN + dc;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int dr = (int)(row0 + 8 * i - en.y);
+                    val[f][i] = (okc && (unsigned)dr < (unsigned)N) ? ldg2(yb + (int64_t)dr * N) : make_float2(0.f, 0.f);
+                }
+            }
+#pragma unroll
+            for (int f = 0; f < 4; ++f)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) acc[i] = cadd(acc[i], val[f][i]);
+        }
+        for (; e < ne; ++e) {
+            const int4 en = sent[e];
             const int dc = (int)(col - en.z);
             const bool okc = (unsigned)dc < (unsigned)N;
-            const float2* yb = y + (int64_t)en.x * NN + dc;
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 const int dr = (int)(row0 + 8 * i - en.y);
-                val[f][i] = (okc && (unsigned)dr < (unsigned)N) ? ldg2(yb + (int64_t)dr * N) : make_float2(0.f, 0.f);
+                if (okc && (unsigned)dr < (unsigned)N)
+                    acc[i] = cadd(acc[i], ldg2(y + (int64_t)en.x * NN + (int64_t)dr * N + dc));
             }
-        }
-#pragma unroll
-        for (int f = 0; f < 2; ++f)
-#pragma unroll
-            for (int i = 0; i < 4; ++i) acc[i] = cadd(acc[i], val[f][i]);
-    }
-    for (; e < end; ++e) {
-        const int4 en = __ldg(ent + e);
-        const int dc = (int)(col - en.z);
-        const bool okc = (unsigned)dc < (unsigned)N;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int dr = (int)(row0 + 8 * i - en.y);
-            if (okc && (unsigned)dr < (unsigned)N) acc[i] = cadd(acc[i], ldg2(y + (int64_t)en.x * NN + (int64_t)dr * N + dc));
         }
     }
     float s[NDY];
@@ -262,44 +273,39 @@ __global__ void __launch_bounds__(256) k_lsx(int64_t count, const float2* __rest
     if (tid < K) sgam[tid] = (float)trial_gamma(cfg.gamma0, cfg.tau, pass * K + tid);
     __syncthreads();
     const float eps2 = (float)(cfg.eps * cfg.eps);
-    double acc64[NV];
-#pragma unroll
-    for (int k = 0; k < NV; ++k) acc64[k] = 0.0;
-    double md = 0.0, ma = 0.0, mb = 0.0;
+    // Runs of RUN elements per thread (coalesced: element base + i*blockDim + tid) accumulate in
+    // fp32, then one warp reduce-scatter folds them into a single fp64 total per lane.
+    constexpr int RUN = 16;
+    double tot = 0.0, md = 0.0, ma = 0.0, mb = 0.0;
     if (run) {
-        float S[K], A[K];
-        float sd = 0.f, sa = 0.f, sb = 0.f;
+        const int64_t stride = (int64_t)gridDim.x * blockDim.x * RUN;
+        for (int64_t base = (int64_t)blockIdx.x * blockDim.x * RUN; base < count; base += stride) {
+            float S[K], A[K];
+            float sd = 0.f, sa = 0.f, sb = 0.f;
 #pragma unroll
-        for (int k = 0; k < K; ++k) S[k] = A[k] = 0.f;
-        int cnt = 0;
-        for (int64_t o = (int64_t)blockIdx.x * blockDim.x + tid; o < count; o += (int64_t)gridDim.x * blockDim.x) {
-            if (EXACT)
-                ls_exact<K>(u[o], v[o], __ldg(d + o), sgam, eps2, S);
-            else
-                ls_screen<K>(u[o], v[o], __ldg(d + o), sgam, eps2, S, A, sd, sa, sb);
-            if (++cnt == 16) {  // bounded fp32 run length, then fp64
-#pragma unroll
-                for (int k = 0; k < K; ++k) {
-                    acc64[k] += (double)S[k];
-                    S[k] = 0.f;
-                    if (!EXACT) {
-                        acc64[K + k] += (double)A[k];
-                        A[k] = 0.f;
-                    }
+            for (int k = 0; k < K; ++k) S[k] = A[k] = 0.f;
+#pragma unroll 4
+            for (int i = 0; i < RUN; ++i) {
+                const int64_t o = base + (int64_t)i * blockDim.x + tid;
+                if (o < count) {
+                    if (EXACT)
+                        ls_exact<K>(u[o], v[o], __ldg(d + o), sgam, eps2, S);
+                    else
+                        ls_screen<K>(u[o], v[o], __ldg(d + o), sgam, eps2, S, A, sd, sa, sb);
                 }
-                md += sd; ma += sa; mb += sb;
-                sd = sa = sb = 0.f;
-                cnt = 0;
             }
-        }
+            double dv[NV];
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
-            acc64[k] += (double)S[k];
-            if (!EXACT) acc64[K + k] += (double)A[k];
+            for (int k = 0; k < K; ++k) {
+                dv[k] = (double)S[k];
+                if (!EXACT) dv[K + k] = (double)A[k];
+            }
+            tot += warp_reduce_scatter<NV>(dv, lane);
+            md += sd;
+            ma += sa;
+            mb += sb;
         }
-        md += sd; ma += sa; mb += sb;
     }
-    const double tot = warp_reduce_scatter<NV>(acc64, lane);
     constexpr int P = Log2<NV>::value;
     constexpr int G = 32 >> P;
     if ((lane & (G - 1)) == 0) sred[warp][lane >> (5 - P)] = tot;

@@ -58,19 +58,30 @@ def test_gradient_sampled_pixels(paper_run):
     pix = np.stack([rng.integers(lo, hi, 48), rng.integers(lo, hi, 48)], 1)
     pix = np.concatenate([pix, [[lo, lo], [hi - 1, hi - 1], [lo + N // 2, hi - 1]]])
     psi0 = np.ones((r["w"].H, r["w"].W), np.complex128)
-    refs, gots = [], []
+    refs, r32s, gots = [], [], []
+    p32 = p.astype(np.complex64)
     for (y, x) in pix:
         cov = np.where((scan[:, 0] <= y) & (y < scan[:, 0] + N) & (scan[:, 1] <= x) & (x < scan[:, 1] + N))[0]
-        acc = 0j
+        acc, acc32 = 0j, 0j
         for j in cov:
             u = O.ufft2(p * O.extract(psi0, scan[j], N))
             yj = np.conj(p) * O.uifft2(O.residual(u, d[j].astype(np.float64)))
             acc += yj[y - scan[j, 0], x - scan[j, 1]]
+            # the same formula in plain float32 (the e32 yardstick of the parity protocol)
+            u32 = np.fft.fft2(p32, norm="ortho").astype(np.complex64)
+            a2 = (u32.real ** 2 + u32.imag ** 2).astype(np.float32)
+            q = np.where(a2 >= np.float32(1e-32), d[j] / np.where(a2 > 0, a2, 1), 0).astype(np.float32)
+            y32 = np.conj(p32) * np.fft.ifft2((u32 - q * u32).astype(np.complex64), norm="ortho")
+            acc32 += complex(y32[y - scan[j, 0], x - scan[j, 1]])
         refs.append(acc)
+        r32s.append(acc32)
         gots.append(complex(r["g"][y, x]))
-    refs, gots = np.array(refs), np.array(gots)
+    refs, r32s, gots = np.array(refs), np.array(r32s), np.array(gots)
     rms = np.sqrt(np.mean(np.abs(refs) ** 2))
-    assert np.max(np.abs(gots - refs)) <= 1e-4 * rms
+    # psi_0 = 1 makes u = F(p) tiny where d > 0 (the residual is ill-conditioned there, SURVEY
+    # 8(c).4): the per-pixel tolerance is 1e-4 rms plus 4x the float32 evaluation's own error
+    tol = 1e-4 * rms + 4 * np.abs(r32s - refs)
+    assert np.all(np.abs(gots - refs) <= tol), (np.abs(gots - refs) / tol).max()
 
 
 def test_first_line_search_all_frames(paper_run):
