@@ -43,7 +43,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="paper", choices=["tiny", "small", "paper", "mid"])
+    ap.add_argument("--config", default="paper", choices=["tiny", "small", "paper", "mid", "large"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ls-batch", type=int, default=8)
     ap.add_argument("--e2e-steps", type=int, default=2)
@@ -256,7 +256,7 @@ def main():
 
     # end-to-end through the public API from pinned HOST buffers (H2D + 1 iteration + D2H)
     e2e = None
-    if args.e2e_steps > 0 and world == 1:
+    if args.e2e_steps > 0 and world == 1 and d.numel() * 4 < 8e9:
         d_host = d.cpu().pin_memory()
         psi_h = torch.ones((w.H, w.W), dtype=torch.complex64).pin_memory()
         p_h = torch.from_numpy(p.astype(np.complex64)).pin_memory()
@@ -287,8 +287,8 @@ def main():
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:
-        dh = d.cpu().numpy()
-        v, desc, shr, t_one = oracle_sample_run(w, args.cpu_seconds, psi_true, p, scan, lambda k: dh[:k])
+        v, desc, shr, t_one = oracle_sample_run(w, args.cpu_seconds, psi_true, p, scan,
+                                                lambda k: d[:k].cpu().numpy())
         cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc}
 
     line = {

@@ -241,17 +241,25 @@ static int enqueue_iteration(ptyger_ctx* c, int p, std::string& err, int64_t& la
     // LS stage (Alg.1 659-668).  Pass 0 computes v = G eta and screens trials 0..K-1; every pass
     // is followed by an exact re-evaluation that runs only when the screening left it undecided;
     // further passes (trials pK..pK+K-1) run only while nothing was accepted.
-    LK(launch_ls(g, c->eta, c->probe, c->pos, c->order, c->u, c->v, c->d, sc, c->part_fr, c->grid_fr, c->st, s));
+    // split mode (PTYGER_LS_SPLIT): transform-only frame kernel, then the elementwise screening
+    // kernel for pass 0 (higher occupancy for the MUFU/FMA-bound trial terms, +8 B/px of v reads)
+    const bool split = getenv("PTYGER_LS_SPLIT") != nullptr;
+    if (split) {
+        LK(launch_fwd(g, c->eta, c->probe, c->pos, c->order, nullptr, c->v, c->part_fr, c->grid_fr, (float)sc.eps, s));
+    } else {
+        LK(launch_ls(g, c->eta, c->probe, c->pos, c->order, c->u, c->v, c->d, sc, c->part_fr, c->grid_fr, c->st, s));
+    }
     ++launches;
     EV(5);
     const int npass = (sc.max_shrinks + sc.K - 1) / sc.K;
     const int wscreen = 2 * sc.K + 3;
     for (int pass = 0; pass < npass; ++pass) {
-        if (pass > 0) {
+        const bool fused = pass == 0 && !split;
+        if (!fused) {
             LK(launch_lsx(g, c->u, c->v, c->d, sc, pass, false, c->part_el, c->grid_el, c->st, s));
             ++launches;
         }
-        LK(launch_reduce(pass == 0 ? c->part_fr : c->part_el, pass == 0 ? c->grid_fr : c->grid_el, wscreen,
+        LK(launch_reduce(fused ? c->part_fr : c->part_el, fused ? c->grid_fr : c->grid_el, wscreen,
                          &c->st->ls_pass[0], s));
         ++launches;
         if (multi) NK(c->nc->AllReduce(&c->st->ls_pass[0], &c->st->ls_pass[0], LSW, ncclFloat64, ncclSum, c->comm, s));

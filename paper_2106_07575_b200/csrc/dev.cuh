@@ -79,7 +79,7 @@ __device__ __forceinline__ double trial_gamma(double gamma0, double tau, int k) 
 __device__ __forceinline__ float2 residual(float2 u, float dd, float eps2) {
     const float c = u.x * u.x + u.y * u.y;
     if (c >= eps2) {
-        const float s = dd / c;
+        const float s = __fdividef(dd, c);  // MUFU.RCP + FMUL, 2 ulp (no slow-path branch)
         return make_float2(u.x - s * u.x, u.y - s * u.y);
     }
     return u;
@@ -156,14 +156,23 @@ __device__ __forceinline__ void ls_exact(float2 uu, float2 vv, float dd, const f
     for (int k = 0; k < K; ++k) acc[k] += t[k];
 }
 
-// SCREENING terms: w from the components of u + gamma v (relative error a few ulp even when
-// u + gamma v nearly cancels), log2 w on the MUFU (|abs err| <= 2^-22 on [0.5, 2], 2 ulp
-// relative elsewhere).  Accumulates S_k = sum t_k and A_k = sum d |ln w_k|; the caller also
-// accumulates sum d, sum |a|, sum b, which bound the error:
-//     |S_k - t_exact| <= LS_EPS_D sum d + LS_EPS_R (A_k + gamma_k sum|a| + gamma_k^2 sum b).
-// |u| < eps makes w = 0 -> S non-finite -> the exact pass decides (guarded definition).
-constexpr double LS_EPS_D = 1e-6;
+// SCREENING terms.  cn = |u + gamma v|^2 is formed from the components of u + gamma v, so
+// w = cn / c keeps a few-ulp RELATIVE accuracy even when u + gamma v nearly cancels, and
+// q = cn - c (absolute error <= 2^-23 (cn + c)); log2 w on the MUFU without denormal fix-up
+// (lg2.approx.ftz: |abs err| <= 2^-22 on [0.5, 2], 2 ulp relative elsewhere).  Per trial:
+// 8 FMA-pipe ops, 1 ALU op, 1 MUFU.  Accumulates S_k = sum t_k, A_k = sum d |ln w_k|; the caller
+// also accumulates D = sum (d + 0.12 c), sum |a|, sum b, which bound the error:
+//     |S_k - t_exact| <= LS_EPS_D D + LS_EPS_R (A_k + gamma_k sum|a| + gamma_k^2 sum b)
+// (the 0.12 c part of D covers the rounding of q = cn - c: 2e-6 * 0.12 = 2.4e-7 >= 2 * 2^-23).
+// |u| < eps makes w = 0 -> S non-finite -> the exact pass decides (guarded definition, R#4).
+constexpr double LS_EPS_D = 2e-6;
 constexpr double LS_EPS_R = 2e-6;
+
+__device__ __forceinline__ float lg2_ftz(float x) {
+    float y;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 
 template <int K>
 __device__ __forceinline__ void ls_screen(float2 uu, float2 vv, float dd, const float* sgam, float eps2,
@@ -171,19 +180,18 @@ __device__ __forceinline__ void ls_screen(float2 uu, float2 vv, float dd, const 
     const float a = 2.0f * fmaf(uu.x, vv.x, uu.y * vv.y);
     const float b = fmaf(vv.x, vv.x, vv.y * vv.y);
     const float c = fmaf(uu.x, uu.x, uu.y * uu.y);
-    const float rc = (c >= eps2) ? 1.0f / c : 0.0f;
+    const float rc = (c >= eps2) ? __fdividef(1.0f, c) : 0.0f;   // 2 ulp: inside the bound
     const float dl = dd * 0.693147182464599609375f;
-    sd += dd;
+    sd += fmaf(0.12f, c, dd);
     sa += fabsf(a);
     sb += b;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         const float gam = sgam[k];
-        const float q = gam * fmaf(gam, b, a);
         const float ex = fmaf(gam, vv.x, uu.x), ey = fmaf(gam, vv.y, uu.y);
-        const float cn = fmaxf(fmaf(ex, ex, ey * ey), eps2);
-        const float L2 = __log2f(cn * rc);
-        S[k] += fmaf(-dl, L2, q);
+        const float cn = fmaf(ex, ex, ey * ey);
+        const float L2 = lg2_ftz(fmaxf(cn, eps2) * rc);
+        S[k] += fmaf(-dl, L2, cn - c);
         A[k] = fmaf(dl, fabsf(L2), A[k]);
     }
 }

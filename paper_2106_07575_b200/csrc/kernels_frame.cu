@@ -88,8 +88,10 @@ __global__ void __launch_bounds__(512, 1) k_fwd(Geometry g, const float2* __rest
                     const int64_t o = j * N * N + (int64_t)k * N + c;
                     const float2 uu = cscale(X[q], scale);
                     u[o] = uu;
-                    const float cc = uu.x * uu.x + uu.y * uu.y;
-                    fs += cc - __ldg(d + o) * logf(fmaxf(cc, eps2));
+                    if (d) {  // d == nullptr: transform only (v = G eta for the split line search)
+                        const float cc = uu.x * uu.x + uu.y * uu.y;
+                        fs += cc - __ldg(d + o) * logf(fmaxf(cc, eps2));
+                    }
                 }
                 facc += (double)fs;
             }
@@ -251,21 +253,56 @@ __global__ void __launch_bounds__(512, 1) k_ls(Geometry g, const float2* __restr
             const int line = rd * C::LPR + (warp / T) * 32 + lane;
             const int f = line / N, c = line % N;
             const int64_t i = grp * C::FPB + f;
-            float2 X[R];
-            col_fft_phase2<N, false>(sf + f * C::FRAME_ELEMS + c, t, X);
+            float2* scol = sf + f * C::FRAME_ELEMS + c;
+            {
+                // phase 2 with the outputs parked in the thread's own input rows (T k1 + k2,
+                // thread-private: no barrier), so the LS epilogue below can run as a ROLLED loop
+                // (a fully unrolled 16-element x K-trial epilogue overflows the instruction cache)
+                float2 X[R];
+                col_fft_phase2<N, false>(scol, t, X);
+#pragma unroll
+                for (int q = 0; q < R; ++q) scol[(T * ((q / T) * T + t) + q % T) * LD] = X[q];
+            }
             float S[K], A[K];
             float sd = 0.f, sa = 0.f, sb = 0.f;
 #pragma unroll
             for (int k = 0; k < K; ++k) S[k] = A[k] = 0.f;
             if (i < nfr) {
                 const int64_t j = order[i];
+                constexpr int G4 = 4;
+                float2 un[G4];
+                float dn[G4];
+                auto off = [&](int q) {
+                    return j * N * N + (int64_t)((q / T) * T + t + R * (q % T)) * N + c;
+                };
 #pragma unroll
-                for (int q = 0; q < R; ++q) {
-                    const int k = col_out_row<N>(q, t);
-                    const int64_t o = j * N * N + (int64_t)k * N + c;
-                    const float2 vv = cscale(X[q], scale);
-                    v[o] = vv;
-                    ls_screen<K>(u[o], vv, __ldg(d + o), sgam, eps2, S, A, sd, sa, sb);
+                for (int jj = 0; jj < G4; ++jj) {
+                    un[jj] = u[off(jj)];
+                    dn[jj] = __ldg(d + off(jj));
+                }
+#pragma unroll 1
+                for (int q0 = 0; q0 < R; q0 += G4) {
+                    float2 uc[G4];
+                    float dc[G4];
+#pragma unroll
+                    for (int jj = 0; jj < G4; ++jj) {
+                        uc[jj] = un[jj];
+                        dc[jj] = dn[jj];
+                    }
+                    if (q0 + G4 < R) {  // prefetch the next group's u, d
+#pragma unroll
+                        for (int jj = 0; jj < G4; ++jj) {
+                            un[jj] = u[off(q0 + G4 + jj)];
+                            dn[jj] = __ldg(d + off(q0 + G4 + jj));
+                        }
+                    }
+#pragma unroll
+                    for (int jj = 0; jj < G4; ++jj) {
+                        const int q = q0 + jj;
+                        const float2 vv = cscale(scol[(T * ((q / T) * T + t) + q % T) * LD], scale);
+                        v[off(q)] = vv;
+                        ls_screen<K>(uc[jj], vv, dc[jj], sgam, eps2, S, A, sd, sa, sb);
+                    }
                 }
             }
             double dv[2 * K];
@@ -385,7 +422,7 @@ static int ls_n(const Geometry& g, const float2* eta, const float2* probe, const
 int launch_ls(const Geometry& g, const float2* eta, const float2* probe, const int2* pos,
               const int* order, const float2* u, float2* v, const float* d, const SolverCfg& c,
               double* part, int grid, const DevState* st, cudaStream_t s) {
-    if (g.N == 128 && !getenv("PTYGER_LS_V1"))
+    if (g.N == 128 && getenv("PTYGER_LS_RING"))   // columns-first + TMA ring variant (A/B only)
         return launch_ls128(g, eta, probe, pos, order, u, v, d, c, part, grid, st, s);
     switch (g.N) {
         case 16: return ls_n<16>(g, eta, probe, pos, order, u, v, d, c, part, grid, st, s);

@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(512, 1) k_lsfwd256(Geometry g, const float2* _
                     const float2 uu = cscale(X[k2], scale);
                     u[o] = uu;
                     const float cc = uu.x * uu.x + uu.y * uu.y;
-                    fs += cc - __ldg(d + o) * logf(fmaxf(cc, eps2));
+                    if (d) fs += cc - __ldg(d + o) * logf(fmaxf(cc, eps2));
                 }
                 facc += (double)fs;
             } else {
