@@ -67,7 +67,8 @@ typedef struct {
     double eps;           /* modulus guard, 1e-16 (R#4)                                   */
     int32_t max_shrinks;  /* trials per iteration before a stall (gamma = 0), 32 (R#9)    */
     int32_t direction;    /* PTYGER_DIR_*                                                 */
-    int32_t ls_batch;     /* K trials evaluated per pass over the frames, 8 or 16 (default 8) */
+    int32_t ls_batch;     /* K in [4, 16] (default 16): trials per extra LS pass over the frames and the
+                             cap of pass 0, whose trial count adapts on the device to k*_prev + 3 */
     int32_t device;       /* CUDA device ordinal                                          */
     int32_t rank;         /* this process's rank, 0..world-1                              */
     int32_t world;        /* number of ranks (one GPU each)                               */
@@ -89,7 +90,7 @@ typedef struct {
 } ptyger_trace;
 
 /* Fill cfg with the paper's defaults (gamma0 1, tau 0.5, t 0, eps 1e-16, max_shrinks 32,
- * direction DY, ls_batch 8, device 0, rank 0, world 1, nccl_id NULL). */
+ * direction DY, ls_batch 16, device 0, rank 0, world 1, nccl_id NULL). */
 void ptyger_config_default(ptyger_config* cfg);
 
 /*

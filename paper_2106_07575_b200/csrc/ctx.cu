@@ -251,8 +251,10 @@ static int enqueue_iteration(ptyger_ctx* c, int p, std::string& err, int64_t& la
     }
     ++launches;
     EV(5);
-    const int npass = (sc.max_shrinks + sc.K - 1) / sc.K;
-    const int wscreen = 2 * sc.K + 3;
+    // pass 0 evaluates keff trials (adaptive on the device, >= KMIN), later passes K each
+    const int rest = sc.max_shrinks > KMIN ? sc.max_shrinks - KMIN : 0;
+    const int npass = 1 + (rest + sc.K - 1) / sc.K;
+    const int wscreen = LSP;
     for (int pass = 0; pass < npass; ++pass) {
         const bool fused = pass == 0 && !split;
         if (!fused) {
@@ -265,8 +267,8 @@ static int enqueue_iteration(ptyger_ctx* c, int p, std::string& err, int64_t& la
         if (multi) NK(c->nc->AllReduce(&c->st->ls_pass[0], &c->st->ls_pass[0], LSW, ncclFloat64, ncclSum, c->comm, s));
         LK(launch_pick(c->st, sc, pass, 0, 0, s)); ++launches;
         LK(launch_lsx(g, c->u, c->v, c->d, sc, pass, true, c->part_el, c->grid_el, c->st, s)); ++launches;
-        LK(launch_reduce(c->part_el, c->grid_el, sc.K, &c->st->ls_pass[0], s)); ++launches;
-        if (multi) NK(c->nc->AllReduce(&c->st->ls_pass[0], &c->st->ls_pass[0], sc.K, ncclFloat64, ncclSum, c->comm, s));
+        LK(launch_reduce(c->part_el, c->grid_el, LSP, &c->st->ls_pass[0], s)); ++launches;
+        if (multi) NK(c->nc->AllReduce(&c->st->ls_pass[0], &c->st->ls_pass[0], KC, ncclFloat64, ncclSum, c->comm, s));
         LK(launch_pick(c->st, sc, pass, 1, pass == npass - 1, s)); ++launches;
     }
     // Update stage (Alg.1 672)
@@ -316,7 +318,7 @@ static int run_forward(ptyger_ctx* c, std::string& err) {
             return PTYGER_E_NCCL;
         }
     }
-    LK(launch_set_F(c->st, c->scratch, c->stream));
+    LK(launch_set_F(c->st, c->scratch, c->sc.K, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     return 0;
 }
@@ -349,7 +351,7 @@ void ptyger_config_default(ptyger_config* cfg) {
     cfg->eps = 1e-16;
     cfg->max_shrinks = 32;
     cfg->direction = PTYGER_DIR_DY;
-    cfg->ls_batch = 8;
+    cfg->ls_batch = 16;
     cfg->device = 0;
     cfg->rank = 0;
     cfg->world = 1;
@@ -574,11 +576,11 @@ ptyger_status ptyger_init(ptyger_ctx** out, const ptyger_config* cfg_in, const f
         ptyger_config_default(&cfg);
     if (!object || !probe || !scan || !intensities) return set_err(nullptr, PTYGER_E_ARG, "init: null input array");
     if (!(cfg.gamma0 > 0) || !(cfg.tau > 0 && cfg.tau < 1) || !(cfg.eps > 0) || cfg.max_shrinks < 1 ||
-        cfg.max_shrinks > SMAX || (cfg.ls_batch != 8 && cfg.ls_batch != 16) || cfg.direction < 0 ||
+        cfg.max_shrinks > SMAX || cfg.ls_batch < KMIN || cfg.ls_batch > KC || cfg.direction < 0 ||
         cfg.direction > 2 || cfg.world < 1 || cfg.rank < 0 || cfg.rank >= cfg.world ||
         (cfg.world > 1 && !cfg.nccl_id) || !std::isfinite(cfg.t))
         return set_err(nullptr, PTYGER_E_ARG,
-                       "init: bad config (need gamma0>0, 0<tau<1, eps>0, 1<=max_shrinks<=64, ls_batch in {8,16}, "
+                       "init: bad config (need gamma0>0, 0<tau<1, eps>0, 1<=max_shrinks<=64, 4<=ls_batch<=16, "
                        "direction in {0,1,2}, 0<=rank<world, nccl_id when world>1)");
     if (N != 16 && N != 32 && N != 64 && N != 128 && N != 256)
         return set_err(nullptr, PTYGER_E_ARG, "init: N must be 16, 32, 64, 128 or 256");

@@ -129,8 +129,9 @@ static __device__ __noinline__ float ls_term_slow(float a, float b, float c, flo
 
 // EXACT terms (accurate log1p, ~1.7e-7 relative): t_k = q_k - d log1p(q_k / c).  Branch-free
 // fast path; a lane needing the guarded definition sends its warp through ls_term_slow.
+// Trials k < cnt (cnt warp-uniform) are evaluated; the others are skipped by uniform branches.
 template <int K>
-__device__ __forceinline__ void ls_exact(float2 uu, float2 vv, float dd, const float* sgam, float eps2,
+__device__ __forceinline__ void ls_exact(float2 uu, float2 vv, float dd, const float* sgam, int cnt, float eps2,
                                          float (&acc)[K]) {
     const float a = 2.0f * fmaf(uu.x, vv.x, uu.y * vv.y);
     const float b = fmaf(vv.x, vv.x, vv.y * vv.y);
@@ -140,16 +141,20 @@ __device__ __forceinline__ void ls_exact(float2 uu, float2 vv, float dd, const f
     float t[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-        const float gam = sgam[k];
-        const float q = gam * fmaf(gam, b, a);
-        const float z = q * rc;
-        bad |= (c + q < eps2) | (z <= -0.999f);
-        t[k] = fmaf(-dd, log1p_poly(fmaxf(z, -0.999f)), q);
+        t[k] = 0.f;
+        if (k < cnt) {
+            const float gam = sgam[k];
+            const float q = gam * fmaf(gam, b, a);
+            const float z = q * rc;
+            bad |= (c + q < eps2) | (z <= -0.999f);
+            t[k] = fmaf(-dd, log1p_poly(fmaxf(z, -0.999f)), q);
+        }
     }
     if (__any_sync(__activemask(), bad)) {
         if (bad) {
-#pragma unroll 1
-            for (int k = 0; k < K; ++k) t[k] = ls_term_slow(a, b, c, dd, sgam[k], eps2);
+#pragma unroll
+            for (int k = 0; k < K; ++k)
+                if (k < cnt) t[k] = ls_term_slow(a, b, c, dd, sgam[k], eps2);
         }
     }
 #pragma unroll
@@ -160,9 +165,10 @@ __device__ __forceinline__ void ls_exact(float2 uu, float2 vv, float dd, const f
 // w = cn / c keeps a few-ulp RELATIVE accuracy even when u + gamma v nearly cancels, and
 // q = cn - c (absolute error <= 2^-23 (cn + c)); log2 w on the MUFU without denormal fix-up
 // (lg2.approx.ftz: |abs err| <= 2^-22 on [0.5, 2], 2 ulp relative elsewhere).  Per trial:
-// 8 FMA-pipe ops, 1 ALU op, 1 MUFU.  Accumulates S_k = sum t_k, A_k = sum d |ln w_k|; the caller
-// also accumulates D = sum (d + 0.12 c), sum |a|, sum b, which bound the error:
-//     |S_k - t_exact| <= LS_EPS_D D + LS_EPS_R (A_k + gamma_k sum|a| + gamma_k^2 sum b)
+// 8 FMA-pipe ops, 2 ALU ops, 1 MUFU.  Accumulates S_k = sum t_k; the caller also accumulates
+// A = sum d max_k |ln w_k|, D = sum (d + 0.12 c), sum |a|, sum b, which bound the error of every
+// trial of the pass:
+//     |S_k - t_exact| <= LS_EPS_D D + LS_EPS_R (A + gamma_k sum|a| + gamma_k^2 sum b)
 // (the 0.12 c part of D covers the rounding of q = cn - c: 2e-6 * 0.12 = 2.4e-7 >= 2 * 2^-23).
 // |u| < eps makes w = 0 -> S non-finite -> the exact pass decides (guarded definition, R#4).
 constexpr double LS_EPS_D = 2e-6;
@@ -174,25 +180,61 @@ __device__ __forceinline__ float lg2_ftz(float x) {
     return y;
 }
 
+// Per-thread moments of the screening bound.
+struct LsMom {
+    float A = 0.f, D = 0.f, sa = 0.f, sb = 0.f;
+};
+
 template <int K>
-__device__ __forceinline__ void ls_screen(float2 uu, float2 vv, float dd, const float* sgam, float eps2,
-                                          float (&S)[K], float (&A)[K], float& sd, float& sa, float& sb) {
+__device__ __forceinline__ void ls_screen(float2 uu, float2 vv, float dd, const float* sgam, int cnt, float eps2,
+                                          float (&S)[K], LsMom& m) {
     const float a = 2.0f * fmaf(uu.x, vv.x, uu.y * vv.y);
     const float b = fmaf(vv.x, vv.x, vv.y * vv.y);
     const float c = fmaf(uu.x, uu.x, uu.y * uu.y);
     const float rc = (c >= eps2) ? __fdividef(1.0f, c) : 0.0f;   // 2 ulp: inside the bound
     const float dl = dd * 0.693147182464599609375f;
-    sd += fmaf(0.12f, c, dd);
-    sa += fabsf(a);
-    sb += b;
+    float amax = 0.f;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-        const float gam = sgam[k];
-        const float ex = fmaf(gam, vv.x, uu.x), ey = fmaf(gam, vv.y, uu.y);
-        const float cn = fmaf(ex, ex, ey * ey);
-        const float L2 = lg2_ftz(fmaxf(cn, eps2) * rc);
-        S[k] += fmaf(-dl, L2, cn - c);
-        A[k] = fmaf(dl, fabsf(L2), A[k]);
+        if (k < cnt) {
+            const float gam = sgam[k];
+            const float ex = fmaf(gam, vv.x, uu.x), ey = fmaf(gam, vv.y, uu.y);
+            const float cn = fmaf(ex, ex, ey * ey);
+            const float L2 = lg2_ftz(fmaxf(cn, eps2) * rc);
+            S[k] += fmaf(-dl, L2, cn - c);
+            amax = fmaxf(amax, fabsf(L2));
+        }
+    }
+    m.A = fmaf(dl, amax, m.A);
+    m.D += fmaf(0.12f, c, dd);
+    m.sa += fabsf(a);
+    m.sb += b;
+}
+
+// Block-level output of the screening partials: per-lane fp64 running total `tot` of entry
+// lane >> (5 - log2 K) of S (after warp_reduce_scatter<K>), per-thread fp64 moments.  Writes
+// [S_0..S_{K-1} | A, D, sum|a|, sum b] for this CTA.  sred: [NW][K], smom: [NW][4].
+template <int K, int NW>
+__device__ __forceinline__ void ls_block_out(double tot, const double (&mom)[4], double (*sred)[K],
+                                             double (*smom)[4], double* __restrict__ part) {
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    constexpr int P = Log2<K>::value;
+    constexpr int G = 32 >> P;
+    if ((lane & (G - 1)) == 0) sred[warp][lane >> (5 - P)] = tot;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const double w = warp_sum(mom[i]);
+        if (lane == 0) smom[warp][i] = w;
+    }
+    __syncthreads();
+    if (tid < K) {
+        double s = 0.0;
+        for (int w = 0; w < NW; ++w) s += sred[w][tid];
+        part[(int64_t)blockIdx.x * (K + 4) + tid] = s;
+    } else if (tid < K + 4) {
+        double s = 0.0;
+        for (int w = 0; w < NW; ++w) s += smom[w][tid - K];
+        part[(int64_t)blockIdx.x * (K + 4) + tid] = s;
     }
 }
 

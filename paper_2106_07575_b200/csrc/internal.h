@@ -7,10 +7,12 @@
 
 namespace pty {
 
-constexpr int KMAX = 32;     // max LS trials per pass
+constexpr int KC = 16;       // LS trial capacity of one pass over the frames
+constexpr int KMIN = 4;      // smallest adaptive pass-0 trial count
 constexpr int SMAX = 64;     // max trials per iteration (max_shrinks bound)
 constexpr int NDY = 6;       // DY partial sums per tile
-constexpr int LSW = 2 * KMAX + 8;  // LS partial vector: [S | A | sum d, sum|a|, sum b], eta^2 at LS_ETA
+constexpr int LSP = KC + 4;  // screening partials: [S_0..S_{KC-1} | A, D, sum|a|, sum b]
+constexpr int LSW = LSP + 4; // reduced LS vector in DevState (eta^2 at LS_ETA)
 constexpr int LS_ETA = LSW - 1;
 
 // Device-resident scalar state of the iteration (all decisions are taken on the device).
@@ -32,6 +34,7 @@ struct DevState {
     int stalled;
     int numeric_error;       // 0 = ok; else stage code (1 DIR, 2 LS, 3 F)
     int err_iter;
+    int keff;                // trials of LS pass 0 this iteration (adaptive: k*_prev + 3 in [KMIN, K])
     int need_exact;          // pass + 1 when the screening pick left that pass undecided
     int k_unc;               // first undecided trial
     int n_exact;             // exact re-evaluations so far (diagnostic)
@@ -51,8 +54,16 @@ struct Geometry {
 
 struct SolverCfg {
     double gamma0, tau, t, eps;
-    int max_shrinks, direction, K;
+    int max_shrinks, direction, K;   // K = trials per extra pass and cap of the adaptive pass 0 (<= KC)
 };
+
+// Trials [base, base + count) evaluated by LS pass p (host and device agree on this rule).
+__host__ __device__ inline void ls_pass_range(int pass, int keff, const SolverCfg& c, int& base, int& count) {
+    base = pass == 0 ? 0 : keff + (pass - 1) * c.K;
+    count = pass == 0 ? keff : c.K;
+    if (base + count > c.max_shrinks) count = c.max_shrinks - base;
+    if (count < 0) count = 0;
+}
 
 // -------- kernel launchers (kernels.cu) ------------------------------------------------
 int launch_fft2(const float2* in, float2* out, int N, int64_t batch, bool inverse, cudaStream_t s);
@@ -63,9 +74,6 @@ int launch_grad(const Geometry& g, float2* u, float2* v, const float* d, const f
                 const int* order, const DevState* st, float eps, int grid, cudaStream_t s);
 int launch_grad128(const Geometry& g, float2* u, float2* v, const float* d, const float2* probe,
                    const DevState* st, float eps, int grid, cudaStream_t s);
-int launch_ls128(const Geometry& g, const float2* eta, const float2* probe, const int2* pos, const int* order,
-                 const float2* u, float2* v, const float* d, const SolverCfg& c, double* part, int grid,
-                 const DevState* st, cudaStream_t s);
 int launch_grad256(const Geometry& g, float2* u, float2* v, const float* d, const float2* probe, const DevState* st,
                    float eps, int grid, cudaStream_t s);
 int launch_ls256(const Geometry& g, const float2* eta, const float2* probe, const int2* pos, const int* order,
@@ -93,7 +101,7 @@ int launch_upd(const Geometry& g, float2* psi, const float2* eta, const DevState
 int launch_begin_iter(DevState* st, cudaStream_t s);
 int launch_validate_d(const float* d, int64_t count, int64_t frame_elems, unsigned long long* bad,
                       cudaStream_t s);
-int launch_set_F(DevState* st, const double* src, cudaStream_t s);
+int launch_set_F(DevState* st, const double* src, int keff0, cudaStream_t s);
 int launch_band_add(float2* gcur, const float2* recv, int64_t row_lo, int64_t rows, int64_t W,
                     const float2* gprev, const float2* eta, int64_t own_lo, int64_t own_hi,
                     double* part, int grid, cudaStream_t s);

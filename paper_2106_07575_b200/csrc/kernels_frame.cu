@@ -190,10 +190,11 @@ __global__ void __launch_bounds__(512, 1) k_grad(Geometry g, float2* __restrict_
 
 // ----------------------------------------------------------------------------------------
 // k_ls: LS stage first pass (Alg.1 659-668 with Eq.7): v_j = F(p * eta[window s_j]) written
-// to HBM, then for K trials gamma_k = gamma0 tau^k the SCREENING terms (dev.cuh ls_screen)
-// against (u, d); per-CTA fp64 partials [S_0..S_{K-1}, A_0..A_{K-1}, sum d, sum|a|, sum b].
+// to HBM, then the SCREENING terms (dev.cuh ls_screen) of the pass-0 trials gamma_k,
+// k < keff (adaptive, read from the device state) against (u, d); per-CTA fp64 partials
+// [S_0..S_{KC-1} | A, D, sum|a|, sum b].
 // ----------------------------------------------------------------------------------------
-template <int N, int K>
+template <int N>
 __global__ void __launch_bounds__(512, 1) k_ls(Geometry g, const float2* __restrict__ eta,
                                                const float2* __restrict__ probe, const int2* __restrict__ pos,
                                                const int* __restrict__ order, const float2* __restrict__ u,
@@ -205,20 +206,22 @@ __global__ void __launch_bounds__(512, 1) k_ls(Geometry g, const float2* __restr
     extern __shared__ float2 smem[];
     float2* sf = smem;
     float2* tw = smem + C::FPB * C::FRAME_ELEMS;
-    __shared__ double sred[16][2 * K];
-    __shared__ double smom[16][3];
-    __shared__ float sgam[K];
+    __shared__ double sred[16][KC];
+    __shared__ double smom[16][4];
+    __shared__ float sgam[KC];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const bool err = st->numeric_error != 0;
+    int base, cnt;
+    ls_pass_range(0, st->keff, cfg, base, cnt);
     build_twiddles<N>(tw);
-    if (tid < K) sgam[tid] = (float)trial_gamma(cfg.gamma0, cfg.tau, tid);
+    if (tid < KC) sgam[tid] = (float)trial_gamma(cfg.gamma0, cfg.tau, base + tid);
     __syncthreads();
     const int64_t nfr = err ? 0 : g.n_local;
     const int64_t ngroups = (nfr + C::FPB - 1) / C::FPB;
     const float scale = 1.0f / (float)N;
     const float eps2 = (float)(cfg.eps * cfg.eps);
-    double tot = 0.0;  // running total of entry lane >> (5 - log2 2K) of [S | A]
-    double md = 0.0, ma = 0.0, mb = 0.0;
+    double tot = 0.0;  // running total of entry lane >> 1 of S
+    double mom[4] = {0.0, 0.0, 0.0, 0.0};
     for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
 #pragma unroll 1
         for (int rd = 0; rd < C::ROUNDS; ++rd) {
@@ -257,19 +260,19 @@ __global__ void __launch_bounds__(512, 1) k_ls(Geometry g, const float2* __restr
             {
                 // phase 2 with the outputs parked in the thread's own input rows (T k1 + k2,
                 // thread-private: no barrier), so the LS epilogue below can run as a ROLLED loop
-                // (a fully unrolled 16-element x K-trial epilogue overflows the instruction cache)
+                // (a fully unrolled 16-element x KC-trial epilogue overflows the instruction cache)
                 float2 X[R];
                 col_fft_phase2<N, false>(scol, t, X);
 #pragma unroll
                 for (int q = 0; q < R; ++q) scol[(T * ((q / T) * T + t) + q % T) * LD] = X[q];
             }
-            float S[K], A[K];
-            float sd = 0.f, sa = 0.f, sb = 0.f;
+            float S[KC];
+            LsMom m;
 #pragma unroll
-            for (int k = 0; k < K; ++k) S[k] = A[k] = 0.f;
+            for (int k = 0; k < KC; ++k) S[k] = 0.f;
             if (i < nfr) {
                 const int64_t j = order[i];
-                constexpr int G4 = 4;
+                constexpr int G4 = (R >= 4) ? 4 : R;
                 float2 un[G4];
                 float dn[G4];
                 auto off = [&](int q) {
@@ -301,46 +304,22 @@ __global__ void __launch_bounds__(512, 1) k_ls(Geometry g, const float2* __restr
                         const int q = q0 + jj;
                         const float2 vv = cscale(scol[(T * ((q / T) * T + t) + q % T) * LD], scale);
                         v[off(q)] = vv;
-                        ls_screen<K>(uc[jj], vv, dc[jj], sgam, eps2, S, A, sd, sa, sb);
+                        ls_screen<KC>(uc[jj], vv, dc[jj], sgam, cnt, eps2, S, m);
                     }
                 }
             }
-            double dv[2 * K];
+            double dv[KC];
 #pragma unroll
-            for (int k = 0; k < K; ++k) {
-                dv[k] = (double)S[k];
-                dv[K + k] = (double)A[k];
-            }
-            tot += warp_reduce_scatter<2 * K>(dv, lane);
-            md += (double)sd;
-            ma += (double)sa;
-            mb += (double)sb;
+            for (int k = 0; k < KC; ++k) dv[k] = (double)S[k];
+            tot += warp_reduce_scatter<KC>(dv, lane);
+            mom[0] += (double)m.A;
+            mom[1] += (double)m.D;
+            mom[2] += (double)m.sa;
+            mom[3] += (double)m.sb;
         }
         __syncthreads();
     }
-    // block reduction: lane-group leader of each entry writes per warp, then fixed-order sums
-    constexpr int P = Log2<2 * K>::value;
-    constexpr int G = 32 >> P;
-    if ((lane & (G - 1)) == 0) sred[warp][lane >> (5 - P)] = tot;
-    md = warp_sum(md);
-    ma = warp_sum(ma);
-    mb = warp_sum(mb);
-    if (lane == 0) {
-        smom[warp][0] = md;
-        smom[warp][1] = ma;
-        smom[warp][2] = mb;
-    }
-    __syncthreads();
-    constexpr int WID = 2 * K + 3;
-    if (tid < 2 * K) {
-        double s = 0.0;
-        for (int w = 0; w < 16; ++w) s += sred[w][tid];
-        part[(int64_t)blockIdx.x * WID + tid] = s;
-    } else if (tid < WID) {
-        double s = 0.0;
-        for (int w = 0; w < 16; ++w) s += smom[w][tid - 2 * K];
-        part[(int64_t)blockIdx.x * WID + tid] = s;
-    }
+    ls_block_out<KC, 16>(tot, mom, sred, smom, part);
 }
 
 
@@ -398,32 +377,19 @@ int launch_grad(const Geometry& g, float2* u, float2* v, const float* d, const f
     return -2;
 }
 
-template <int N, int K>
-static int ls_nk(const Geometry& g, const float2* eta, const float2* probe, const int2* pos,
-                 const int* order, const float2* u, float2* v, const float* d, const SolverCfg& c,
-                 double* part, int grid, const DevState* st, cudaStream_t s) {
-    using C = FFTCfg<N>;
-    if (set_smem(k_ls<N, K>, C::SMEM_BYTES)) return -1;
-    k_ls<N, K><<<grid, C::NT, C::SMEM_BYTES, s>>>(g, eta, probe, pos, order, u, v, d, c, part, st);
-    return cudaGetLastError() == cudaSuccess ? 0 : -1;
-}
-
 template <int N>
 static int ls_n(const Geometry& g, const float2* eta, const float2* probe, const int2* pos,
                 const int* order, const float2* u, float2* v, const float* d, const SolverCfg& c,
                 double* part, int grid, const DevState* st, cudaStream_t s) {
-    switch (c.K) {
-        case 8: return ls_nk<N, 8>(g, eta, probe, pos, order, u, v, d, c, part, grid, st, s);
-        case 16: return ls_nk<N, 16>(g, eta, probe, pos, order, u, v, d, c, part, grid, st, s);
-    }
-    return -2;
+    using C = FFTCfg<N>;
+    if (set_smem(k_ls<N>, C::SMEM_BYTES)) return -1;
+    k_ls<N><<<grid, C::NT, C::SMEM_BYTES, s>>>(g, eta, probe, pos, order, u, v, d, c, part, st);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
 int launch_ls(const Geometry& g, const float2* eta, const float2* probe, const int2* pos,
               const int* order, const float2* u, float2* v, const float* d, const SolverCfg& c,
               double* part, int grid, const DevState* st, cudaStream_t s) {
-    if (g.N == 128 && getenv("PTYGER_LS_RING"))   // columns-first + TMA ring variant (A/B only)
-        return launch_ls128(g, eta, probe, pos, order, u, v, d, c, part, grid, st, s);
     switch (g.N) {
         case 16: return ls_n<16>(g, eta, probe, pos, order, u, v, d, c, part, grid, st, s);
         case 32: return ls_n<32>(g, eta, probe, pos, order, u, v, d, c, part, grid, st, s);

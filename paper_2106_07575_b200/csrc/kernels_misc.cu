@@ -174,9 +174,10 @@ __global__ void __launch_bounds__(1024) k_reduce(const double* __restrict__ part
     }
 }
 
-__global__ void k_set_F(DevState* st, const double* src) {
+__global__ void k_set_F(DevState* st, const double* src, int keff0) {
     st->F = src[0];
     st->gamma = 0.0;
+    st->keff = keff0;  // no previous k*: the first line search evaluates the full pass capacity
 }
 
 __global__ void k_begin_iter(DevState* st) {
@@ -253,100 +254,81 @@ __global__ void __launch_bounds__(256) k_eta(Geometry g, const float2* __restric
 }
 
 
-// Further LS passes over the cached (u, v, d): trials pass*K .. pass*K+K-1.  SCREEN mode runs
-// unless an earlier pass accepted; EXACT mode runs only when the screening pick left this pass
-// undecided (st->need_exact == pass + 1).  Partials: screen [S | A | sum d, sum|a|, sum b],
-// exact [S].
-template <int K, bool EXACT>
+// Further LS passes over the cached (u, v, d): trials [base, base + count) of pass `pass`
+// (ls_pass_range).  SCREEN mode runs unless an earlier pass accepted; EXACT mode runs only when
+// the screening pick left this pass undecided (st->need_exact == pass + 1).  Partials: screen
+// [S_0..S_{KC-1} | A, D, sum|a|, sum b], exact [S_0..S_{KC-1}].
+template <bool EXACT>
 __global__ void __launch_bounds__(256) k_lsx(int64_t count, const float2* __restrict__ u,
                                              const float2* __restrict__ v, const float* __restrict__ d,
                                              SolverCfg cfg, int pass, double* __restrict__ part,
                                              const DevState* __restrict__ st) {
-    constexpr int NV = EXACT ? K : 2 * K;
-    constexpr int WID = EXACT ? K : 2 * K + 3;
-    __shared__ double sred[8][NV];
-    __shared__ double smom[8][3];
-    __shared__ float sgam[K];
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const bool run = EXACT ? (st->need_exact == pass + 1 && !st->numeric_error)
-                           : (!st->accepted && !st->numeric_error);
-    if (tid < K) sgam[tid] = (float)trial_gamma(cfg.gamma0, cfg.tau, pass * K + tid);
+    __shared__ double sred[8][KC];
+    __shared__ double smom[8][4];
+    __shared__ float sgam[KC];
+    const int tid = threadIdx.x, lane = tid & 31;
+    int base, cnt;
+    ls_pass_range(pass, st->keff, cfg, base, cnt);
+    const bool run = cnt > 0 && !st->numeric_error &&
+                     (EXACT ? (st->need_exact == pass + 1) : (!st->accepted));
+    if (tid < KC) sgam[tid] = (float)trial_gamma(cfg.gamma0, cfg.tau, base + tid);
     __syncthreads();
     const float eps2 = (float)(cfg.eps * cfg.eps);
     // Runs of RUN elements per thread (coalesced: element base + i*blockDim + tid) accumulate in
     // fp32, then one warp reduce-scatter folds them into a single fp64 total per lane.
     constexpr int RUN = 16;
-    double tot = 0.0, md = 0.0, ma = 0.0, mb = 0.0;
+    double tot = 0.0;
+    double mom[4] = {0.0, 0.0, 0.0, 0.0};
     if (run) {
         const int64_t stride = (int64_t)gridDim.x * blockDim.x * RUN;
-        for (int64_t base = (int64_t)blockIdx.x * blockDim.x * RUN; base < count; base += stride) {
-            float S[K], A[K];
-            float sd = 0.f, sa = 0.f, sb = 0.f;
+        for (int64_t e0 = (int64_t)blockIdx.x * blockDim.x * RUN; e0 < count; e0 += stride) {
+            float S[KC];
+            LsMom m;
 #pragma unroll
-            for (int k = 0; k < K; ++k) S[k] = A[k] = 0.f;
+            for (int k = 0; k < KC; ++k) S[k] = 0.f;
 #pragma unroll 4
             for (int i = 0; i < RUN; ++i) {
-                const int64_t o = base + (int64_t)i * blockDim.x + tid;
+                const int64_t o = e0 + (int64_t)i * blockDim.x + tid;
                 if (o < count) {
                     if (EXACT)
-                        ls_exact<K>(u[o], v[o], __ldg(d + o), sgam, eps2, S);
+                        ls_exact<KC>(u[o], v[o], __ldg(d + o), sgam, cnt, eps2, S);
                     else
-                        ls_screen<K>(u[o], v[o], __ldg(d + o), sgam, eps2, S, A, sd, sa, sb);
+                        ls_screen<KC>(u[o], v[o], __ldg(d + o), sgam, cnt, eps2, S, m);
                 }
             }
-            double dv[NV];
+            double dv[KC];
 #pragma unroll
-            for (int k = 0; k < K; ++k) {
-                dv[k] = (double)S[k];
-                if (!EXACT) dv[K + k] = (double)A[k];
-            }
-            tot += warp_reduce_scatter<NV>(dv, lane);
-            md += sd;
-            ma += sa;
-            mb += sb;
+            for (int k = 0; k < KC; ++k) dv[k] = (double)S[k];
+            tot += warp_reduce_scatter<KC>(dv, lane);
+            mom[0] += (double)m.A;
+            mom[1] += (double)m.D;
+            mom[2] += (double)m.sa;
+            mom[3] += (double)m.sb;
         }
     }
-    constexpr int P = Log2<NV>::value;
-    constexpr int G = 32 >> P;
-    if ((lane & (G - 1)) == 0) sred[warp][lane >> (5 - P)] = tot;
-    md = warp_sum(md);
-    ma = warp_sum(ma);
-    mb = warp_sum(mb);
-    if (lane == 0) {
-        smom[warp][0] = md;
-        smom[warp][1] = ma;
-        smom[warp][2] = mb;
-    }
-    __syncthreads();
-    if (tid < NV) {
-        double s = 0.0;
-        for (int w = 0; w < 8; ++w) s += sred[w][tid];
-        part[(int64_t)blockIdx.x * WID + tid] = s;
-    } else if (tid < WID) {
-        double s = 0.0;
-        for (int w = 0; w < 8; ++w) s += smom[w][tid - NV];
-        part[(int64_t)blockIdx.x * WID + tid] = s;
-    }
+    ls_block_out<KC, 8>(tot, mom, sred, smom, part);
 }
 
 // Line-search decision (Eq.7, Alg.1 659-668): the first trial with DeltaF_k <= gamma_k t.
 // SCREEN mode: a trial is decided only if the screening sum S_k is farther than its error bound
-// B_k = LS_EPS_D sum d + LS_EPS_R (A_k + gamma_k sum|a| + gamma_k^2 sum b) from gamma_k t;
-// otherwise the EXACT pass re-evaluates this pass's trials with the accurate log1p and the
-// EXACT-mode pick decides from the first undecided trial on.  F += DeltaF_k* (R#11); after
-// max_shrinks trials: gamma = 0, stalled (R#9); the last pass writes the trace.
+// B_k = LS_EPS_D D + LS_EPS_R (A + gamma_k sum|a| + gamma_k^2 sum b) from gamma_k t; otherwise
+// the EXACT pass re-evaluates this pass's trials with the accurate log1p and the EXACT-mode pick
+// decides from the first undecided trial on.  F += DeltaF_k* (R#11); after max_shrinks trials:
+// gamma = 0, stalled (R#9).  The last pass writes the trace and sets the next iteration's
+// adaptive pass-0 trial count keff = clamp(k* + 3, KMIN, K) (K after a stall).
 __global__ void k_pick(DevState* st, SolverCfg c, int pass, int exact_mode, int last_pass) {
-    const int K = c.K;
     if (pass == 0 && !exact_mode) st->eta2 = st->ls_pass[LS_ETA];
-    if (!st->numeric_error && !st->accepted) {
+    int base, cnt;
+    ls_pass_range(pass, st->keff, c, base, cnt);
+    if (!st->numeric_error && !st->accepted && cnt > 0) {
         if (!exact_mode) {
-            const double sd = st->ls_pass[2 * K], sa = st->ls_pass[2 * K + 1], sb = st->ls_pass[2 * K + 2];
-            for (int k = 0; k < K; ++k) {
-                const int kk = pass * K + k;
-                if (kk >= c.max_shrinks) break;
+            const double A = st->ls_pass[KC], D = st->ls_pass[KC + 1];
+            const double sa = st->ls_pass[KC + 2], sb = st->ls_pass[KC + 3];
+            for (int k = 0; k < cnt; ++k) {
+                const int kk = base + k;
                 const double gk = trial_gamma(c.gamma0, c.tau, kk);
-                const double S = st->ls_pass[k], A = st->ls_pass[K + k];
-                const double B = LS_EPS_D * sd + LS_EPS_R * (A + gk * sa + gk * gk * sb);
+                const double S = st->ls_pass[k];
+                const double B = LS_EPS_D * D + LS_EPS_R * (A + gk * sa + gk * gk * sb);
                 st->ls_hist[kk] = S;
                 st->ls_bnd[kk] = B;
                 st->n_eval = kk + 1;
@@ -364,8 +346,8 @@ __global__ void k_pick(DevState* st, SolverCfg c, int pass, int exact_mode, int 
                 }
             }
         } else if (st->need_exact == pass + 1) {
-            for (int kk = st->k_unc; kk < (pass + 1) * K && kk < c.max_shrinks; ++kk) {
-                const double dF = st->ls_pass[kk - pass * K];
+            for (int kk = st->k_unc; kk < base + cnt; ++kk) {
+                const double dF = st->ls_pass[kk - base];
                 const double gk = trial_gamma(c.gamma0, c.tau, kk);
                 st->ls_hist[kk] = dF;
                 st->ls_bnd[kk] = 0.0;
@@ -415,6 +397,7 @@ __global__ void k_pick(DevState* st, SolverCfg c, int pass, int exact_mode, int 
     if (st->trace_ptr && st->trace_idx < st->trace_cap) st->trace_ptr[st->trace_idx] = t;
     st->trace_idx += 1;
     st->m += 1;
+    st->keff = st->stalled ? c.K : min(c.K, max(KMIN, st->kstar + 3));
 }
 
 // Update stage (Eq.5, Alg.1 672): psi <- psi + gamma eta over the storage rows.
@@ -456,15 +439,10 @@ int launch_lsx(const Geometry& g, const float2* u, const float2* v, const float*
                const SolverCfg& c, int pass, bool exact, double* part, int grid, const DevState* st,
                cudaStream_t s) {
     const int64_t count = g.n_local * (int64_t)g.N * g.N;
-    if (c.K == 8) {
-        if (exact) k_lsx<8, true><<<grid, 256, 0, s>>>(count, u, v, d, c, pass, part, st);
-        else k_lsx<8, false><<<grid, 256, 0, s>>>(count, u, v, d, c, pass, part, st);
-    } else if (c.K == 16) {
-        if (exact) k_lsx<16, true><<<grid, 256, 0, s>>>(count, u, v, d, c, pass, part, st);
-        else k_lsx<16, false><<<grid, 256, 0, s>>>(count, u, v, d, c, pass, part, st);
-    } else {
-        return -2;
-    }
+    if (exact)
+        k_lsx<true><<<grid, 256, 0, s>>>(count, u, v, d, c, pass, part, st);
+    else
+        k_lsx<false><<<grid, 256, 0, s>>>(count, u, v, d, c, pass, part, st);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
@@ -506,8 +484,8 @@ int launch_validate_d(const float* d, int64_t count, int64_t frame_elems, unsign
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
-int launch_set_F(DevState* st, const double* src, cudaStream_t s) {
-    k_set_F<<<1, 1, 0, s>>>(st, src);
+int launch_set_F(DevState* st, const double* src, int keff0, cudaStream_t s) {
+    k_set_F<<<1, 1, 0, s>>>(st, src, keff0);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 

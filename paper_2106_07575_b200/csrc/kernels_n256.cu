@@ -139,19 +139,21 @@ __global__ void __launch_bounds__(512, 1) k_lsfwd256(Geometry g, const float2* _
     extern __shared__ float2 smem[];
     float2* buf = smem;
     float2* tw = smem + BUF;
-    constexpr int NV = FWD ? 1 : 2 * K;
-    __shared__ double sred[16][NV];
-    __shared__ double smom[16][3];
+    __shared__ double sred[16][K];
+    __shared__ double smom[16][4];
     __shared__ float sgam[K];
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int tid = threadIdx.x, lane = tid & 31;
     const bool err = !FWD && st->numeric_error != 0;
+    int base = 0, cnt = 0;
+    if (!FWD) ls_pass_range(0, st->keff, cfg, base, cnt);
     build_twiddles<N>(tw);
-    if (tid < K) sgam[tid] = (float)trial_gamma(cfg.gamma0, cfg.tau, tid);
+    if (tid < K) sgam[tid] = (float)trial_gamma(cfg.gamma0, cfg.tau, base + tid);
     __syncthreads();
     const int64_t nfr = err ? 0 : g.n_local;
     const float eps2 = (float)(cfg.eps * cfg.eps), scale = 1.0f / (float)N;
     float2* out = FWD ? u : v;
-    double tot = 0.0, md = 0.0, ma = 0.0, mb = 0.0, facc = 0.0;
+    double tot = 0.0, facc = 0.0;
+    double mom[4] = {0.0, 0.0, 0.0, 0.0};
     for (int64_t i = blockIdx.x; i < nfr; i += gridDim.x) {
         const int64_t j = order[i];
         const int2 s = pos[j];
@@ -190,27 +192,30 @@ __global__ void __launch_bounds__(512, 1) k_lsfwd256(Geometry g, const float2* _
                 }
                 facc += (double)fs;
             } else {
-                float S[K], A[K];
-                float sd_ = 0.f, sa_ = 0.f, sb_ = 0.f;
+                float S[K];
+                LsMom m;
 #pragma unroll
-                for (int kk = 0; kk < K; ++kk) S[kk] = A[kk] = 0.f;
+                for (int kk = 0; kk < K; ++kk) S[kk] = 0.f;
+                // park X in the thread's own phase-2 rows of buf so the epilogue can be a rolled
+                // loop (instruction-cache friendly, no local-memory array)
+                float2* mine = buf + (T * t) * COLB + (c - cb * COLB);
 #pragma unroll
+                for (int k2 = 0; k2 < T; ++k2) mine[k2 * COLB] = X[k2];
+#pragma unroll 1
                 for (int k2 = 0; k2 < T; ++k2) {
                     const int64_t o = j * N * N + (int64_t)(t + R * k2) * N + c;
-                    const float2 vv = cscale(X[k2], scale);
+                    const float2 vv = cscale(mine[k2 * COLB], scale);
                     v[o] = vv;
-                    ls_screen<K>(u[o], vv, __ldg(d + o), sgam, eps2, S, A, sd_, sa_, sb_);
+                    ls_screen<K>(u[o], vv, __ldg(d + o), sgam, cnt, eps2, S, m);
                 }
-                double dv[NV];
+                double dv[K];
 #pragma unroll
-                for (int kk = 0; kk < K; ++kk) {
-                    dv[kk] = (double)S[kk];
-                    dv[K + kk] = (double)A[kk];
-                }
-                tot += warp_reduce_scatter<NV>(dv, lane);
-                md += (double)sd_;
-                ma += (double)sa_;
-                mb += (double)sb_;
+                for (int kk = 0; kk < K; ++kk) dv[kk] = (double)S[kk];
+                tot += warp_reduce_scatter<K>(dv, lane);
+                mom[0] += (double)m.A;
+                mom[1] += (double)m.D;
+                mom[2] += (double)m.sa;
+                mom[3] += (double)m.sb;
             }
         }
         __syncthreads();
@@ -220,28 +225,7 @@ __global__ void __launch_bounds__(512, 1) k_lsfwd256(Geometry g, const float2* _
         if (tid == 0) part[blockIdx.x] = s2;
         return;
     }
-    constexpr int P = Log2<NV>::value;
-    constexpr int G = 32 >> P;
-    if ((lane & (G - 1)) == 0) sred[warp][lane >> (5 - P)] = tot;
-    md = warp_sum(md);
-    ma = warp_sum(ma);
-    mb = warp_sum(mb);
-    if (lane == 0) {
-        smom[warp][0] = md;
-        smom[warp][1] = ma;
-        smom[warp][2] = mb;
-    }
-    __syncthreads();
-    constexpr int WID = 2 * K + 3;
-    if (tid < NV) {
-        double a = 0.0;
-        for (int w = 0; w < 16; ++w) a += sred[w][tid];
-        part[(int64_t)blockIdx.x * WID + tid] = a;
-    } else if (tid < WID) {
-        double a = 0.0;
-        for (int w = 0; w < 16; ++w) a += smom[w][tid - NV];
-        part[(int64_t)blockIdx.x * WID + tid] = a;
-    }
+    ls_block_out<K, 16>(tot, mom, sred, smom, part);
 }
 
 // Batched 2-D FFT (ptyger_fft2, N = 256): pass 1 writes row transforms into `out`, pass 2 reads
@@ -305,15 +289,8 @@ int launch_ls256(const Geometry& g, const float2* eta, const float2* probe, cons
                  const float2* u, float2* v, const float* d, const SolverCfg& c, double* part, int grid,
                  const DevState* st, cudaStream_t s) {
     float2* uu = const_cast<float2*>(u);
-    if (c.K == 8) {
-        if (n256_smem(k_lsfwd256<8, false>)) return -1;
-        k_lsfwd256<8, false><<<grid, 512, n256::SMEM, s>>>(g, eta, probe, pos, order, uu, v, d, c, part, st);
-    } else if (c.K == 16) {
-        if (n256_smem(k_lsfwd256<16, false>)) return -1;
-        k_lsfwd256<16, false><<<grid, 512, n256::SMEM, s>>>(g, eta, probe, pos, order, uu, v, d, c, part, st);
-    } else {
-        return -2;
-    }
+    if (n256_smem(k_lsfwd256<KC, false>)) return -1;
+    k_lsfwd256<KC, false><<<grid, 512, n256::SMEM, s>>>(g, eta, probe, pos, order, uu, v, d, c, part, st);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 

@@ -95,7 +95,7 @@ def test_init_validation_before_device(L):
         L.Ptyger(psi, p, bad, d)
     assert ei.value.status == 3 and "frame 7" in str(ei.value)
     with pytest.raises(L.PtygerError) as ei:
-        L.Ptyger(psi, p, scan, d, ls_batch=5)
+        L.Ptyger(psi, p, scan, d, ls_batch=17)
     assert ei.value.status == 2
     with pytest.raises(L.PtygerError) as ei:
         L.Ptyger(np.ones((64, 64), complex), np.ones((24, 24), complex), scan, d)
