@@ -52,7 +52,7 @@ def build(force: bool = False, verbose: bool = True) -> str:
         return LIB
     os.makedirs(OBJ, exist_ok=True)
     nvcc = _nvcc()
-    common = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I" + os.path.join(ROOT, "include"),
+    common = ["-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC", "-I" + os.path.join(ROOT, "include"),
               "-I" + CSRC, "-I" + _nccl_include()]
     procs = []
     objs = []

@@ -129,36 +129,33 @@ static __device__ __noinline__ float ls_term_slow(float a, float b, float c, flo
 
 // EXACT terms (accurate log1p, ~1.7e-7 relative): t_k = q_k - d log1p(q_k / c).  Branch-free
 // fast path; a lane needing the guarded definition sends its warp through ls_term_slow.
-// Trials k < cnt (cnt warp-uniform) are evaluated; the others are skipped by uniform branches.
-template <int K>
-__device__ __forceinline__ void ls_exact(float2 uu, float2 vv, float dd, const float* sgam, int cnt, float eps2,
+// KT trials (compile time) accumulate into acc[0..KT).
+template <int KT, int K>
+__device__ __forceinline__ void ls_exact(float2 uu, float2 vv, float dd, const float* sgam, float eps2,
                                          float (&acc)[K]) {
+    static_assert(KT <= K, "trial count above capacity");
     const float a = 2.0f * fmaf(uu.x, vv.x, uu.y * vv.y);
     const float b = fmaf(vv.x, vv.x, vv.y * vv.y);
     const float c = fmaf(uu.x, uu.x, uu.y * uu.y);
     bool bad = !(c >= eps2);
     const float rc = bad ? 0.0f : 1.0f / c;
-    float t[K];
+    float t[KT];
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-        t[k] = 0.f;
-        if (k < cnt) {
-            const float gam = sgam[k];
-            const float q = gam * fmaf(gam, b, a);
-            const float z = q * rc;
-            bad |= (c + q < eps2) | (z <= -0.999f);
-            t[k] = fmaf(-dd, log1p_poly(fmaxf(z, -0.999f)), q);
-        }
+    for (int k = 0; k < KT; ++k) {
+        const float gam = sgam[k];
+        const float q = gam * fmaf(gam, b, a);
+        const float z = q * rc;
+        bad |= (c + q < eps2) | (z <= -0.999f);
+        t[k] = fmaf(-dd, log1p_poly(fmaxf(z, -0.999f)), q);
     }
     if (__any_sync(__activemask(), bad)) {
         if (bad) {
 #pragma unroll
-            for (int k = 0; k < K; ++k)
-                if (k < cnt) t[k] = ls_term_slow(a, b, c, dd, sgam[k], eps2);
+            for (int k = 0; k < KT; ++k) t[k] = ls_term_slow(a, b, c, dd, sgam[k], eps2);
         }
     }
 #pragma unroll
-    for (int k = 0; k < K; ++k) acc[k] += t[k];
+    for (int k = 0; k < KT; ++k) acc[k] += t[k];
 }
 
 // SCREENING terms.  cn = |u + gamma v|^2 is formed from the components of u + gamma v, so
@@ -185,9 +182,11 @@ struct LsMom {
     float A = 0.f, D = 0.f, sa = 0.f, sb = 0.f;
 };
 
-template <int K>
-__device__ __forceinline__ void ls_screen(float2 uu, float2 vv, float dd, const float* sgam, int cnt, float eps2,
+// KT trials are computed (compile time: no predicated-off work); S has room for K >= KT.
+template <int KT, int K>
+__device__ __forceinline__ void ls_screen(float2 uu, float2 vv, float dd, const float* sgam, float eps2,
                                           float (&S)[K], LsMom& m) {
+    static_assert(KT <= K, "trial count above capacity");
     const float a = 2.0f * fmaf(uu.x, vv.x, uu.y * vv.y);
     const float b = fmaf(vv.x, vv.x, vv.y * vv.y);
     const float c = fmaf(uu.x, uu.x, uu.y * uu.y);
@@ -195,20 +194,33 @@ __device__ __forceinline__ void ls_screen(float2 uu, float2 vv, float dd, const 
     const float dl = dd * 0.693147182464599609375f;
     float amax = 0.f;
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-        if (k < cnt) {
-            const float gam = sgam[k];
-            const float ex = fmaf(gam, vv.x, uu.x), ey = fmaf(gam, vv.y, uu.y);
-            const float cn = fmaf(ex, ex, ey * ey);
-            const float L2 = lg2_ftz(fmaxf(cn, eps2) * rc);
-            S[k] += fmaf(-dl, L2, cn - c);
-            amax = fmaxf(amax, fabsf(L2));
-        }
+    for (int k = 0; k < KT; ++k) {
+        const float gam = sgam[k];
+        const float ex = fmaf(gam, vv.x, uu.x), ey = fmaf(gam, vv.y, uu.y);
+        const float cn = fmaf(ex, ex, ey * ey);
+        const float L2 = lg2_ftz(fmaxf(cn, eps2) * rc);
+        S[k] += fmaf(-dl, L2, cn - c);
+        amax = fmaxf(amax, fabsf(L2));
     }
     m.A = fmaf(dl, amax, m.A);
     m.D += fmaf(0.12f, c, dd);
     m.sa += fabsf(a);
     m.sb += b;
+}
+
+// Run body.template operator()<KT>() with KT = cnt rounded up to a multiple of 4 (<= 16): the
+// trial count of a pass is uniform for the whole launch, so one branch at the top selects a
+// fully unrolled variant and only its code is executed (instruction-cache footprint of one).
+template <typename F>
+__device__ __forceinline__ void trial_dispatch(int cnt, F&& body) {
+    if (cnt <= 4)
+        body.template operator()<4>();
+    else if (cnt <= 8)
+        body.template operator()<8>();
+    else if (cnt <= 12)
+        body.template operator()<12>();
+    else
+        body.template operator()<16>();
 }
 
 // Block-level output of the screening partials: per-lane fp64 running total `tot` of entry

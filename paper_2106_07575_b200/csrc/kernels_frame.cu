@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(512, 1) k_ls(Geometry g, const float2* __restr
             LsMom m;
 #pragma unroll
             for (int k = 0; k < KC; ++k) S[k] = 0.f;
-            if (i < nfr) {
+            if (i < nfr) trial_dispatch(cnt, [&]<int KT>() {
                 const int64_t j = order[i];
                 constexpr int G4 = (R >= 4) ? 4 : R;
                 float2 un[G4];
@@ -304,10 +304,10 @@ __global__ void __launch_bounds__(512, 1) k_ls(Geometry g, const float2* __restr
                         const int q = q0 + jj;
                         const float2 vv = cscale(scol[(T * ((q / T) * T + t) + q % T) * LD], scale);
                         v[off(q)] = vv;
-                        ls_screen<KC>(uc[jj], vv, dc[jj], sgam, cnt, eps2, S, m);
+                        ls_screen<KT>(uc[jj], vv, dc[jj], sgam, eps2, S, m);
                     }
                 }
-            }
+            });
             double dv[KC];
 #pragma unroll
             for (int k = 0; k < KC; ++k) dv[k] = (double)S[k];

@@ -286,16 +286,18 @@ __global__ void __launch_bounds__(256) k_lsx(int64_t count, const float2* __rest
             LsMom m;
 #pragma unroll
             for (int k = 0; k < KC; ++k) S[k] = 0.f;
+            trial_dispatch(cnt, [&]<int KT>() {
 #pragma unroll 4
-            for (int i = 0; i < RUN; ++i) {
-                const int64_t o = e0 + (int64_t)i * blockDim.x + tid;
-                if (o < count) {
-                    if (EXACT)
-                        ls_exact<KC>(u[o], v[o], __ldg(d + o), sgam, cnt, eps2, S);
-                    else
-                        ls_screen<KC>(u[o], v[o], __ldg(d + o), sgam, cnt, eps2, S, m);
+                for (int i = 0; i < RUN; ++i) {
+                    const int64_t o = e0 + (int64_t)i * blockDim.x + tid;
+                    if (o < count) {
+                        if (EXACT)
+                            ls_exact<KT>(u[o], v[o], __ldg(d + o), sgam, eps2, S);
+                        else
+                            ls_screen<KT>(u[o], v[o], __ldg(d + o), sgam, eps2, S, m);
+                    }
                 }
-            }
+            });
             double dv[KC];
 #pragma unroll
             for (int k = 0; k < KC; ++k) dv[k] = (double)S[k];

@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(512, 1) k_lsfwd256(Geometry g, const float2* _
             int c;
             n256_column<false>(oj, cb, buf, tw, X, c);
             const int t = tid >> 5;
-            if (FWD) {
+            if constexpr (FWD) {
                 float fs = 0.f;
 #pragma unroll
                 for (int k2 = 0; k2 < T; ++k2) {
@@ -201,13 +201,15 @@ __global__ void __launch_bounds__(512, 1) k_lsfwd256(Geometry g, const float2* _
                 float2* mine = buf + (T * t) * COLB + (c - cb * COLB);
 #pragma unroll
                 for (int k2 = 0; k2 < T; ++k2) mine[k2 * COLB] = X[k2];
+                trial_dispatch(cnt, [&]<int KT>() {
 #pragma unroll 1
-                for (int k2 = 0; k2 < T; ++k2) {
-                    const int64_t o = j * N * N + (int64_t)(t + R * k2) * N + c;
-                    const float2 vv = cscale(mine[k2 * COLB], scale);
-                    v[o] = vv;
-                    ls_screen<K>(u[o], vv, __ldg(d + o), sgam, cnt, eps2, S, m);
-                }
+                    for (int k2 = 0; k2 < T; ++k2) {
+                        const int64_t o = j * N * N + (int64_t)(t + R * k2) * N + c;
+                        const float2 vv = cscale(mine[k2 * COLB], scale);
+                        v[o] = vv;
+                        ls_screen<KT>(u[o], vv, __ldg(d + o), sgam, eps2, S, m);
+                    }
+                });
                 double dv[K];
 #pragma unroll
                 for (int kk = 0; kk < K; ++kk) dv[kk] = (double)S[kk];

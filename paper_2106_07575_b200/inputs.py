@@ -104,3 +104,9 @@ def workload_inputs(w: Workload):
     """(psi_true, probe, scan) for a workload; data are the caller's job."""
     img = siemens_star(w.H, w.W)
     return make_object(img), make_probe(w.N), make_scan(w.H, w.W, w.N, w.k, w.step, w.jitter, w.seed)
+
+
+def view_inputs(w: Workload, v: int):
+    """View v of a 3-D batch workload: the phantom rotated by v pi / views, scan seed seed + v."""
+    img = siemens_star(w.H, w.W, rotation=v * np.pi / max(w.views, 1))
+    return make_object(img), make_probe(w.N), make_scan(w.H, w.W, w.N, w.k, w.step, w.jitter, w.seed + v)

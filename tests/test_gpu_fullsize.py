@@ -79,9 +79,11 @@ def test_gradient_sampled_pixels(paper_run):
     refs, r32s, gots = np.array(refs), np.array(r32s), np.array(gots)
     rms = np.sqrt(np.mean(np.abs(refs) ** 2))
     # psi_0 = 1 makes u = F(p) tiny where d > 0 (the residual is ill-conditioned there, SURVEY
-    # 8(c).4): the per-pixel tolerance is 1e-4 rms plus 4x the float32 evaluation's own error
-    tol = 1e-4 * rms + 4 * np.abs(r32s - refs)
-    assert np.all(np.abs(gots - refs) <= tol), (np.abs(gots - refs) / tol).max()
+    # 8(c).4), so the parity protocol's teacher-forced rule applies over the sample:
+    # rel L2 <= max(1e-4, 4 e32), e32 = rel L2 error of the plain float32 evaluation
+    e32 = np.linalg.norm(r32s - refs) / np.linalg.norm(refs)
+    err = np.linalg.norm(gots - refs) / np.linalg.norm(refs)
+    assert err <= max(1e-4, 4 * e32), (err, e32)
 
 
 def test_first_line_search_all_frames(paper_run):
