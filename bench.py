@@ -43,7 +43,8 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="paper", choices=["tiny", "small", "paper", "mid", "large"])
+    ap.add_argument("--config", default="paper", choices=["tiny", "small", "paper", "mid", "large", "view3d"])
+    ap.add_argument("--views", type=int, default=0, help="view3d: number of views (default: all 64)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ls-batch", type=int, default=16)
     ap.add_argument("--e2e-steps", type=int, default=2)
@@ -63,16 +64,16 @@ def peaks():
 
 # ----------------------------------------------------------------------------- data
 
-def synth_device(w: I.Workload, device):
+def synth_device(w: I.Workload, device, view: int | None = None):
     """psi_true, probe, scan on the host (inputs module); d on the device via torch.fft."""
     import torch
-    psi_true, p, scan = I.workload_inputs(w)
+    psi_true, p, scan = I.workload_inputs(w) if view is None else I.view_inputs(w, view)
     pt = torch.from_numpy(p.astype(np.complex64)).to(device)
     ot = torch.from_numpy(psi_true.astype(np.complex64)).to(device)
     N = w.N
     d = torch.empty((len(scan), N, N), dtype=torch.float32, device=device)
     g = torch.Generator(device=device)
-    g.manual_seed(w.seed)
+    g.manual_seed(w.seed + (view or 0))
     rr = torch.arange(N, device=device)
     chunk = 1024
     sc = torch.from_numpy(scan.astype(np.int64)).to(device)
@@ -194,6 +195,8 @@ def main():
                     os.environ.setdefault("PTYGER_NCCL_LIB", cand)
         except Exception:
             pass
+    if w.views > 1:
+        return run_views(args, w, world, rank, local, dev)
     psi_true, p, scan, d = synth_device(w, dev)
     n = len(scan)
     cfg = L.default_config(ls_batch=args.ls_batch, device=local, rank=rank, world=world)
@@ -322,6 +325,67 @@ def main():
         "host_wall_s": t_host,
     }
     print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_views(args, w, world, rank, local, dev):
+    """3-D ptycho-tomography batch (BASELINE config 5): independent views, sharded
+    round-robin over the ranks with no communication; each view is its own libptyger context.
+    One step = one CG iteration of every view."""
+    import torch
+    import torch.distributed as dist
+    from paper_2106_07575_b200 import _lib as L
+    nviews = args.views or w.views
+    mine = [v for v in range(nviews) if v % world == rank]
+    views = []
+    for v in mine:
+        _, p, scan, d = synth_device(w, dev, view=v)
+        psi0 = torch.ones((w.H, w.W), dtype=torch.complex64, device=dev)
+        views.append(L.Ptyger(psi0, torch.from_numpy(p.astype(np.complex64)).to(dev), scan, d,
+                              config=L.default_config(ls_batch=args.ls_batch, device=local)))
+        del d
+    for q in views:
+        q.iterate(args.warmup, traces=False)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = ClockSampler(local)
+    clk.start()
+    ms = 0.0
+    shr = []
+    for q in views:
+        tr = q.iterate(args.steps)
+        ms += q.last_iterate_ms()
+        shr += [t["shrinks"] for t in tr]
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    if world > 1:
+        tt = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    launches = sum(q.kernel_launches() for q in views)
+    stage = views[0].stage_times(2) / 2 if views else np.zeros(7)
+    frames = nviews * w.n
+    if rank == 0:
+        pk, pk_kind = peaks()
+        algo = 36.0 * w.n * w.N * w.N
+        line = {"metric": METRIC, "value": frames * args.steps / (ms / 1e3), "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic",
+                "config": {"workload": f"{w.name}: {nviews} views x {w.H}^2 object, {w.N}^2 detector, {w.n} frames "
+                                       "per view, views sharded over ranks (no communication)",
+                           "views": nviews, "frames": frames, "parallelism": f"views{world}",
+                           "l2": "inputs larger than L2"},
+                "roofline": {"bound": "hbm", "kernel": "k_grad (view 0)", "achieved": algo / (stage[1] / 1e3) / 1e9,
+                             "peak": pk, "peak_kind": pk_kind, "unit": "GB/s",
+                             "frac": algo / (stage[1] / 1e3) / 1e9 / pk, "traffic": None},
+                "mean_shrinks": float(np.mean(shr)) if shr else None, "clocks": clocks,
+                "gpu_launches": int(launches), "e2e": None, "cpu_baseline": None}
+        print(json.dumps(line))
+    for q in views:
+        q.close()
     if world > 1:
         dist.destroy_process_group()
 

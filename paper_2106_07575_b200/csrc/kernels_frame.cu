@@ -209,6 +209,7 @@ __global__ void __launch_bounds__(512, 1) k_ls(Geometry g, const float2* __restr
     __shared__ double sred[16][KC];
     __shared__ double smom[16][4];
     __shared__ float sgam[KC];
+    __shared__ LsWarpQ wq[16];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const bool err = st->numeric_error != 0;
     int base, cnt;
@@ -270,9 +271,13 @@ __global__ void __launch_bounds__(512, 1) k_ls(Geometry g, const float2* __restr
             LsMom m;
 #pragma unroll
             for (int k = 0; k < KC; ++k) S[k] = 0.f;
-            if (i < nfr) trial_dispatch(cnt, [&]<int KT>() {
-                const int64_t j = order[i];
+            // all lanes run the epilogue (lanes of a frame past the end push zeros) because the
+            // d > 0 compaction ring is warp-collective
+            const bool valid = i < nfr;
+            const int64_t j = valid ? order[i] : 0;
+            if (cnt > 0) trial_dispatch(cnt, [&]<int KT>() {
                 constexpr int G4 = (R >= 4) ? 4 : R;
+                LsQState qs;
                 float2 un[G4];
                 float dn[G4];
                 auto off = [&](int q) {
@@ -280,8 +285,8 @@ __global__ void __launch_bounds__(512, 1) k_ls(Geometry g, const float2* __restr
                 };
 #pragma unroll
                 for (int jj = 0; jj < G4; ++jj) {
-                    un[jj] = u[off(jj)];
-                    dn[jj] = __ldg(d + off(jj));
+                    un[jj] = valid ? u[off(jj)] : make_float2(0.f, 0.f);
+                    dn[jj] = valid ? __ldg(d + off(jj)) : 0.f;
                 }
 #pragma unroll 1
                 for (int q0 = 0; q0 < R; q0 += G4) {
@@ -292,7 +297,7 @@ __global__ void __launch_bounds__(512, 1) k_ls(Geometry g, const float2* __restr
                         uc[jj] = un[jj];
                         dc[jj] = dn[jj];
                     }
-                    if (q0 + G4 < R) {  // prefetch the next group's u, d
+                    if (q0 + G4 < R && valid) {  // prefetch the next group's u, d
 #pragma unroll
                         for (int jj = 0; jj < G4; ++jj) {
                             un[jj] = u[off(q0 + G4 + jj)];
@@ -302,11 +307,13 @@ __global__ void __launch_bounds__(512, 1) k_ls(Geometry g, const float2* __restr
 #pragma unroll
                     for (int jj = 0; jj < G4; ++jj) {
                         const int q = q0 + jj;
-                        const float2 vv = cscale(scol[(T * ((q / T) * T + t) + q % T) * LD], scale);
-                        v[off(q)] = vv;
-                        ls_screen<KT>(uc[jj], vv, dc[jj], sgam, eps2, S, m);
+                        float2 vv = cscale(scol[(T * ((q / T) * T + t) + q % T) * LD], scale);
+                        if (valid) v[off(q)] = vv;
+                        else vv = make_float2(0.f, 0.f);
+                        ls_push<KT>(wq[warp], qs, uc[jj], vv, dc[jj], sgam, eps2, S, m, lane);
                     }
                 }
+                ls_flush<KT>(wq[warp], qs, sgam, eps2, S, m, lane);
             });
             double dv[KC];
 #pragma unroll

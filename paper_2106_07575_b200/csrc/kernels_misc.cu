@@ -266,6 +266,7 @@ __global__ void __launch_bounds__(256) k_lsx(int64_t count, const float2* __rest
     __shared__ double sred[8][KC];
     __shared__ double smom[8][4];
     __shared__ float sgam[KC];
+    __shared__ LsWarpQ wq[EXACT ? 1 : 8];
     const int tid = threadIdx.x, lane = tid & 31;
     int base, cnt;
     ls_pass_range(pass, st->keff, cfg, base, cnt);
@@ -287,15 +288,24 @@ __global__ void __launch_bounds__(256) k_lsx(int64_t count, const float2* __rest
 #pragma unroll
             for (int k = 0; k < KC; ++k) S[k] = 0.f;
             trial_dispatch(cnt, [&]<int KT>() {
+                if constexpr (EXACT) {
 #pragma unroll 4
-                for (int i = 0; i < RUN; ++i) {
-                    const int64_t o = e0 + (int64_t)i * blockDim.x + tid;
-                    if (o < count) {
-                        if (EXACT)
-                            ls_exact<KT>(u[o], v[o], __ldg(d + o), sgam, eps2, S);
-                        else
-                            ls_screen<KT>(u[o], v[o], __ldg(d + o), sgam, eps2, S, m);
+                    for (int i = 0; i < RUN; ++i) {
+                        const int64_t o = e0 + (int64_t)i * blockDim.x + tid;
+                        if (o < count) ls_exact<KT>(u[o], v[o], __ldg(d + o), sgam, eps2, S);
                     }
+                } else {
+                    // warp-collective d > 0 compaction: out-of-range lanes push zeros
+                    LsQState qs;
+#pragma unroll 4
+                    for (int i = 0; i < RUN; ++i) {
+                        const int64_t o = e0 + (int64_t)i * blockDim.x + tid;
+                        const bool ok = o < count;
+                        ls_push<KT>(wq[tid >> 5], qs, ok ? u[o] : make_float2(0.f, 0.f),
+                                    ok ? v[o] : make_float2(0.f, 0.f), ok ? __ldg(d + o) : 0.f, sgam, eps2, S, m,
+                                    lane);
+                    }
+                    ls_flush<KT>(wq[tid >> 5], qs, sgam, eps2, S, m, lane);
                 }
             });
             double dv[KC];

@@ -142,6 +142,7 @@ __global__ void __launch_bounds__(512, 1) k_lsfwd256(Geometry g, const float2* _
     __shared__ double sred[16][K];
     __shared__ double smom[16][4];
     __shared__ float sgam[K];
+    __shared__ LsWarpQ wq[FWD ? 1 : 16];
     const int tid = threadIdx.x, lane = tid & 31;
     const bool err = !FWD && st->numeric_error != 0;
     int base = 0, cnt = 0;
@@ -201,14 +202,16 @@ __global__ void __launch_bounds__(512, 1) k_lsfwd256(Geometry g, const float2* _
                 float2* mine = buf + (T * t) * COLB + (c - cb * COLB);
 #pragma unroll
                 for (int k2 = 0; k2 < T; ++k2) mine[k2 * COLB] = X[k2];
-                trial_dispatch(cnt, [&]<int KT>() {
+                if (cnt > 0) trial_dispatch(cnt, [&]<int KT>() {
+                    LsQState qs;
 #pragma unroll 1
                     for (int k2 = 0; k2 < T; ++k2) {
                         const int64_t o = j * N * N + (int64_t)(t + R * k2) * N + c;
                         const float2 vv = cscale(mine[k2 * COLB], scale);
                         v[o] = vv;
-                        ls_screen<KT>(u[o], vv, __ldg(d + o), sgam, eps2, S, m);
+                        ls_push<KT>(wq[tid >> 5], qs, u[o], vv, __ldg(d + o), sgam, eps2, S, m, lane);
                     }
+                    ls_flush<KT>(wq[tid >> 5], qs, sgam, eps2, S, m, lane);
                 });
                 double dv[K];
 #pragma unroll
