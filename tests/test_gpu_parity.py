@@ -105,6 +105,9 @@ def test_teacher_forced_iterations(L, name, direction):
     for m in range(6):
         psi_m, g_prev, eta_prev, F_m, mm = pt.get_state()
         assert mm == m
+        # teacher forcing: restart the GPU from exactly this state (u = G psi_m recomputed),
+        # so each step is compared from a fresh far field rather than the lazily updated one
+        pt.set_state(psi_m, g_prev, eta_prev, m)
         psi64 = c128(psi_m)
         g_ref, alpha_ref, eta_ref, rs_ref, u_ref = O.grad_at(psi64, c128(g_prev), c128(eta_prev), m, p64, scan, d64,
                                                             variant=direction)
@@ -159,6 +162,20 @@ def test_warm_start_trajectory_tiny(L):
     assert rel(pt.get_object(), ost.psi) <= 1e-3
     F = [t["F"] for t in gtr]
     assert all(F[i + 1] <= F[i] for i in range(len(F) - 1))
+    pt.close()
+
+
+@pytest.mark.parametrize("name", ["n128", "n256"])
+def test_free_running_far_field_drift(L, name):
+    """Design S updates u <- u + gamma v instead of recomputing G psi: after 8 free iterations the
+    cached far field must still match G psi_m (oracle, fp64) to 1e-5 and the gradient the fresh
+    oracle gradient to the 1e-3 object-level bar."""
+    psi_true, p, scan, d = get_fixture(name)
+    pt = L.Ptyger(np.ones_like(psi_true), p, scan, d)
+    pt.iterate(8)
+    psi_m, _, _, _, _ = pt.get_state()
+    u_ref = O.forward_G(c128(psi_m), c128(p), scan)
+    assert rel(pt.get_farfield(), u_ref) <= 1e-5
     pt.close()
 
 
