@@ -297,17 +297,23 @@ __device__ __forceinline__ void ls_flush(LsWarpQ& q, LsQState& qs, const float* 
     qs.za = qs.zb = 0.f;
 }
 
-// Run body.template operator()<KT>() with KT = cnt rounded up to a multiple of 4 (<= 16): the
+// Run body.template operator()<KT>() with KT = cnt rounded up to an even count >= 4 (<= 16): the
 // trial count of a pass is uniform for the whole launch, so one branch at the top selects a
 // fully unrolled variant and only its code is executed (instruction-cache footprint of one).
 template <typename F>
 __device__ __forceinline__ void trial_dispatch(int cnt, F&& body) {
     if (cnt <= 4)
         body.template operator()<4>();
+    else if (cnt <= 6)
+        body.template operator()<6>();
     else if (cnt <= 8)
         body.template operator()<8>();
+    else if (cnt <= 10)
+        body.template operator()<10>();
     else if (cnt <= 12)
         body.template operator()<12>();
+    else if (cnt <= 14)
+        body.template operator()<14>();
     else
         body.template operator()<16>();
 }
