@@ -79,7 +79,9 @@ __device__ __forceinline__ double trial_gamma(double gamma0, double tau, int k) 
 __device__ __forceinline__ float2 residual(float2 u, float dd, float eps2) {
     const float c = u.x * u.x + u.y * u.y;
     if (c >= eps2) {
-        const float s = __fdividef(dd, c);  // MUFU.RCP + FMUL, 2 ulp (no slow-path branch)
+        // correctly rounded division: where |u| is small and d > 0 the residual is ill-conditioned
+        // and a 2-ulp approximate quotient measurably inflated the gradient error
+        const float s = __fdiv_rn(dd, c);
         return make_float2(u.x - s * u.x, u.y - s * u.y);
     }
     return u;
