@@ -58,7 +58,14 @@ typedef enum {
 /* Direction variants (R#6). */
 enum { PTYGER_DIR_DY = 0,      /* complex alpha exactly as printed (Eq.6 / Eq.8)   */
        PTYGER_DIR_DY_REAL = 1, /* Re(alpha)                                        */
-       PTYGER_DIR_FR = 2 };    /* Fletcher-Reeves ||g||^2 / ||g_prev||^2            */
+       PTYGER_DIR_FR = 2,      /* Fletcher-Reeves ||g||^2 / ||g_prev||^2            */
+       PTYGER_DIR_PR = 3,      /* Polak-Ribiere+ max(0, Re<g, g - g_prev>) / ||g_prev||^2 */
+       PTYGER_DIR_GD = 4 };    /* gradient descent, Eq.4: eta = -g, gamma = gamma0
+                                  taken without line search (constant step)         */
+
+/* Estimators (R#19): the Poisson maximum likelihood of Eq.2 or the least squares (Gaussian)
+ * estimator F = sum (|G psi| - sqrt d)^2 the paper says the techniques also apply to. */
+enum { PTYGER_EST_ML = 0, PTYGER_EST_LS = 1 };
 
 typedef struct {
     double gamma0;        /* first LS trial, 1.0 (Alg.1)                            */
@@ -69,6 +76,7 @@ typedef struct {
     int32_t direction;    /* PTYGER_DIR_*                                                 */
     int32_t ls_batch;     /* K in [4, 16] (default 16): trials per extra LS pass over the frames and the
                              cap of pass 0, whose trial count adapts on the device to k*_prev + 3 */
+    int32_t estimator;    /* PTYGER_EST_ML (default) or PTYGER_EST_LS                          */
     int32_t device;       /* CUDA device ordinal                                          */
     int32_t rank;         /* this process's rank, 0..world-1                              */
     int32_t world;        /* number of ranks (one GPU each)                               */
@@ -128,8 +136,11 @@ ptyger_status ptyger_get_object(ptyger_ctx* ctx, float* out);
  * iteration).  Collective when world > 1. */
 ptyger_status ptyger_get_gradient(ptyger_ctx* ctx, float* out);
 
-/* Cached far field u = G psi (n*N*N complex64, frames in input order) of the frames this
- * rank owns (all frames when world = 1), for parity tests. */
+/* Cached far field u = G psi_m (n*N*N complex64, frames in input order) of the frames this
+ * rank owns (all frames when world = 1), for parity tests.  The cache lags psi by the last
+ * accepted gamma v (R#11); this call first folds that update in on the device (the same
+ * fp32 fma the next GRAD stage would apply, which then skips it), so the result is G psi_m
+ * of ptyger_get_object's psi_m and the iteration sequence is unchanged. */
 ptyger_status ptyger_get_farfield(ptyger_ctx* ctx, float* out);
 
 /* Teacher-forcing state: psi_m, grad F(psi_{m-1}), eta_{m-1} (H*W complex64 each), the

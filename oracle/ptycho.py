@@ -264,25 +264,81 @@ class Trace:
     trials: list = field(default_factory=list)
 
 
+# --------------------------------------------------------------------------
+# Least-squares (Gaussian) estimator: "all the techniques introduced in this
+# paper are also applicable to the LS estimator".  Reading R#19:
+#   F_LS(psi) = sum_j (|G psi|_j - sqrt(d_j))^2,   grad = G^H( G psi - sqrt(d) G psi / |G psi| )
+# (Wirtinger), the quotient dropped where |G psi| < eps exactly as for Eq.3 (R#4).
+# --------------------------------------------------------------------------
+EST_ML = 0
+EST_LS = 1
+
+
+def objective_F_ls(far: np.ndarray, d: np.ndarray, eps: float = EPS) -> float:
+    return float(np.sum((np.abs(far) - np.sqrt(d)) ** 2))
+
+
+def residual_ls(far: np.ndarray, d: np.ndarray, eps: float = EPS) -> np.ndarray:
+    a = np.abs(far)
+    ok = a >= eps
+    q = np.zeros_like(far)
+    q[ok] = np.sqrt(d[ok]) * far[ok] / a[ok]
+    return far - q
+
+
+def gradient_ls(psi, probe, scan, d, eps: float = EPS):
+    far = forward_G(psi, probe, scan)
+    return adjoint_GH(residual_ls(far, d, eps), probe, scan, psi.shape), far
+
+
+def _estimator(est: int):
+    if est == EST_LS:
+        return objective_F_ls, gradient_ls
+    return objective_F, gradient
+
+
+# Further direction rules of the CG family the paper cites around Eq.6 (P:443:
+# Dai-Yuan, Polak / Polyak): Polak-Ribiere-Polyak with the usual PR+ clipping.
+DIR_PR = 3
+
+
+def polak_ribiere(g, g_prev, eta_prev):
+    """beta = max(0, Re<g, g - g_prev> / ||g_prev||^2); eta = -g + beta eta_prev."""
+    if g_prev is None or eta_prev is None:
+        return -g, 0j, False
+    den = float(np.sum(np.abs(g_prev) ** 2))
+    if den < DEN_EPS:
+        return -g, 0j, True
+    beta = max(0.0, float(np.real(inner(g, g - g_prev))) / den)
+    return -g + beta * eta_prev, complex(beta, 0.0), False
+
+
+def direction(g, g_prev, eta_prev, variant: int):
+    if variant == DIR_PR:
+        return polak_ribiere(g, g_prev, eta_prev)
+    return dai_yuan(g, g_prev, eta_prev, variant)
+
+
 def cg_iterate(state: CGState, probe, scan, d, ls: LSConfig = LSConfig(),
-               variant: int = DIR_DY_COMPLEX, eps: float = EPS):
+               variant: int = DIR_DY_COMPLEX, eps: float = EPS, est: int = EST_ML):
     """One iteration of Alg.1 with Eq.7 LS semantics (R#7).
 
-    GRAD: g = grad F(psi_m) (Eq.3).
-    DIR  (P:651-656): eta = Dai-Yuan(g, g_prev, eta_prev) (Eq.6).
+    GRAD: g = grad F(psi_m) (Eq.3; LS estimator: R#19).
+    DIR: eta = Dai-Yuan(g, g_prev, eta_prev) (Eq.6) or a variant (R#6, f3).
     LS: gamma from line_search, F evaluated BY DEFINITION on
                       G(psi + gamma eta) for every trial.
     UPD:     psi_{m+1} = psi_m + gamma eta (Eq.5); F cached (R#11).
     Returns (new_state, trace, g, eta).
     """
+    objective, grad_fn = _estimator(est)
     psi = state.psi
-    g, far = gradient(psi, probe, scan, d, eps)
-    f0 = state.F if state.F is not None else objective_F(far, d, eps)
-    eta, alpha, restarted = dai_yuan(g, state.g_prev if state.m > 0 else None,
-                                     state.eta_prev if state.m > 0 else None, variant)
+    g, far = grad_fn(psi, probe, scan, d, eps)
+    f0 = state.F if state.F is not None else objective(far, d, eps)
+    eta, alpha, restarted = direction(g, state.g_prev if state.m > 0 else None,
+                                      state.eta_prev if state.m > 0 else None, variant)
 
     def eval_f(gamma):
-        return objective_F(forward_G(psi + gamma * eta, probe, scan), d, eps)
+        return objective(forward_G(psi + gamma * eta, probe, scan), d, eps)
 
     gamma, k, f_new, stalled, trials = line_search(eval_f, f0, ls)
     psi_new = psi + gamma * eta
@@ -294,31 +350,42 @@ def cg_iterate(state: CGState, probe, scan, d, ls: LSConfig = LSConfig(),
 
 
 def run_cg(psi0, probe, scan, d, iters: int, ls: LSConfig = LSConfig(),
-           variant: int = DIR_DY_COMPLEX, eps: float = EPS):
+           variant: int = DIR_DY_COMPLEX, eps: float = EPS, est: int = EST_ML):
     """Alg.1 end to end on one worker: iters CG iterations from psi0 (R#10)."""
     st = CGState(psi=np.asarray(psi0, dtype=np.complex128).copy())
     traces = []
     for _ in range(iters):
-        st, tr, _, _ = cg_iterate(st, probe, scan, d, ls, variant, eps)
+        st, tr, _, _ = cg_iterate(st, probe, scan, d, ls, variant, eps, est)
         traces.append(tr)
     return st, traces
 
 
-def gd_iterate(psi, probe, scan, d, gamma: float, eps: float = EPS):
+def gd_iterate(psi, probe, scan, d, gamma: float, eps: float = EPS, est: int = EST_ML):
     """Gradient-descent update psi - gamma grad F (Eq.4)."""
-    g, _ = gradient(psi, probe, scan, d, eps)
+    g, _ = _estimator(est)[1](psi, probe, scan, d, eps)
     return psi - gamma * g
+
+
+def ls_delta_ls(u, v, d, gamma: float, eps: float = EPS) -> float:
+    """LS-estimator difference form: sum (|u + g v| - sqrt d)^2 - (|u| - sqrt d)^2
+    = sum q (1 - 2 sqrt(d) / (|u + g v| + |u|)),  q = |u + g v|^2 - |u|^2."""
+    un = np.abs(u + gamma * v)
+    uo = np.abs(u)
+    q = un * un - uo * uo
+    s = un + uo
+    frac = np.where(s > 0, 2.0 * np.sqrt(d) / np.where(s > 0, s, 1.0), 0.0)
+    return float(np.sum(q * (1.0 - frac)))
 
 
 # --------------------------------------------------------------------------
 # Teacher-forcing helpers: what one GPU iteration must produce from a given state
 # --------------------------------------------------------------------------
 
-def grad_at(psi, g_prev, eta_prev, m, probe, scan, d, variant=DIR_DY_COMPLEX, eps=EPS):
+def grad_at(psi, g_prev, eta_prev, m, probe, scan, d, variant=DIR_DY_COMPLEX, eps=EPS, est=EST_ML):
     """From state (psi_m, g_{m-1}, eta_{m-1}, m): g_m, alpha_m, eta_m, restarted, u=G psi_m."""
-    g, far = gradient(psi, probe, scan, d, eps)
-    eta, alpha, restarted = dai_yuan(g, g_prev if m > 0 else None,
-                                     eta_prev if m > 0 else None, variant)
+    g, far = _estimator(est)[1](psi, probe, scan, d, eps)
+    eta, alpha, restarted = direction(g, g_prev if m > 0 else None,
+                                      eta_prev if m > 0 else None, variant)
     return g, alpha, eta, restarted, far
 
 

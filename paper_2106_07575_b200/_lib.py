@@ -15,7 +15,8 @@ LIB_PATH = os.path.join(_HERE, "libptyger.so")
 
 PTYGER_OK = 0
 STATUS = {0: "OK", 2: "E_ARG", 3: "E_DATA", 4: "E_NUMERIC", 5: "E_CUDA", 6: "E_NCCL", 7: "E_OOM", 8: "E_STATE"}
-DIR_DY, DIR_DY_REAL, DIR_FR = 0, 1, 2
+DIR_DY, DIR_DY_REAL, DIR_FR, DIR_PR, DIR_GD = 0, 1, 2, 3, 4
+EST_ML, EST_LS = 0, 1
 
 
 class PtygerError(RuntimeError):
@@ -27,6 +28,7 @@ class PtygerError(RuntimeError):
 class Config(C.Structure):
     _fields_ = [("gamma0", C.c_double), ("tau", C.c_double), ("t", C.c_double), ("eps", C.c_double),
                 ("max_shrinks", C.c_int32), ("direction", C.c_int32), ("ls_batch", C.c_int32),
+                ("estimator", C.c_int32),
                 ("device", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32), ("nccl_id", C.c_void_p)]
 
 

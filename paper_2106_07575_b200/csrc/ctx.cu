@@ -352,6 +352,7 @@ void ptyger_config_default(ptyger_config* cfg) {
     cfg->max_shrinks = 32;
     cfg->direction = PTYGER_DIR_DY;
     cfg->ls_batch = 16;
+    cfg->estimator = PTYGER_EST_ML;
     cfg->device = 0;
     cfg->rank = 0;
     cfg->world = 1;
@@ -451,6 +452,7 @@ static ptyger_status init_impl(ptyger_ctx* c, const float* object, const float* 
     g.band_lo1 = c->band_lo[1];
     g.band_hi1 = c->band_lo[1] + c->band_rows[1];
     g.n_local = nl;
+    g.est = cfg.estimator;
     // local positions and canonical processing order
     std::vector<int32_t> lpos(2 * nl);
     std::vector<int32_t> sub(2 * nl);
@@ -577,7 +579,8 @@ ptyger_status ptyger_init(ptyger_ctx** out, const ptyger_config* cfg_in, const f
     if (!object || !probe || !scan || !intensities) return set_err(nullptr, PTYGER_E_ARG, "init: null input array");
     if (!(cfg.gamma0 > 0) || !(cfg.tau > 0 && cfg.tau < 1) || !(cfg.eps > 0) || cfg.max_shrinks < 1 ||
         cfg.max_shrinks > SMAX || cfg.ls_batch < KMIN || cfg.ls_batch > KC || cfg.direction < 0 ||
-        cfg.direction > 2 || cfg.world < 1 || cfg.rank < 0 || cfg.rank >= cfg.world ||
+        cfg.direction > PTYGER_DIR_GD || cfg.estimator < 0 || cfg.estimator > PTYGER_EST_LS || cfg.world < 1 ||
+        cfg.rank < 0 || cfg.rank >= cfg.world ||
         (cfg.world > 1 && !cfg.nccl_id) || !std::isfinite(cfg.t))
         return set_err(nullptr, PTYGER_E_ARG,
                        "init: bad config (need gamma0>0, 0<tau<1, eps>0, 1<=max_shrinks<=64, 4<=ls_batch<=16, "
@@ -602,6 +605,8 @@ ptyger_status ptyger_init(ptyger_ctx** out, const ptyger_config* cfg_in, const f
     c->sc.max_shrinks = cfg.max_shrinks;
     c->sc.direction = cfg.direction;
     c->sc.K = cfg.ls_batch;
+    c->sc.est = cfg.estimator;
+    if (cfg.direction == PTYGER_DIR_GD) c->sc.max_shrinks = 1;   // Eq.4: one fixed step gamma0
     c->H = H;
     c->W = W;
     c->N = N;
@@ -710,6 +715,8 @@ ptyger_status ptyger_get_farfield(ptyger_ctx* c, float* out) {
     if (!c || !out) return set_err(c, PTYGER_E_ARG, "get_farfield: null pointer");
     std::string& err = c->err;
     CK(cudaSetDevice(c->cfg.device));
+    // u lags psi by the last accepted gamma v (R#11): fold it in first (bit-identical to k_grad's fold)
+    LK(launch_fold(c->geo, c->u, c->v, c->st, c->grid_el, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     CK(cudaMemcpy(out, c->u, sizeof(float2) * c->geo.n_local * c->N * c->N, cudaMemcpyDeviceToHost));
     return PTYGER_OK;

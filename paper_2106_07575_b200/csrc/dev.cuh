@@ -76,15 +76,26 @@ __device__ __forceinline__ double trial_gamma(double gamma0, double tau, int k) 
 }
 
 // Residual of Eq.3: u - d/u^* = u - d u / |u|^2, quotient dropped where |u| < eps (R#4).
-__device__ __forceinline__ float2 residual(float2 u, float dd, float eps2) {
+// Least-squares estimator (R#19): u - sqrt(d) u / |u|.
+__device__ __forceinline__ float2 residual(float2 u, float dd, float eps2, int est = PTYGER_EST_ML) {
     const float c = u.x * u.x + u.y * u.y;
     if (c >= eps2) {
         // correctly rounded division: where |u| is small and d > 0 the residual is ill-conditioned
         // and a 2-ulp approximate quotient measurably inflated the gradient error
-        const float s = __fdiv_rn(dd, c);
+        float s = __fdiv_rn(dd, c);
+        if (est == PTYGER_EST_LS) s = __fsqrt_rn(s);
         return make_float2(u.x - s * u.x, u.y - s * u.y);
     }
     return u;
+}
+
+// Per-pixel objective term: Eq.2 c - d log c (Poisson ML) or (|u| - sqrt d)^2 (LS estimator).
+__device__ __forceinline__ float objective_term(float c, float dd, float eps2, int est) {
+    if (est == PTYGER_EST_LS) {
+        const float r = __fsqrt_rn(c) - __fsqrt_rn(dd);
+        return r * r;
+    }
+    return c - dd * logf(fmaxf(c, eps2));
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -129,13 +140,34 @@ static __device__ __noinline__ float ls_term_slow(float a, float b, float c, flo
     return (cn - c) - dd * (logf(fmaxf(cn, eps2)) - logf(fmaxf(c, eps2)));
 }
 
+// Least-squares estimator terms t = q (1 - 2 sqrt(d) / (|u + g v| + |u|)), q = |u + g v|^2 - |u|^2
+// with correctly rounded sqrt / reciprocal (a few ulp per term, no transcendental approximation).
+template <int KT, int K>
+__device__ __forceinline__ void ls_screen_lse(float2 uu, float2 vv, float dd, const float* sgam, float (&S)[K]) {
+    const float c = fmaf(uu.x, uu.x, uu.y * uu.y);
+    const float sc = __fsqrt_rn(c), sd2 = 2.0f * __fsqrt_rn(dd);
+#pragma unroll
+    for (int k = 0; k < KT; ++k) {
+        const float gam = sgam[k];
+        const float ex = fmaf(gam, vv.x, uu.x), ey = fmaf(gam, vv.y, uu.y);
+        const float cn = fmaf(ex, ex, ey * ey);
+        const float q = cn - c;
+        const float den = __fsqrt_rn(cn) + sc;
+        S[k] += (den > 0.f) ? fmaf(-q, sd2 * __frcp_rn(den), q) : q;
+    }
+}
+
 // EXACT terms (accurate log1p, ~1.7e-7 relative): t_k = q_k - d log1p(q_k / c).  Branch-free
 // fast path; a lane needing the guarded definition sends its warp through ls_term_slow.
 // KT trials (compile time) accumulate into acc[0..KT).
-template <int KT, int K>
+template <int KT, bool LSE, int K>
 __device__ __forceinline__ void ls_exact(float2 uu, float2 vv, float dd, const float* sgam, float eps2,
                                          float (&acc)[K]) {
     static_assert(KT <= K, "trial count above capacity");
+    if constexpr (LSE) {   // least-squares estimator: the screening formula is already exact
+        ls_screen_lse<KT>(uu, vv, dd, sgam, acc);
+        return;
+    }
     const float a = 2.0f * fmaf(uu.x, vv.x, uu.y * vv.y);
     const float b = fmaf(vv.x, vv.x, vv.y * vv.y);
     const float c = fmaf(uu.x, uu.x, uu.y * uu.y);
@@ -224,23 +256,30 @@ struct LsWarpQ {
     float d[64];
 };
 
-template <int KT, int K>
+// LSE = false: Poisson ML terms (screened, MUFU log2).  LSE = true: least-squares estimator terms
+// t = q (1 - 2 sqrt(d) / (|u + g v| + |u|)) with correctly rounded sqrt / reciprocal: a few ulp per
+// term, no transcendental approximation, so A stays 0 and the bound reduces to its rounding part.
+template <int KT, bool LSE, int K>
 __device__ __forceinline__ void ls_screen_nz(float2 uu, float2 vv, float dd, const float* sgam, float eps2,
                                              float (&S)[K], LsMom& m) {
     const float c = fmaf(uu.x, uu.x, uu.y * uu.y);
-    const float rc = (c >= eps2) ? __fdividef(1.0f, c) : 0.0f;
-    const float dl = dd * 0.693147182464599609375f;
-    float amax = 0.f;
+    if constexpr (LSE) {
+        ls_screen_lse<KT>(uu, vv, dd, sgam, S);
+    } else {
+        const float rc = (c >= eps2) ? __fdividef(1.0f, c) : 0.0f;
+        const float dl = dd * 0.693147182464599609375f;
+        float amax = 0.f;
 #pragma unroll
-    for (int k = 0; k < KT; ++k) {
-        const float gam = sgam[k];
-        const float ex = fmaf(gam, vv.x, uu.x), ey = fmaf(gam, vv.y, uu.y);
-        const float cn = fmaf(ex, ex, ey * ey);
-        const float L2 = lg2_ftz(fmaxf(cn, eps2) * rc);
-        S[k] += fmaf(-dl, L2, cn - c);
-        amax = fmaxf(amax, fabsf(L2));
+        for (int k = 0; k < KT; ++k) {
+            const float gam = sgam[k];
+            const float ex = fmaf(gam, vv.x, uu.x), ey = fmaf(gam, vv.y, uu.y);
+            const float cn = fmaf(ex, ex, ey * ey);
+            const float L2 = lg2_ftz(fmaxf(cn, eps2) * rc);
+            S[k] += fmaf(-dl, L2, cn - c);
+            amax = fmaxf(amax, fabsf(L2));
+        }
+        m.A = fmaf(dl, amax, m.A);
     }
-    m.A = fmaf(dl, amax, m.A);
 }
 
 struct LsQState {
@@ -248,7 +287,7 @@ struct LsQState {
     float za = 0.f, zb = 0.f;    // per lane: sum a, sum b over the d = 0 pixels it saw
 };
 
-template <int KT, int K>
+template <int KT, bool LSE, int K>
 __device__ __forceinline__ void ls_push(LsWarpQ& q, LsQState& qs, float2 uu, float2 vv, float dd, const float* sgam,
                                         float eps2, float (&S)[K], LsMom& m, int lane) {
     const float a = 2.0f * fmaf(uu.x, vv.x, uu.y * vv.y);
@@ -273,7 +312,7 @@ __device__ __forceinline__ void ls_push(LsWarpQ& q, LsQState& qs, float2 uu, flo
     if (qs.pending >= 32) {
         __syncwarp();
         const int slot = (qs.head + lane) & 63;
-        ls_screen_nz<KT>(q.u[slot], q.v[slot], q.d[slot], sgam, eps2, S, m);
+        ls_screen_nz<KT, LSE>(q.u[slot], q.v[slot], q.d[slot], sgam, eps2, S, m);
         qs.head = (qs.head + 32) & 63;
         qs.pending -= 32;
         __syncwarp();
@@ -281,14 +320,14 @@ __device__ __forceinline__ void ls_push(LsWarpQ& q, LsQState& qs, float2 uu, flo
 }
 
 // Drain the ring and fold the d = 0 moments into S (call once per accumulation run).
-template <int KT, int K>
+template <int KT, bool LSE, int K>
 __device__ __forceinline__ void ls_flush(LsWarpQ& q, LsQState& qs, const float* sgam, float eps2, float (&S)[K],
                                          LsMom& m, int lane) {
     if (qs.pending > 0) {
         __syncwarp();
         if (lane < qs.pending) {
             const int slot = (qs.head + lane) & 63;
-            ls_screen_nz<KT>(q.u[slot], q.v[slot], q.d[slot], sgam, eps2, S, m);
+            ls_screen_nz<KT, LSE>(q.u[slot], q.v[slot], q.d[slot], sgam, eps2, S, m);
         }
         qs.head = (qs.head + qs.pending) & 63;
         qs.pending = 0;
@@ -302,22 +341,31 @@ __device__ __forceinline__ void ls_flush(LsWarpQ& q, LsQState& qs, const float* 
 // Run body.template operator()<KT>() with KT = cnt rounded up to an even count >= 4 (<= 16): the
 // trial count of a pass is uniform for the whole launch, so one branch at the top selects a
 // fully unrolled variant and only its code is executed (instruction-cache footprint of one).
-template <typename F>
-__device__ __forceinline__ void trial_dispatch(int cnt, F&& body) {
+template <bool LSE, typename F>
+__device__ __forceinline__ void trial_dispatch_k(int cnt, F& body) {
     if (cnt <= 4)
-        body.template operator()<4>();
+        body.template operator()<4, LSE>();
     else if (cnt <= 6)
-        body.template operator()<6>();
+        body.template operator()<6, LSE>();
     else if (cnt <= 8)
-        body.template operator()<8>();
+        body.template operator()<8, LSE>();
     else if (cnt <= 10)
-        body.template operator()<10>();
+        body.template operator()<10, LSE>();
     else if (cnt <= 12)
-        body.template operator()<12>();
+        body.template operator()<12, LSE>();
     else if (cnt <= 14)
-        body.template operator()<14>();
+        body.template operator()<14, LSE>();
     else
-        body.template operator()<16>();
+        body.template operator()<16, LSE>();
+}
+
+// ... and on the estimator (uniform for the whole run): body<KT, LSE>.
+template <typename F>
+__device__ __forceinline__ void trial_dispatch(int cnt, int est, F&& body) {
+    if (est == PTYGER_EST_LS)
+        trial_dispatch_k<true>(cnt, body);
+    else
+        trial_dispatch_k<false>(cnt, body);
 }
 
 // Block-level output of the screening partials: per-lane fp64 running total `tot` of entry

@@ -10,7 +10,7 @@ namespace pty {
 constexpr int KC = 16;       // LS trial capacity of one pass over the frames
 constexpr int KMIN = 4;      // smallest adaptive pass-0 trial count
 constexpr int SMAX = 64;     // max trials per iteration (max_shrinks bound)
-constexpr int NDY = 6;       // DY partial sums per tile
+constexpr int NDY = 7;       // DY partial sums per tile (+ Re<g, g_prev> for Polak-Ribiere)
 constexpr int LSP = KC + 4;  // screening partials: [S_0..S_{KC-1} | A, D, sum|a|, sum b]
 constexpr int LSW = LSP + 4; // reduced LS vector in DevState (eta^2 at LS_ETA)
 constexpr int LS_ETA = LSW - 1;
@@ -50,11 +50,13 @@ struct Geometry {
     int64_t own_lo, own_hi;  // owned rows, storage-local coordinates (for reductions)
     int64_t band_lo0, band_hi0, band_lo1, band_hi1;  // storage-local band rows excluded from k_adj partials
     int64_t n_local;         // frames stored on this rank
+    int est;                 // estimator (PTYGER_EST_ML / PTYGER_EST_LS) for the residual and F terms
 };
 
 struct SolverCfg {
     double gamma0, tau, t, eps;
     int max_shrinks, direction, K;   // K = trials per extra pass and cap of the adaptive pass 0 (<= KC)
+    int est;                         // PTYGER_EST_ML / PTYGER_EST_LS
 };
 
 // Trials [base, base + count) evaluated by LS pass p (host and device agree on this rule).
@@ -99,6 +101,7 @@ int launch_pick(DevState* st, const SolverCfg& c, int pass, int exact_mode, int 
 int launch_upd(const Geometry& g, float2* psi, const float2* eta, const DevState* st, int grid,
                cudaStream_t s);
 int launch_begin_iter(DevState* st, cudaStream_t s);
+int launch_fold(const Geometry& g, float2* u, const float2* v, DevState* st, int grid, cudaStream_t s);
 int launch_validate_d(const float* d, int64_t count, int64_t frame_elems, unsigned long long* bad,
                       cudaStream_t s);
 int launch_set_F(DevState* st, const double* src, int keff0, cudaStream_t s);

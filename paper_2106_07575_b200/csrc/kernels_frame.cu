@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(512, 1) k_fwd(Geometry g, const float2* __rest
                     u[o] = uu;
                     if (d) {  // d == nullptr: transform only (v = G eta for the split line search)
                         const float cc = uu.x * uu.x + uu.y * uu.y;
-                        fs += cc - __ldg(d + o) * logf(fmaxf(cc, eps2));
+                        fs += objective_term(cc, __ldg(d + o), eps2, g.est);
                     }
                 }
                 facc += (double)fs;
@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(512, 1) k_grad(Geometry g, float2* __restrict_
                     }
                 }
 #pragma unroll
-                for (int n1 = 0; n1 < R; ++n1) x[n1] = residual(uu[n1], dd[n1], eps2);
+                for (int n1 = 0; n1 < R; ++n1) x[n1] = residual(uu[n1], dd[n1], eps2, g.est);
             } else {
 #pragma unroll
                 for (int n1 = 0; n1 < R; ++n1) x[n1] = make_float2(0.f, 0.f);
@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(512, 1) k_ls(Geometry g, const float2* __restr
             // d > 0 compaction ring is warp-collective
             const bool valid = i < nfr;
             const int64_t j = valid ? order[i] : 0;
-            if (cnt > 0) trial_dispatch(cnt, [&]<int KT>() {
+            if (cnt > 0) trial_dispatch(cnt, cfg.est, [&]<int KT, bool LSE>() {
                 constexpr int G4 = (R >= 4) ? 4 : R;
                 LsQState qs;
                 float2 un[G4];
@@ -310,10 +310,10 @@ __global__ void __launch_bounds__(512, 1) k_ls(Geometry g, const float2* __restr
                         float2 vv = cscale(scol[(T * ((q / T) * T + t) + q % T) * LD], scale);
                         if (valid) v[off(q)] = vv;
                         else vv = make_float2(0.f, 0.f);
-                        ls_push<KT>(wq[warp], qs, uc[jj], vv, dc[jj], sgam, eps2, S, m, lane);
+                        ls_push<KT, LSE>(wq[warp], qs, uc[jj], vv, dc[jj], sgam, eps2, S, m, lane);
                     }
                 }
-                ls_flush<KT>(wq[warp], qs, sgam, eps2, S, m, lane);
+                ls_flush<KT, LSE>(wq[warp], qs, sgam, eps2, S, m, lane);
             });
             double dv[KC];
 #pragma unroll

@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(512, 1) k_grad128(Geometry g, float2* __restri
             }
             float2 x[R];
 #pragma unroll
-            for (int n1 = 0; n1 < R; ++n1) x[n1] = residual(uu[n1], dd[n1], eps2);
+            for (int n1 = 0; n1 < R; ++n1) x[n1] = residual(uu[n1], dd[n1], eps2, g.est);
             row_fft<N, true>(x, sf + row * LD, t, tw);
         }
         __syncthreads();

@@ -94,6 +94,7 @@ __global__ void __launch_bounds__(256) k_adj(Geometry g, const float2* __restric
                     const float2 eg = cconjmul(et, acc[i]);
                     s[4] += eg.x;
                     s[5] += eg.y;
+                    s[6] += acc[i].x * gp.x + acc[i].y * gp.y;
                 }
             }
         }
@@ -136,6 +137,7 @@ __global__ void __launch_bounds__(256) k_band_add(float2* __restrict__ gcur, con
             const float2 eg = cconjmul(et, gv);
             s[4] += eg.x;
             s[5] += eg.y;
+            s[6] += gv.x * gp.x + gv.y * gp.y;
         }
     }
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -203,7 +205,21 @@ __global__ void k_dir(DevState* st, SolverCfg c) {
         st->gamma = 0.0;
         return;
     }
-    if (st->m > 0) {
+    if (c.direction == PTYGER_DIR_GD) {
+        // Eq.4: steepest descent, eta = -g every iteration (alpha = 0, not a restart)
+    } else if (c.direction == PTYGER_DIR_PR && st->m > 0) {
+        // Polak-Ribiere+ (P:443): beta = max(0, Re<g, g - g_prev>) / ||g_prev||^2
+        const double gp2 = st->dy[3];
+        if (gp2 < 1e-30) {
+            restarted = 1;
+        } else {
+            are = fmax(0.0, (gg - st->dy[6]) / gp2);
+            if (!isfinite(are)) {
+                are = 0.0;
+                restarted = 1;
+            }
+        }
+    } else if (st->m > 0) {
         double dre, dim;
         if (c.direction == PTYGER_DIR_FR) {
             dre = st->dy[3];
@@ -287,12 +303,12 @@ __global__ void __launch_bounds__(256) k_lsx(int64_t count, const float2* __rest
             LsMom m;
 #pragma unroll
             for (int k = 0; k < KC; ++k) S[k] = 0.f;
-            trial_dispatch(cnt, [&]<int KT>() {
+            trial_dispatch(cnt, cfg.est, [&]<int KT, bool LSE>() {
                 if constexpr (EXACT) {
 #pragma unroll 4
                     for (int i = 0; i < RUN; ++i) {
                         const int64_t o = e0 + (int64_t)i * blockDim.x + tid;
-                        if (o < count) ls_exact<KT>(u[o], v[o], __ldg(d + o), sgam, eps2, S);
+                        if (o < count) ls_exact<KT, LSE>(u[o], v[o], __ldg(d + o), sgam, eps2, S);
                     }
                 } else {
                     // warp-collective d > 0 compaction: out-of-range lanes push zeros
@@ -301,11 +317,11 @@ __global__ void __launch_bounds__(256) k_lsx(int64_t count, const float2* __rest
                     for (int i = 0; i < RUN; ++i) {
                         const int64_t o = e0 + (int64_t)i * blockDim.x + tid;
                         const bool ok = o < count;
-                        ls_push<KT>(wq[tid >> 5], qs, ok ? u[o] : make_float2(0.f, 0.f),
+                        ls_push<KT, LSE>(wq[tid >> 5], qs, ok ? u[o] : make_float2(0.f, 0.f),
                                     ok ? v[o] : make_float2(0.f, 0.f), ok ? __ldg(d + o) : 0.f, sgam, eps2, S, m,
                                     lane);
                     }
-                    ls_flush<KT>(wq[tid >> 5], qs, sgam, eps2, S, m, lane);
+                    ls_flush<KT, LSE>(wq[tid >> 5], qs, sgam, eps2, S, m, lane);
                 }
             });
             double dv[KC];
@@ -332,6 +348,17 @@ __global__ void k_pick(DevState* st, SolverCfg c, int pass, int exact_mode, int 
     if (pass == 0 && !exact_mode) st->eta2 = st->ls_pass[LS_ETA];
     int base, cnt;
     ls_pass_range(pass, st->keff, c, base, cnt);
+    if (c.direction == PTYGER_DIR_GD && !exact_mode && !st->numeric_error && pass == 0) {
+        // Eq.4: the constant step gamma0 is taken whatever F does (no line search); the
+        // (screened) DeltaF only updates the cached F for the trace
+        st->ls_hist[0] = st->ls_pass[0];
+        st->ls_bnd[0] = 0.0;
+        st->n_eval = 1;
+        st->accepted = 1;
+        st->kstar = 0;
+        st->gamma = c.gamma0;
+        st->F += st->ls_pass[0];
+    }
     if (!st->numeric_error && !st->accepted && cnt > 0) {
         if (!exact_mode) {
             const double A = st->ls_pass[KC], D = st->ls_pass[KC + 1];
@@ -428,6 +455,27 @@ __global__ void __launch_bounds__(256) k_upd(Geometry g, float2* __restrict__ ps
     }
 }
 
+// Applies the pending lazy far-field update (R#11, u <- u + gamma v, the same fmaf as k_grad) in
+// place; k_clear_gamma then zeroes gamma so the next k_grad does not apply it again.  Used by
+// ptyger_get_farfield so the far field it returns is G psi_m of the returned object.
+__global__ void __launch_bounds__(256) k_fold(int64_t count, float2* __restrict__ u, const float2* __restrict__ v,
+                                              const DevState* __restrict__ st) {
+    if (st->numeric_error) return;
+    const float gam = (float)st->gamma;
+    if (gam == 0.0f) return;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+        const float2 w = v[i];
+        float2 a = u[i];
+        a.x = fmaf(gam, w.x, a.x);
+        a.y = fmaf(gam, w.y, a.y);
+        u[i] = a;
+    }
+}
+
+__global__ void k_clear_gamma(DevState* st) {
+    if (!st->numeric_error) st->gamma = 0.0;
+}
+
 // d must be finite and >= 0: records the smallest offending frame index.
 __global__ void k_validate_d(const float* __restrict__ d, int64_t count, int64_t frame_elems,
                              unsigned long long* bad) {
@@ -482,6 +530,13 @@ int launch_pick(DevState* st, const SolverCfg& c, int pass, int exact_mode, int 
 int launch_upd(const Geometry& g, float2* psi, const float2* eta, const DevState* st, int grid,
                cudaStream_t s) {
     k_upd<<<grid, 256, 0, s>>>(g, psi, eta, st);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+int launch_fold(const Geometry& g, float2* u, const float2* v, DevState* st, int grid, cudaStream_t s) {
+    k_fold<<<grid, 256, 0, s>>>(g.n_local * (int64_t)g.N * g.N, u, v, st);
+    if (cudaGetLastError() != cudaSuccess) return -1;
+    k_clear_gamma<<<1, 1, 0, s>>>(st);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 

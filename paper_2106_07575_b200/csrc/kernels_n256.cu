@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(512, 1) k_grad256(Geometry g, float2* __restri
             }
             float2 x[R];
 #pragma unroll
-            for (int n1 = 0; n1 < R; ++n1) x[n1] = residual(uu[n1], dd[n1], eps2);
+            for (int n1 = 0; n1 < R; ++n1) x[n1] = residual(uu[n1], dd[n1], eps2, g.est);
             float2* srow = buf + (tid / T) * LD;
             __syncwarp();
             row_fft_regs<N, true>(x, srow, t, tw);
@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(512, 1) k_lsfwd256(Geometry g, const float2* _
                     const float2 uu = cscale(X[k2], scale);
                     u[o] = uu;
                     const float cc = uu.x * uu.x + uu.y * uu.y;
-                    if (d) fs += cc - __ldg(d + o) * logf(fmaxf(cc, eps2));
+                    if (d) fs += objective_term(cc, __ldg(d + o), eps2, g.est);
                 }
                 facc += (double)fs;
             } else {
@@ -202,16 +202,16 @@ __global__ void __launch_bounds__(512, 1) k_lsfwd256(Geometry g, const float2* _
                 float2* mine = buf + (T * t) * COLB + (c - cb * COLB);
 #pragma unroll
                 for (int k2 = 0; k2 < T; ++k2) mine[k2 * COLB] = X[k2];
-                if (cnt > 0) trial_dispatch(cnt, [&]<int KT>() {
+                if (cnt > 0) trial_dispatch(cnt, cfg.est, [&]<int KT, bool LSE>() {
                     LsQState qs;
 #pragma unroll 1
                     for (int k2 = 0; k2 < T; ++k2) {
                         const int64_t o = j * N * N + (int64_t)(t + R * k2) * N + c;
                         const float2 vv = cscale(mine[k2 * COLB], scale);
                         v[o] = vv;
-                        ls_push<KT>(wq[tid >> 5], qs, u[o], vv, __ldg(d + o), sgam, eps2, S, m, lane);
+                        ls_push<KT, LSE>(wq[tid >> 5], qs, u[o], vv, __ldg(d + o), sgam, eps2, S, m, lane);
                     }
-                    ls_flush<KT>(wq[tid >> 5], qs, sgam, eps2, S, m, lane);
+                    ls_flush<KT, LSE>(wq[tid >> 5], qs, sgam, eps2, S, m, lane);
                 });
                 double dv[K];
 #pragma unroll

@@ -252,3 +252,80 @@ def test_single_frame_and_device_inputs(L):
     g_ref, _ = O.gradient(np.ones_like(psi_true), c128(p), sc, dd.astype(np.float64))
     assert tr[0]["iter"] == 0 and np.isfinite(tr[1]["F"])
     pt.close()
+
+
+# ------------------------------------------------------------------ f2 / f3: estimator and direction variants
+
+@pytest.mark.parametrize("name", ["n32", "n128", "n256"])
+@pytest.mark.parametrize("direction", [0, 3])
+def test_teacher_forced_ls_estimator_and_pr(L, name, direction):
+    """Least-squares (Gaussian) estimator (R#19) with Dai-Yuan, and Polak-Ribiere+ (f3) with
+    it: gradient, beta/alpha, LS partials (difference form ls_delta_ls) and the accepted trial
+    against the oracle from the same teacher-forced state."""
+    psi_true, p, scan, d = get_fixture(name)
+    d64 = d.astype(np.float64)
+    p64 = c128(p)
+    pt = L.Ptyger(np.ones_like(psi_true), p, scan, d, direction=direction, estimator=L.EST_LS)
+    for m in range(5):
+        psi_m, g_prev, eta_prev, F_m, mm = pt.get_state()
+        pt.set_state(psi_m, g_prev, eta_prev, m)
+        g_ref, alpha_ref, eta_ref, rs_ref, u_ref = O.grad_at(c128(psi_m), c128(g_prev), c128(eta_prev), m, p64,
+                                                            scan, d64, variant=direction, est=O.EST_LS)
+        F_ref = O.objective_F_ls(u_ref, d64)
+        assert abs(F_m - F_ref) <= 2e-6 * abs(F_ref) or m > 0
+        tr = pt.iterate(1)[0]
+        assert rel(pt.get_gradient(), g_ref) <= 1e-4, (m, rel(pt.get_gradient(), g_ref))
+        if m > 0 and not rs_ref:
+            gg = float(np.sum(np.abs(g_ref) ** 2))
+            gp = float(np.sum(np.abs(c128(g_prev)) ** 2))
+            assert abs(complex(tr["alpha_re"], tr["alpha_im"]) - alpha_ref) <= 1e-3 * abs(alpha_ref) + 1e-4 * gg / gp
+        _, _, eta_m, _, _ = pt.get_state()
+        v_ref = O.forward_G(c128(eta_m), p64, scan)
+        dF, bnd = pt.get_ls_partials(with_bound=True)
+        refs = []
+        for k, val in enumerate(dF):
+            gk = 0.5 ** k
+            ref = O.ls_delta_ls(u_ref, v_ref, d64, gk)
+            refs.append(ref)
+            scale = np.sum(np.abs(u_ref + gk * v_ref) ** 2) + np.sum(np.abs(u_ref) ** 2) + np.sum(d64)
+            assert abs(val - ref) <= max(1e-5 * scale, 2 * bnd[k]), (m, k, val, ref, scale, bnd[k])
+        kref = next((k for k, r in enumerate(refs) if r <= 0), None)
+        if kref is not None and not tr["stalled"]:
+            scale = np.sum(np.abs(u_ref) ** 2) + np.sum(d64)
+            if min(abs(r) for r in refs[:kref + 1]) > 1e-5 * scale:
+                assert tr["shrinks"] == kref
+        # F cached after the step is the LS objective at psi_{m+1} by definition
+        psi_n, _, _, F_n, _ = pt.get_state()
+        F_def = O.objective_F_ls(O.forward_G(c128(psi_n), p64, scan), d64)
+        assert abs(F_n - F_def) <= 1e-5 * (np.sum(np.abs(u_ref) ** 2) + np.sum(d64))
+    pt.close()
+
+
+@pytest.mark.parametrize("est", [0, 1])
+def test_gradient_descent_steps(L, est):
+    """Eq.4 gradient descent (direction GD): psi_{m+1} = psi_m - gamma0 grad F(psi_m), one
+    fixed step per iteration (no line search), against oracle.gd_iterate from the same psi."""
+    psi_true, p, scan, d = get_fixture("n64")
+    d64 = d.astype(np.float64)
+    p64 = c128(p)
+    Ill = O.illumination(p64, scan, psi_true.shape)
+    gamma0 = 0.5 / float(Ill.max())
+    pt = L.Ptyger(np.ones_like(psi_true), p, scan, d, direction=L.DIR_GD, gamma0=gamma0, estimator=est)
+    Fs = []
+    for m in range(4):
+        psi_m, _, _, _, _ = pt.get_state()
+        psi_ref = O.gd_iterate(c128(psi_m), p64, scan, d64, gamma0, est=est)
+        tr = pt.iterate(1)[0]
+        assert tr["shrinks"] == 0 and tr["gamma"] == gamma0 and tr["alpha_re"] == 0.0 and tr["alpha_im"] == 0.0
+        step = np.linalg.norm(psi_ref - c128(psi_m))
+        got = pt.get_object()
+        assert np.linalg.norm(got - psi_ref) <= 2e-6 * np.linalg.norm(psi_ref) + 1e-4 * step, m
+        objective = O.objective_F_ls if est else O.objective_F
+        u_new = O.forward_G(c128(got), p64, scan)
+        F_def = objective(u_new, d64)
+        a2 = np.abs(u_new) ** 2
+        scale = np.sum(a2) + np.sum(d64 * (1.0 + np.abs(np.log(np.maximum(a2, 1e-30)))))
+        assert abs(tr["F"] - F_def) <= 1e-5 * scale
+        Fs.append(tr["F"])
+    assert Fs[-1] < Fs[0]
+    pt.close()

@@ -213,3 +213,67 @@ def test_gd_update_trivial_cases():
     y = np.ones_like(psi_true)
     F = lambda z: O.objective_F(O.forward_G(z, p, scan), d)
     assert F(O.gd_iterate(y, p, scan, d, 1.0 / 64)) < F(y)
+
+
+# ---------------------------------------------------------------- LS estimator (R#19)
+
+def test_ls_estimator_closed_forms_and_fd():
+    rng = np.random.default_rng(5)
+    d = rng.uniform(0.1, 4, size=(2, 8, 8))
+    u_eq = np.sqrt(d) * np.exp(1j * rng.uniform(0, 6, size=d.shape))
+    assert O.objective_F_ls(u_eq, d) < 1e-24                         # F = 0 iff |u| = sqrt d
+    u = I.random_complex(d.shape, seed=3)
+    assert abs(O.objective_F_ls(u, np.zeros_like(d)) - np.sum(np.abs(u) ** 2)) < 1e-12
+    H, N, n = 32, 8, 9
+    scan = rng.integers(0, H - N + 1, size=(n, 2))
+    p = I.make_probe(N)
+    psi = I.random_complex((H, H), seed=21, scale=0.5) + 1.0
+    dd = rng.uniform(0, 4, size=(n, N, N))
+    g, _ = O.gradient_ls(psi, p, scan, dd)
+    F = lambda x: O.objective_F_ls(O.forward_G(x, p, scan), dd)
+    for k in range(4):
+        delta = I.random_complex((H, H), seed=200 + k) * (1j if k % 2 else 1)
+        fd = (F(psi + 1e-6 * delta) - F(psi - 1e-6 * delta)) / 2e-6
+        assert abs(fd - 2 * np.real(np.vdot(g, delta))) <= 1e-6 * abs(fd)
+
+
+def test_ls_estimator_stationary_and_delta():
+    psi_true, p, scan, _ = tiny_problem()
+    d = np.abs(O.forward_G(psi_true, p, scan)) ** 2
+    g, _ = O.gradient_ls(psi_true, p, scan, d)
+    assert np.linalg.norm(g) <= 1e-12 * np.linalg.norm(psi_true)
+    psi = np.ones_like(psi_true)
+    eta = I.random_complex(psi.shape, seed=12, scale=0.1)
+    u, v = O.forward_G(psi, p, scan), O.forward_G(eta, p, scan)
+    for gm in [1.0, 0.25, 2.0 ** -10]:
+        ref = O.objective_F_ls(u + gm * v, d) - O.objective_F_ls(u, d)
+        assert abs(O.ls_delta_ls(u, v, d, gm) - ref) <= 1e-10 * (np.sum(np.abs(u) ** 2) + np.sum(d))
+
+
+def test_ls_estimator_cg_monotone_recovery():
+    psi_true, p, scan, _ = tiny_problem()
+    d = np.abs(O.forward_G(psi_true, p, scan)) ** 2
+    st, trs = O.run_cg(np.ones_like(psi_true), p, scan, d, 60, est=O.EST_LS)
+    F = [t.F for t in trs]
+    assert all(F[i + 1] <= F[i] for i in range(len(F) - 1))
+    assert F[-1] < 2e-2 * F[0]          # measured 831 -> 8.5 in 60 iterations
+
+
+@pytest.mark.parametrize("variant", [O.DIR_PR])
+def test_pr_terminates_on_quadratic(variant):
+    """Polak-Ribiere (P:443 cites Polak / Polyak) equals DY / FR on a quadratic with exact
+    line search, hence n-step termination."""
+    n = 6
+    rng = np.random.default_rng(4)
+    M = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    A = M.conj().T @ M + 0.5 * np.eye(n)
+    b = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    x = np.zeros(n, complex)
+    g_prev = eta_prev = None
+    for m in range(n):
+        g = A @ x - b
+        eta, beta, rs = O.direction(g, g_prev, eta_prev, variant)
+        gamma = -np.real(np.vdot(eta, g)) / np.real(np.vdot(eta, A @ eta))
+        x = x + gamma * eta
+        g_prev, eta_prev = g, eta
+    assert np.linalg.norm(A @ x - b) < 1e-9 * np.linalg.norm(b)
