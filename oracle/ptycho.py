@@ -402,10 +402,11 @@ def round_positions(raw) -> np.ndarray:
     return np.floor(raw + 0.5).astype(np.int64)
 
 
-def gradient_f32(psi, probe, scan, d, eps: float = EPS):
+def gradient_f32(psi, probe, scan, d, eps: float = EPS, est: int = EST_ML):
     """The same Eq.3 formula evaluated in plain complex64/float32 NumPy (no reordering):
     the 'e32' yardstick of the teacher-forced tolerance (DESIGN.md Parity protocol,
-    SURVEY 8(c).4 item 2).  Returns grad as complex128 for comparison."""
+    SURVEY 8(c).4 item 2).  est = EST_LS evaluates the R#19 residual u - sqrt(d) u/|u|
+    instead.  Returns grad as complex128 for comparison."""
     psi = np.asarray(psi, np.complex64)
     probe = np.asarray(probe, np.complex64)
     d = np.asarray(d, np.float32)
@@ -417,6 +418,8 @@ def gradient_f32(psi, probe, scan, d, eps: float = EPS):
         a2 = (u.real * u.real + u.imag * u.imag).astype(np.float32)
         ok = a2 >= np.float32(eps) * np.float32(eps)
         q = np.where(ok, d[j] / np.where(ok, a2, np.float32(1)), np.float32(0)).astype(np.float32)
+        if est == EST_LS:
+            q = np.sqrt(q).astype(np.float32)
         res = (u - q * u).astype(np.complex64)
         acc[r:r + N, c:c + N] += np.conj(probe) * np.fft.ifft2(res, norm="ortho").astype(np.complex64)
     return acc.astype(np.complex128)

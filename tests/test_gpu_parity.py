@@ -274,7 +274,8 @@ def test_teacher_forced_ls_estimator_and_pr(L, name, direction):
         F_ref = O.objective_F_ls(u_ref, d64)
         assert abs(F_m - F_ref) <= 2e-6 * abs(F_ref) or m > 0
         tr = pt.iterate(1)[0]
-        assert rel(pt.get_gradient(), g_ref) <= 1e-4, (m, rel(pt.get_gradient(), g_ref))
+        e32 = rel(O.gradient_f32(psi_m, p, scan, d, est=O.EST_LS), g_ref)
+        assert rel(pt.get_gradient(), g_ref) <= max(1e-4, 4 * e32), (m, rel(pt.get_gradient(), g_ref), e32)
         if m > 0 and not rs_ref:
             gg = float(np.sum(np.abs(g_ref) ** 2))
             gp = float(np.sum(np.abs(c128(g_prev)) ** 2))
@@ -304,22 +305,26 @@ def test_teacher_forced_ls_estimator_and_pr(L, name, direction):
 @pytest.mark.parametrize("est", [0, 1])
 def test_gradient_descent_steps(L, est):
     """Eq.4 gradient descent (direction GD): psi_{m+1} = psi_m - gamma0 grad F(psi_m), one
-    fixed step per iteration (no line search), against oracle.gd_iterate from the same psi."""
+    fixed step per iteration (no line search), against oracle.gd_iterate from the same psi.
+    Starts near the truth: from a flat object the ML gradient is dominated by d/|u| at
+    near-zero far-field pixels and a fixed step is meaningless."""
     psi_true, p, scan, d = get_fixture("n64")
     d64 = d.astype(np.float64)
     p64 = c128(p)
     Ill = O.illumination(p64, scan, psi_true.shape)
-    gamma0 = 0.5 / float(Ill.max())
-    pt = L.Ptyger(np.ones_like(psi_true), p, scan, d, direction=L.DIR_GD, gamma0=gamma0, estimator=est)
+    gamma0 = 0.25 / float(Ill.max())
+    psi0 = 0.9 * psi_true + 0.05 * I.random_complex(psi_true.shape, seed=7)
+    pt = L.Ptyger(psi0, p, scan, d, direction=L.DIR_GD, gamma0=gamma0, estimator=est)
     Fs = []
     for m in range(4):
         psi_m, _, _, _, _ = pt.get_state()
         psi_ref = O.gd_iterate(c128(psi_m), p64, scan, d64, gamma0, est=est)
+        e32 = rel(O.gradient_f32(psi_m, p, scan, d, est=est), (c128(psi_m) - psi_ref) / gamma0)
         tr = pt.iterate(1)[0]
         assert tr["shrinks"] == 0 and tr["gamma"] == gamma0 and tr["alpha_re"] == 0.0 and tr["alpha_im"] == 0.0
         step = np.linalg.norm(psi_ref - c128(psi_m))
         got = pt.get_object()
-        assert np.linalg.norm(got - psi_ref) <= 2e-6 * np.linalg.norm(psi_ref) + 1e-4 * step, m
+        assert np.linalg.norm(got - psi_ref) <= 2e-6 * np.linalg.norm(psi_ref) + max(1e-4, 4 * e32) * step, (m, e32)
         objective = O.objective_F_ls if est else O.objective_F
         u_new = O.forward_G(c128(got), p64, scan)
         F_def = objective(u_new, d64)
@@ -329,3 +334,28 @@ def test_gradient_descent_steps(L, est):
         Fs.append(tr["F"])
     assert Fs[-1] < Fs[0]
     pt.close()
+
+
+def test_view_batch_equals_independent_views(L):
+    """f1 (3-D view batch): the views are independent 2-D problems, so a ViewBatch iteration of
+    every view is bit-identical to running each view alone, and each matches the oracle."""
+    w = I.Workload("vtiny", H=64, W=64, N=16, k=7, step=8, jitter=1, seed=9, photons=1e2, views=3)
+    views = []
+    for v in range(w.views):
+        psi_true, p, scan = I.view_inputs(w, v)
+        d = I.poisson_counts(w.photons * np.abs(O.forward_G(psi_true, p, scan)) ** 2, w.seed + v)
+        views.append((np.ones_like(psi_true), p, scan, np.asarray(d, np.float32)))
+    vb = L.ViewBatch(views)
+    trs = vb.iterate(3)
+    for v, (o, p, scan, d) in enumerate(views):
+        pt = L.Ptyger(o, p, scan, d)
+        tr = pt.iterate(3)
+        assert [t["shrinks"] for t in tr] == [t["shrinks"] for t in trs[v]]
+        assert np.array_equal(pt.get_object(), vb.views[v].get_object())
+        st, otr = O.run_cg(c128(o), c128(p), scan, d.astype(np.float64), 3)
+        assert [t.shrinks for t in otr] == [t["shrinks"] for t in tr]
+        assert rel(pt.get_object(), st.psi) <= 1e-3
+        pt.close()
+    # rotated phantoms: the views really differ
+    assert rel(vb.views[0].get_object(), vb.views[1].get_object()) > 1e-3
+    vb.close()

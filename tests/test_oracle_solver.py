@@ -277,3 +277,18 @@ def test_pr_terminates_on_quadratic(variant):
         x = x + gamma * eta
         g_prev, eta_prev = g, eta
     assert np.linalg.norm(A @ x - b) < 1e-9 * np.linalg.norm(b)
+
+
+@pytest.mark.parametrize("est", [O.EST_ML, O.EST_LS])
+def test_gradient_f32_yardstick_tracks_fp64(est):
+    """The e32 yardstick evaluates the same formula as the fp64 gradient: on a well-conditioned
+    state (near the truth, no near-zero far-field pixels dominate) it agrees to fp32 rounding,
+    and a dropped term (the residual's data part) is far outside that."""
+    psi_true, p, scan, d = tiny_problem(noisy=True)
+    psi = 0.9 * psi_true + 0.05 * I.random_complex(psi_true.shape, seed=3)
+    g64, far = O._estimator(est)[1](psi, p, scan, d)
+    g32 = O.gradient_f32(psi, p, scan, d, est=est)
+    e = np.linalg.norm(g32 - g64) / np.linalg.norm(g64)
+    assert e < 1e-5
+    g_nodata = O.adjoint_GH(far, p, scan, psi.shape)
+    assert np.linalg.norm(g_nodata - g64) / np.linalg.norm(g64) > 1e-2
