@@ -80,9 +80,15 @@ __device__ __forceinline__ double trial_gamma(double gamma0, double tau, int k) 
 __device__ __forceinline__ float2 residual(float2 u, float dd, float eps2, int est = PTYGER_EST_ML) {
     const float c = u.x * u.x + u.y * u.y;
     if (c >= eps2) {
-        // correctly rounded division: where |u| is small and d > 0 the residual is ill-conditioned
-        // and a 2-ulp approximate quotient measurably inflated the gradient error
-        float s = __fdiv_rn(dd, c);
+        // d / c to <= 1 ulp (MUFU reciprocal + one Newton correction of the quotient): where |u| is
+        // small and d > 0 the residual is ill-conditioned and a 2-ulp approximate
+        // quotient measurably inflated the gradient error; __fdiv_rn's slow-path call cost the
+        // GRAD kernel 18 %.  c >= eps^2 = 1e-32 is a normal float, so the FTZ reciprocal is exact
+        // to 1 ulp over the whole guarded range.
+        float r;
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(c));
+        float s = dd * r;
+        s = fmaf(fmaf(-c, s, dd), r, s);
         if (est == PTYGER_EST_LS) s = __fsqrt_rn(s);
         return make_float2(u.x - s * u.x, u.y - s * u.y);
     }
@@ -192,15 +198,15 @@ __device__ __forceinline__ void ls_exact(float2 uu, float2 vv, float dd, const f
     for (int k = 0; k < KT; ++k) acc[k] += t[k];
 }
 
-// SCREENING terms.  cn = |u + gamma v|^2 is formed from the components of u + gamma v, so
-// w = cn / c keeps a few-ulp RELATIVE accuracy even when u + gamma v nearly cancels, and
-// q = cn - c (absolute error <= 2^-23 (cn + c)); log2 w on the MUFU without denormal fix-up
-// (lg2.approx.ftz: |abs err| <= 2^-22 on [0.5, 2], 2 ulp relative elsewhere).  Per trial:
-// 8 FMA-pipe ops, 2 ALU ops, 1 MUFU.  Accumulates S_k = sum t_k; the caller also accumulates
-// A = sum d max_k |ln w_k|, D = sum (d + 0.12 c), sum |a|, sum b, which bound the error of every
-// trial of the pass:
+// SCREENING terms.  cn = |u + gamma v|^2 is formed from the components of u + gamma v (each an
+// fma of exact inputs, correctly rounded), so w = cn / c keeps a few-ulp RELATIVE accuracy even
+// when u + gamma v nearly cancels; log2 w on the MUFU without denormal fix-up (lg2.approx.ftz:
+// |abs err| <= 2^-22 on [0.5, 2], 2 ulp relative elsewhere).  The non-log part q_k = gamma_k a +
+// gamma_k^2 b (a = 2 Re(u* v), b = |v|^2) enters through per-pixel moments (LsQState).  Per
+// trial: 7 FMA-pipe ops, 1 ALU op, 1 MUFU.  The caller also accumulates A = sum d max_k |ln w_k|,
+// D = sum (d + 0.12 c), sum |a|, sum b, which bound the error of every trial of the pass:
 //     |S_k - t_exact| <= LS_EPS_D D + LS_EPS_R (A + gamma_k sum|a| + gamma_k^2 sum b)
-// (the 0.12 c part of D covers the rounding of q = cn - c: 2e-6 * 0.12 = 2.4e-7 >= 2 * 2^-23).
+// (the 0.12 c part of D covers the rounding of the q moments: 2e-6 * 0.12 = 2.4e-7 >= 2 * 2^-23).
 // |u| < eps makes w = 0 -> S non-finite -> the exact pass decides (guarded definition, R#4).
 constexpr double LS_EPS_D = 2e-6;
 constexpr double LS_EPS_R = 2e-6;
@@ -215,32 +221,6 @@ __device__ __forceinline__ float lg2_ftz(float x) {
 struct LsMom {
     float A = 0.f, D = 0.f, sa = 0.f, sb = 0.f;
 };
-
-// KT trials are computed (compile time: no predicated-off work); S has room for K >= KT.
-template <int KT, int K>
-__device__ __forceinline__ void ls_screen(float2 uu, float2 vv, float dd, const float* sgam, float eps2,
-                                          float (&S)[K], LsMom& m) {
-    static_assert(KT <= K, "trial count above capacity");
-    const float a = 2.0f * fmaf(uu.x, vv.x, uu.y * vv.y);
-    const float b = fmaf(vv.x, vv.x, vv.y * vv.y);
-    const float c = fmaf(uu.x, uu.x, uu.y * uu.y);
-    const float rc = (c >= eps2) ? __fdividef(1.0f, c) : 0.0f;   // 2 ulp: inside the bound
-    const float dl = dd * 0.693147182464599609375f;
-    float amax = 0.f;
-#pragma unroll
-    for (int k = 0; k < KT; ++k) {
-        const float gam = sgam[k];
-        const float ex = fmaf(gam, vv.x, uu.x), ey = fmaf(gam, vv.y, uu.y);
-        const float cn = fmaf(ex, ex, ey * ey);
-        const float L2 = lg2_ftz(fmaxf(cn, eps2) * rc);
-        S[k] += fmaf(-dl, L2, cn - c);
-        amax = fmaxf(amax, fabsf(L2));
-    }
-    m.A = fmaf(dl, amax, m.A);
-    m.D += fmaf(0.12f, c, dd);
-    m.sa += fabsf(a);
-    m.sb += b;
-}
 
 // ---------------------------------------------------------------------------------------------
 // Sparse-data screening.  Poisson counts are 0 on most detector pixels (59 % at the bench
@@ -271,20 +251,27 @@ __device__ __forceinline__ void ls_screen_nz(float2 uu, float2 vv, float dd, con
         float amax = 0.f;
 #pragma unroll
         for (int k = 0; k < KT; ++k) {
+            // only the log part: q_k = gamma_k a + gamma_k^2 b of EVERY pixel goes to the (za, zb)
+            // moments in ls_push (one op per trial less than forming cn - c here)
             const float gam = sgam[k];
             const float ex = fmaf(gam, vv.x, uu.x), ey = fmaf(gam, vv.y, uu.y);
             const float cn = fmaf(ex, ex, ey * ey);
             const float L2 = lg2_ftz(fmaxf(cn, eps2) * rc);
-            S[k] += fmaf(-dl, L2, cn - c);
+            S[k] = fmaf(-dl, L2, S[k]);
             amax = fmaxf(amax, fabsf(L2));
         }
         m.A = fmaf(dl, amax, m.A);
     }
 }
 
+// za, zb: per lane sums of a, b.  Poisson ML: over ALL pixels (q_k = gamma_k a + gamma_k^2 b is
+// the whole non-log part of t_k, so the d > 0 screening only adds -d ln w_k).  Its rounding is
+// inside the screening bound: gamma |err a| <= 2^-23 (c + gamma^2 b) (AM-GM on 2|u||v|), covered
+// by the 0.12 c part of D and the gamma^2 sum b term.  LS estimator: over the d = 0 pixels only
+// (its d > 0 term is not separable).
 struct LsQState {
     int head = 0, pending = 0;   // warp-uniform
-    float za = 0.f, zb = 0.f;    // per lane: sum a, sum b over the d = 0 pixels it saw
+    float za = 0.f, zb = 0.f;
 };
 
 template <int KT, bool LSE, int K>
@@ -297,7 +284,7 @@ __device__ __forceinline__ void ls_push(LsWarpQ& q, LsQState& qs, float2 uu, flo
     m.sa += fabsf(a);
     m.sb += b;
     const bool nz = dd != 0.0f;
-    if (!nz) {
+    if (!LSE || !nz) {
         qs.za += a;
         qs.zb += b;
     }
@@ -319,7 +306,7 @@ __device__ __forceinline__ void ls_push(LsWarpQ& q, LsQState& qs, float2 uu, flo
     }
 }
 
-// Drain the ring and fold the d = 0 moments into S (call once per accumulation run).
+// Drain the ring and fold the (za, zb) moments into S (call once per accumulation run).
 template <int KT, bool LSE, int K>
 __device__ __forceinline__ void ls_flush(LsWarpQ& q, LsQState& qs, const float* sgam, float eps2, float (&S)[K],
                                          LsMom& m, int lane) {

@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(512, 1) k_grad(Geometry g, float2* __restrict_
 
 // ----------------------------------------------------------------------------------------
 // k_ls: LS stage first pass (Alg.1 659-668 with Eq.7): v_j = F(p * eta[window s_j]) written
-// to HBM, then the SCREENING terms (dev.cuh ls_screen) of the pass-0 trials gamma_k,
+// to HBM, then the SCREENING terms (dev.cuh ls_push / ls_screen_nz) of the pass-0 trials gamma_k,
 // k < keff (adaptive, read from the device state) against (u, d); per-CTA fp64 partials
 // [S_0..S_{KC-1} | A, D, sum|a|, sum b].
 // ----------------------------------------------------------------------------------------
@@ -275,18 +275,22 @@ __global__ void __launch_bounds__(512, 1) k_ls(Geometry g, const float2* __restr
             // d > 0 compaction ring is warp-collective
             const bool valid = i < nfr;
             const int64_t j = valid ? order[i] : 0;
+            // this thread's column c of frame j at row t: element q of its column sits at row
+            // (q / T) T + t + R (q % T); 32-bit in-frame offsets off a 64-bit frame base
+            const int64_t fb = j * (int64_t)(N * N) + (int64_t)t * N + c;
+            const float2* __restrict__ ub = u + fb;
+            const float* __restrict__ db = d + fb;
+            float2* __restrict__ vb = v + fb;
             if (cnt > 0) trial_dispatch(cnt, cfg.est, [&]<int KT, bool LSE>() {
                 constexpr int G4 = (R >= 4) ? 4 : R;
                 LsQState qs;
                 float2 un[G4];
                 float dn[G4];
-                auto off = [&](int q) {
-                    return j * N * N + (int64_t)((q / T) * T + t + R * (q % T)) * N + c;
-                };
+                auto off = [&](int q) -> int { return ((q / T) * T + R * (q % T)) * N; };
 #pragma unroll
                 for (int jj = 0; jj < G4; ++jj) {
-                    un[jj] = valid ? u[off(jj)] : make_float2(0.f, 0.f);
-                    dn[jj] = valid ? __ldg(d + off(jj)) : 0.f;
+                    un[jj] = valid ? ub[off(jj)] : make_float2(0.f, 0.f);
+                    dn[jj] = valid ? __ldg(db + off(jj)) : 0.f;
                 }
 #pragma unroll 1
                 for (int q0 = 0; q0 < R; q0 += G4) {
@@ -300,15 +304,15 @@ __global__ void __launch_bounds__(512, 1) k_ls(Geometry g, const float2* __restr
                     if (q0 + G4 < R && valid) {  // prefetch the next group's u, d
 #pragma unroll
                         for (int jj = 0; jj < G4; ++jj) {
-                            un[jj] = u[off(q0 + G4 + jj)];
-                            dn[jj] = __ldg(d + off(q0 + G4 + jj));
+                            un[jj] = ub[off(q0 + G4 + jj)];
+                            dn[jj] = __ldg(db + off(q0 + G4 + jj));
                         }
                     }
 #pragma unroll
                     for (int jj = 0; jj < G4; ++jj) {
                         const int q = q0 + jj;
                         float2 vv = cscale(scol[(T * ((q / T) * T + t) + q % T) * LD], scale);
-                        if (valid) v[off(q)] = vv;
+                        if (valid) vb[off(q)] = vv;
                         else vv = make_float2(0.f, 0.f);
                         ls_push<KT, LSE>(wq[warp], qs, uc[jj], vv, dc[jj], sgam, eps2, S, m, lane);
                     }

@@ -1,0 +1,16 @@
+#!/bin/bash
+# gpurun: bench (paper config), ncu launch list of the same command, and one `--set full` capture of
+# k_grad128 / k_ls / k_adj at the paper config.  Outputs under gpurun_out/ with the given tag.
+cd "${GRAFT_REPO_ROOT:-/root/repo}"
+mkdir -p gpurun_out
+TAG=${1:-r1c}
+python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
+timeout 600 python bench.py > gpurun_out/bench_${TAG}.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench_${TAG}.log
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}.csv \
+    python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 0 > gpurun_out/ncu_launch_${TAG}.log 2>&1
+echo "launch-list rc=$?" >> gpurun_out/ncu_launch_${TAG}.log
+timeout 1500 ncu --set full --clock-control none --import-source on -k 'regex:^(k_ls|k_grad128|k_adj|k_lsx)$' -s 6 -c 3 \
+    -o gpurun_out/prof_${TAG} -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --e2e-steps 0 \
+    > gpurun_out/ncu_full_${TAG}.log 2>&1
+echo "ncu rc=$?" >> gpurun_out/ncu_full_${TAG}.log
+tail -2 gpurun_out/bench_${TAG}.log | cut -c1-300; tail -2 gpurun_out/ncu_launch_${TAG}.log; tail -3 gpurun_out/ncu_full_${TAG}.log
