@@ -122,7 +122,7 @@ struct ptyger_ctx {
     Geometry geo{};
     // device
     float2 *psi = nullptr, *g[2] = {nullptr, nullptr}, *eta = nullptr, *u = nullptr, *v = nullptr,
-           *probe = nullptr, *full = nullptr, *recv[2] = {nullptr, nullptr};
+           *probe = nullptr, *probe_s = nullptr, *full = nullptr, *recv[2] = {nullptr, nullptr};
     float* d = nullptr;
     int2* pos = nullptr;
     int* order = nullptr;
@@ -139,6 +139,8 @@ struct ptyger_ctx {
     cudaEvent_t ev_it[2] = {nullptr, nullptr};
     float last_ms = 0.f;
     int grid_fr = 0, grid_el = 0;
+    bool hf = false;     // N = 128 half-frame cluster kernels (kernels_hf128.cu)
+    int parts_ls = 0;    // per-CTA partial rows written by the LS pass-0 frame kernel
     int m_host = 0;
     int64_t launches_per_iter = 0, last_launches = 0;
     bool failed_numeric = false;
@@ -205,7 +207,12 @@ static int enqueue_iteration(ptyger_ctx* c, int p, std::string& err, int64_t& la
     LK(launch_begin_iter(c->st, s)); ++launches;
     EV(1);
     // GRAD stage (Alg.1 648-649)
-    LK(launch_grad(g, c->u, c->v, c->d, c->probe, c->order, c->st, eps, c->grid_fr, s)); ++launches;
+    if (c->hf) {
+        LK(launch_grad_hf(g, c->u, c->v, c->d, c->probe_s, c->st, eps, s));
+    } else {
+        LK(launch_grad(g, c->u, c->v, c->d, c->probe, c->probe_s, c->st, eps, c->grid_fr, s));
+    }
+    ++launches;
     EV(2);
     LK(launch_adj(g, c->v, c->tile_ptr, c->entries, c->ntx, c->nty, gcur, gprev, c->eta, c->part_adj, c->st, s));
     ++launches;
@@ -246,8 +253,10 @@ static int enqueue_iteration(ptyger_ctx* c, int p, std::string& err, int64_t& la
     const bool split = getenv("PTYGER_LS_SPLIT") != nullptr;
     if (split) {
         LK(launch_fwd(g, c->eta, c->probe, c->pos, c->order, nullptr, c->v, c->part_fr, c->grid_fr, (float)sc.eps, s));
+    } else if (c->hf) {
+        LK(launch_ls_hf(g, c->eta, c->probe_s, c->pos, c->order, c->u, c->v, c->d, sc, c->part_fr, c->st, s));
     } else {
-        LK(launch_ls(g, c->eta, c->probe, c->pos, c->order, c->u, c->v, c->d, sc, c->part_fr, c->grid_fr, c->st, s));
+        LK(launch_ls(g, c->eta, c->probe, c->probe_s, c->pos, c->order, c->u, c->v, c->d, sc, c->part_fr, c->grid_fr, c->st, s));
     }
     ++launches;
     EV(5);
@@ -261,7 +270,7 @@ static int enqueue_iteration(ptyger_ctx* c, int p, std::string& err, int64_t& la
             LK(launch_lsx(g, c->u, c->v, c->d, sc, pass, false, c->part_el, c->grid_el, c->st, s));
             ++launches;
         }
-        LK(launch_reduce(fused ? c->part_fr : c->part_el, fused ? c->grid_fr : c->grid_el, wscreen,
+        LK(launch_reduce(fused ? c->part_fr : c->part_el, fused ? c->parts_ls : c->grid_el, wscreen,
                          &c->st->ls_pass[0], s));
         ++launches;
         if (multi) NK(c->nc->AllReduce(&c->st->ls_pass[0], &c->st->ls_pass[0], LSW, ncclFloat64, ncclSum, c->comm, s));
@@ -327,7 +336,7 @@ static void free_ctx(ptyger_ctx* c) {
     if (!c) return;
     for (int p = 0; p < 2; ++p)
         if (c->graph[p]) cudaGraphExecDestroy(c->graph[p]);
-    void* ptrs[] = {c->psi, c->g[0], c->g[1], c->eta, c->u, c->v, c->probe, c->full, c->recv[0], c->recv[1], c->d,
+    void* ptrs[] = {c->psi, c->g[0], c->g[1], c->eta, c->u, c->v, c->probe, c->probe_s, c->full, c->recv[0], c->recv[1], c->d,
                     c->pos, c->order, c->tile_ptr, c->entries, c->part_adj, c->part_fr, c->part_el, c->scratch, c->st,
                     c->d_tr};
     if (c->stream) cudaStreamSynchronize(c->stream);
@@ -514,7 +523,14 @@ static ptyger_status init_impl(ptyger_ctx* c, const float* object, const float* 
     c->grid_el = c->sms * 8;
     c->band_grid = c->sms * 2;
     AL(c->part_adj, double, ((int64_t)c->ntx * c->nty + 2 * c->band_grid) * NDY);
-    AL(c->part_fr, double, (int64_t)c->grid_fr * LSW);
+    c->hf = N == 128 && getenv("PTYGER_HF") && atoi(getenv("PTYGER_HF")) == 1;   // opt-in (see r1_history)
+    c->parts_ls = c->hf ? hf_ls_parts(nl) : c->grid_fr;
+    if (c->parts_ls <= 0) {
+        err = "half-frame kernel setup failed";
+        return PTYGER_E_CUDA;
+    }
+    AL(c->probe_s, float2, NN);
+    AL(c->part_fr, double, (int64_t)std::max(c->grid_fr, c->parts_ls) * LSW);
     AL(c->part_el, double, (int64_t)c->grid_el * LSW);
     AL(c->scratch, double, 64);
     AL(c->st, DevState, 1);
@@ -525,6 +541,9 @@ static ptyger_status init_impl(ptyger_ctx* c, const float* object, const float* 
     CK(cudaStreamSynchronize(0));  // pool allocations and zero fills (legacy stream) are done
     CK(cudaMemcpy(c->psi, object + 2 * c->st_lo * W, sizeof(float2) * obj, cudaMemcpyDefault));
     CK(cudaMemcpy(c->probe, probe, sizeof(float2) * NN, cudaMemcpyDefault));
+    // probe / N (exact: N is a power of two) carries the unitary FFT scale of the HF kernels
+    LK(launch_scale_c(c->probe, c->probe_s, NN, 1.0f / (float)N, 0));
+    CK(cudaStreamSynchronize(0));
     // d: contiguous runs of local frames
     for (int64_t i = 0; i < nl;) {
         int64_t k = i;

@@ -148,8 +148,8 @@ static __device__ __noinline__ float ls_term_slow(float a, float b, float c, flo
 
 // Least-squares estimator terms t = q (1 - 2 sqrt(d) / (|u + g v| + |u|)), q = |u + g v|^2 - |u|^2
 // with correctly rounded sqrt / reciprocal (a few ulp per term, no transcendental approximation).
-template <int KT, int K>
-__device__ __forceinline__ void ls_screen_lse(float2 uu, float2 vv, float dd, const float* sgam, float (&S)[K]) {
+template <int KT, int K, typename G>
+__device__ __forceinline__ void ls_screen_lse(float2 uu, float2 vv, float dd, const G& sgam, float (&S)[K]) {
     const float c = fmaf(uu.x, uu.x, uu.y * uu.y);
     const float sc = __fsqrt_rn(c), sd2 = 2.0f * __fsqrt_rn(dd);
 #pragma unroll
@@ -239,8 +239,8 @@ struct LsWarpQ {
 // LSE = false: Poisson ML terms (screened, MUFU log2).  LSE = true: least-squares estimator terms
 // t = q (1 - 2 sqrt(d) / (|u + g v| + |u|)) with correctly rounded sqrt / reciprocal: a few ulp per
 // term, no transcendental approximation, so A stays 0 and the bound reduces to its rounding part.
-template <int KT, bool LSE, int K>
-__device__ __forceinline__ void ls_screen_nz(float2 uu, float2 vv, float dd, const float* sgam, float eps2,
+template <int KT, bool LSE, int K, typename G>
+__device__ __forceinline__ void ls_screen_nz(float2 uu, float2 vv, float dd, const G& sgam, float eps2,
                                              float (&S)[K], LsMom& m) {
     const float c = fmaf(uu.x, uu.x, uu.y * uu.y);
     if constexpr (LSE) {
@@ -252,11 +252,13 @@ __device__ __forceinline__ void ls_screen_nz(float2 uu, float2 vv, float dd, con
 #pragma unroll
         for (int k = 0; k < KT; ++k) {
             // only the log part: q_k = gamma_k a + gamma_k^2 b of EVERY pixel goes to the (za, zb)
-            // moments in ls_push (one op per trial less than forming cn - c here)
+            // moments in ls_push (one op per trial less than forming cn - c here).  No clamp of cn:
+            // cn * rc = 0 (|u + gamma v| or |u| below eps, or an FTZ underflow) gives log2 = -inf, a
+            // non-finite S and therefore the exact pass, which applies the guarded definition R#4.
             const float gam = sgam[k];
             const float ex = fmaf(gam, vv.x, uu.x), ey = fmaf(gam, vv.y, uu.y);
             const float cn = fmaf(ex, ex, ey * ey);
-            const float L2 = lg2_ftz(fmaxf(cn, eps2) * rc);
+            const float L2 = lg2_ftz(cn * rc);
             S[k] = fmaf(-dl, L2, S[k]);
             amax = fmaxf(amax, fabsf(L2));
         }
@@ -274,15 +276,15 @@ struct LsQState {
     float za = 0.f, zb = 0.f;
 };
 
-template <int KT, bool LSE, int K>
-__device__ __forceinline__ void ls_push(LsWarpQ& q, LsQState& qs, float2 uu, float2 vv, float dd, const float* sgam,
+template <int KT, bool LSE, int K, typename G>
+__device__ __forceinline__ void ls_push(LsWarpQ& q, LsQState& qs, float2 uu, float2 vv, float dd, const G& sgam,
                                         float eps2, float (&S)[K], LsMom& m, int lane) {
     const float a = 2.0f * fmaf(uu.x, vv.x, uu.y * vv.y);
     const float b = fmaf(vv.x, vv.x, vv.y * vv.y);
     const float c = fmaf(uu.x, uu.x, uu.y * uu.y);
     m.D += fmaf(0.12f, c, dd);
     m.sa += fabsf(a);
-    m.sb += b;
+    if (LSE) m.sb += b;   // Poisson ML: sum b is zb (all pixels), folded in at ls_flush
     const bool nz = dd != 0.0f;
     if (!LSE || !nz) {
         qs.za += a;
@@ -307,8 +309,8 @@ __device__ __forceinline__ void ls_push(LsWarpQ& q, LsQState& qs, float2 uu, flo
 }
 
 // Drain the ring and fold the (za, zb) moments into S (call once per accumulation run).
-template <int KT, bool LSE, int K>
-__device__ __forceinline__ void ls_flush(LsWarpQ& q, LsQState& qs, const float* sgam, float eps2, float (&S)[K],
+template <int KT, bool LSE, int K, typename G>
+__device__ __forceinline__ void ls_flush(LsWarpQ& q, LsQState& qs, const G& sgam, float eps2, float (&S)[K],
                                          LsMom& m, int lane) {
     if (qs.pending > 0) {
         __syncwarp();
@@ -322,6 +324,7 @@ __device__ __forceinline__ void ls_flush(LsWarpQ& q, LsQState& qs, const float* 
     }
 #pragma unroll
     for (int k = 0; k < KT; ++k) S[k] += sgam[k] * fmaf(sgam[k], qs.zb, qs.za);
+    if (!LSE) m.sb += qs.zb;
     qs.za = qs.zb = 0.f;
 }
 

@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(512, 1) k_fwd(Geometry g, const float2* __rest
 // ----------------------------------------------------------------------------------------
 template <int N>
 __global__ void __launch_bounds__(512, 1) k_grad(Geometry g, float2* __restrict__ u, float2* __restrict__ v,
-                                                 const float* __restrict__ d, const float2* __restrict__ probe,
+                                                 const float* __restrict__ d, const float2* __restrict__ probe_s,
                                                  const DevState* __restrict__ st, float eps) {
     using C = FFTCfg<N>;
     constexpr int R = C::R, T = C::T, LD = C::LD;
@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(512, 1) k_grad(Geometry g, float2* __restrict_
     const int64_t nfr = g.n_local;
     const int64_t ngroups = (nfr + C::FPB - 1) / C::FPB;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const float scale = 1.0f / (float)N, eps2 = eps * eps;
+    const float eps2 = eps * eps;
     for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
 #pragma unroll 1
         for (int rd = 0; rd < C::ROUNDS; ++rd) {
@@ -178,8 +178,8 @@ __global__ void __launch_bounds__(512, 1) k_grad(Geometry g, float2* __restrict_
 #pragma unroll
                 for (int q = 0; q < R; ++q) {
                     const int k = col_out_row<N>(q, t);
-                    const float2 pk = ldg2(probe + k * N + c);
-                    v[j * N * N + (int64_t)k * N + c] = cscale(cconjmul(pk, X[q]), scale);
+                    const float2 pk = ldg2(probe_s + k * N + c);   // conj(p / N): unitary scale folded in
+                    v[j * N * N + (int64_t)k * N + c] = cconjmul(pk, X[q]);
                 }
             }
         }
@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(512, 1) k_grad(Geometry g, float2* __restrict_
 // ----------------------------------------------------------------------------------------
 template <int N>
 __global__ void __launch_bounds__(512, 1) k_ls(Geometry g, const float2* __restrict__ eta,
-                                               const float2* __restrict__ probe, const int2* __restrict__ pos,
+                                               const float2* __restrict__ probe_s, const int2* __restrict__ pos,
                                                const int* __restrict__ order, const float2* __restrict__ u,
                                                float2* __restrict__ v, const float* __restrict__ d,
                                                SolverCfg cfg, double* __restrict__ part,
@@ -219,7 +219,6 @@ __global__ void __launch_bounds__(512, 1) k_ls(Geometry g, const float2* __restr
     __syncthreads();
     const int64_t nfr = err ? 0 : g.n_local;
     const int64_t ngroups = (nfr + C::FPB - 1) / C::FPB;
-    const float scale = 1.0f / (float)N;
     const float eps2 = (float)(cfg.eps * cfg.eps);
     double tot = 0.0;  // running total of entry lane >> 1 of S
     double mom[4] = {0.0, 0.0, 0.0, 0.0};
@@ -234,7 +233,7 @@ __global__ void __launch_bounds__(512, 1) k_ls(Geometry g, const float2* __restr
                 const int j = order[i];
                 const int2 s = pos[j];
                 const float2* src = eta + (int64_t)(s.x + row) * g.W + s.y + t;
-                const float2* pp = probe + row * N + t;
+                const float2* pp = probe_s + row * N + t;   // p / N: unitary scale folded in
 #pragma unroll
                 for (int n1 = 0; n1 < R; ++n1) x[n1] = cmul(ldg2(pp + T * n1), ldg2(src + T * n1));
             } else {
@@ -282,42 +281,67 @@ __global__ void __launch_bounds__(512, 1) k_ls(Geometry g, const float2* __restr
             const float* __restrict__ db = d + fb;
             float2* __restrict__ vb = v + fb;
             if (cnt > 0) trial_dispatch(cnt, cfg.est, [&]<int KT, bool LSE>() {
-                constexpr int G4 = (R >= 4) ? 4 : R;
+                float gk[KT];   // trial gammas in registers for the whole run
+#pragma unroll
+                for (int k = 0; k < KT; ++k) gk[k] = sgam[k];
                 LsQState qs;
-                float2 un[G4];
-                float dn[G4];
-                auto off = [&](int q) -> int { return ((q / T) * T + R * (q % T)) * N; };
+                if constexpr (T >= 4) {
+                    // groups of 4 consecutive elements q = 4 gi + e share j = q / T, so inside a
+                    // group the global offsets step by R N and the parked rows by one (immediates)
+                    float2 un[4];
+                    float dn[4];
 #pragma unroll
-                for (int jj = 0; jj < G4; ++jj) {
-                    un[jj] = valid ? ub[off(jj)] : make_float2(0.f, 0.f);
-                    dn[jj] = valid ? __ldg(db + off(jj)) : 0.f;
-                }
-#pragma unroll 1
-                for (int q0 = 0; q0 < R; q0 += G4) {
-                    float2 uc[G4];
-                    float dc[G4];
-#pragma unroll
-                    for (int jj = 0; jj < G4; ++jj) {
-                        uc[jj] = un[jj];
-                        dc[jj] = dn[jj];
+                    for (int e = 0; e < 4; ++e) {
+                        un[e] = valid ? ub[e * R * N] : make_float2(0.f, 0.f);
+                        dn[e] = valid ? __ldg(db + e * R * N) : 0.f;
                     }
-                    if (q0 + G4 < R && valid) {  // prefetch the next group's u, d
+#pragma unroll 1
+                    for (int gi = 0; gi < R / 4; ++gi) {
+                        const int q0 = 4 * gi;
+                        const int go = ((q0 / T) * T + R * (q0 % T)) * N;
+                        const float2* sp = scol + (T * ((q0 / T) * T + t) + q0 % T) * LD;
+                        float2 uc[4];
+                        float dc[4];
 #pragma unroll
-                        for (int jj = 0; jj < G4; ++jj) {
-                            un[jj] = ub[off(q0 + G4 + jj)];
-                            dn[jj] = __ldg(db + off(q0 + G4 + jj));
+                        for (int e = 0; e < 4; ++e) {
+                            uc[e] = un[e];
+                            dc[e] = dn[e];
+                        }
+                        if (gi + 1 < R / 4 && valid) {  // prefetch the next group's u, d
+                            const int q1 = q0 + 4;
+                            const int gn = ((q1 / T) * T + R * (q1 % T)) * N;
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                un[e] = ub[gn + e * R * N];
+                                dn[e] = __ldg(db + gn + e * R * N);
+                            }
+                        }
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            float2 vv = sp[e * LD];
+                            if (valid) vb[go + e * R * N] = vv;
+                            else vv = make_float2(0.f, 0.f);
+                            ls_push<KT, LSE>(wq[warp], qs, uc[e], vv, dc[e], gk, eps2, S, m, lane);
                         }
                     }
-#pragma unroll
-                    for (int jj = 0; jj < G4; ++jj) {
-                        const int q = q0 + jj;
-                        float2 vv = cscale(scol[(T * ((q / T) * T + t) + q % T) * LD], scale);
-                        if (valid) vb[off(q)] = vv;
-                        else vv = make_float2(0.f, 0.f);
-                        ls_push<KT, LSE>(wq[warp], qs, uc[jj], vv, dc[jj], sgam, eps2, S, m, lane);
+                } else {
+                    auto off = [&](int q) -> int { return ((q / T) * T + R * (q % T)) * N; };
+#pragma unroll 1
+                    for (int q = 0; q < R; ++q) {
+                        float2 vv = scol[(T * ((q / T) * T + t) + q % T) * LD];
+                        float2 uu = make_float2(0.f, 0.f);
+                        float dd = 0.f;
+                        if (valid) {
+                            uu = ub[off(q)];
+                            dd = __ldg(db + off(q));
+                            vb[off(q)] = vv;
+                        } else {
+                            vv = make_float2(0.f, 0.f);
+                        }
+                        ls_push<KT, LSE>(wq[warp], qs, uu, vv, dd, gk, eps2, S, m, lane);
                     }
                 }
-                ls_flush<KT, LSE>(wq[warp], qs, sgam, eps2, S, m, lane);
+                ls_flush<KT, LSE>(wq[warp], qs, gk, eps2, S, m, lane);
             });
             double dv[KC];
 #pragma unroll
@@ -375,14 +399,14 @@ static int grad_n(const Geometry& g, float2* u, float2* v, const float* d, const
 }
 
 int launch_grad(const Geometry& g, float2* u, float2* v, const float* d, const float2* probe,
-                const int* /*order*/, const DevState* st, float eps, int grid, cudaStream_t s) {
+                const float2* probe_s, const DevState* st, float eps, int grid, cudaStream_t s) {
     switch (g.N) {
-        case 16: return grad_n<16>(g, u, v, d, probe, st, eps, grid, s);
-        case 32: return grad_n<32>(g, u, v, d, probe, st, eps, grid, s);
-        case 64: return grad_n<64>(g, u, v, d, probe, st, eps, grid, s);
+        case 16: return grad_n<16>(g, u, v, d, probe_s, st, eps, grid, s);
+        case 32: return grad_n<32>(g, u, v, d, probe_s, st, eps, grid, s);
+        case 64: return grad_n<64>(g, u, v, d, probe_s, st, eps, grid, s);
         case 128:
-            if (!getenv("PTYGER_GRAD_V1")) return launch_grad128(g, u, v, d, probe, st, eps, grid, s);
-            return grad_n<128>(g, u, v, d, probe, st, eps, grid, s);
+            if (!getenv("PTYGER_GRAD_V1")) return launch_grad128(g, u, v, d, probe_s, st, eps, grid, s);
+            return grad_n<128>(g, u, v, d, probe_s, st, eps, grid, s);
         case 256: return launch_grad256(g, u, v, d, probe, st, eps, grid, s);
     }
     return -2;
@@ -398,14 +422,14 @@ static int ls_n(const Geometry& g, const float2* eta, const float2* probe, const
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
-int launch_ls(const Geometry& g, const float2* eta, const float2* probe, const int2* pos,
+int launch_ls(const Geometry& g, const float2* eta, const float2* probe, const float2* probe_s, const int2* pos,
               const int* order, const float2* u, float2* v, const float* d, const SolverCfg& c,
               double* part, int grid, const DevState* st, cudaStream_t s) {
     switch (g.N) {
-        case 16: return ls_n<16>(g, eta, probe, pos, order, u, v, d, c, part, grid, st, s);
-        case 32: return ls_n<32>(g, eta, probe, pos, order, u, v, d, c, part, grid, st, s);
-        case 64: return ls_n<64>(g, eta, probe, pos, order, u, v, d, c, part, grid, st, s);
-        case 128: return ls_n<128>(g, eta, probe, pos, order, u, v, d, c, part, grid, st, s);
+        case 16: return ls_n<16>(g, eta, probe_s, pos, order, u, v, d, c, part, grid, st, s);
+        case 32: return ls_n<32>(g, eta, probe_s, pos, order, u, v, d, c, part, grid, st, s);
+        case 64: return ls_n<64>(g, eta, probe_s, pos, order, u, v, d, c, part, grid, st, s);
+        case 128: return ls_n<128>(g, eta, probe_s, pos, order, u, v, d, c, part, grid, st, s);
         case 256: return launch_ls256(g, eta, probe, pos, order, u, v, d, c, part, grid, st, s);
     }
     return -2;

@@ -35,7 +35,7 @@ static_assert(SMEM <= 232448, "exceeds the 227 KB per-CTA shared memory");
 }  // namespace g128
 
 __global__ void __launch_bounds__(512, 1) k_grad128(Geometry g, float2* __restrict__ u, float2* __restrict__ v,
-                                                    const float* __restrict__ d, const float2* __restrict__ probe,
+                                                    const float* __restrict__ d, const float2* __restrict__ probe_s,
                                                     const DevState* __restrict__ st, float eps) {
     using namespace g128;
     extern __shared__ __align__(128) unsigned char sm[];
@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(512, 1) k_grad128(Geometry g, float2* __restri
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int grp = tid >> 7, gtid = tid & 127;
     const uint32_t chunk_bytes = ROWS * ((upd ? 2048u : 1024u) + 512u);
-    const float scale = 1.0f / (float)N, eps2 = eps * eps;
+    const float eps2 = eps * eps;
 
     auto issue = [&](int64_t c) {
         const int64_t fi = c / CHUNKS;
@@ -149,20 +149,20 @@ __global__ void __launch_bounds__(512, 1) k_grad128(Geometry g, float2* __restri
 #pragma unroll
             for (int qq = 0; qq < R; ++qq) {
                 const int k = col_out_row<N>(qq, t);
-                const float2 pk = ldg2(probe + k * N + c);
-                v[j * N * N + (int64_t)k * N + c] = cscale(cconjmul(pk, X[qq]), scale);
+                const float2 pk = ldg2(probe_s + k * N + c);   // conj(p / N): unitary scale folded in
+                v[j * N * N + (int64_t)k * N + c] = cconjmul(pk, X[qq]);
             }
         }
         __syncthreads();
     }
 }
 
-int launch_grad128(const Geometry& g, float2* u, float2* v, const float* d, const float2* probe,
+int launch_grad128(const Geometry& g, float2* u, float2* v, const float* d, const float2* probe_s,
                    const DevState* st, float eps, int grid, cudaStream_t s) {
     if (cudaFuncSetAttribute(k_grad128, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g128::SMEM) !=
         cudaSuccess)
         return -1;
-    k_grad128<<<grid, 512, g128::SMEM, s>>>(g, u, v, d, probe, st, eps);
+    k_grad128<<<grid, 512, g128::SMEM, s>>>(g, u, v, d, probe_s, st, eps);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 

@@ -1,0 +1,424 @@
+// Half-frame (HF) frame kernels for N = 128: one 128x128 frame per CLUSTER OF TWO CTAs.
+//
+// Why: a 128^2 complex64 frame (128 KB) fills one SM's shared memory, so the single-CTA kernels
+// run one frame per SM with 16 warps in lock-step barrier phases: HBM idles while the frame is
+// transformed (ncu: k_grad128 IPC 1.4 with 29 % of stall samples waiting for its TMA ring, k_ls
+// IPC 2.3 at 25 % occupancy).  Here the frame is split between the two CTAs of a cluster
+// (PTX barrier.cluster + st.shared::cluster, i.e. distributed shared memory):
+//   * CTA r transforms rows [64 r, 64 r + 64) (row pass, inputs straight from global memory);
+//   * each row's 128 outputs are stored into the CTA that owns their column: columns
+//     [64 r, 64 r + 64) belong to CTA r, so every CTA ends up with a 128 x 64 column block
+//     (64 KB) -- the 2-D transpose IS the DSMEM exchange (32 KB each way per frame);
+//   * CTA r then runs the column pass and the fused epilogue on its 64 columns locally.
+// A CTA needs 110 KB of shared memory and 256 threads x 128 registers, so TWO CTAs (of different
+// clusters) share an SM and interleave their memory and compute phases.
+//
+// Arithmetic is identical to the single-CTA path (fft.cuh: radix-16 in registers x radix-8
+// across 8 threads per dimension, fp64-built twiddles); the unitary 1/N is folded into the
+// probe (probe_s = p / N) so the FFTs run unscaled.
+//
+//   k_ls_hf    LS stage pass 0 (Alg.1 659-668, Eq.7 on the Eq.2 objective): v = F(p eta[window]),
+//              screening partials of the pass-0 trials against (u, d)   (same outputs as k_ls<128>)
+//   k_grad_hf  GRAD stage frame part (Alg.1 648-649): u <- u + gamma v, r = u - d/u^*,
+//              y = conj(p) F^H r into v's slot                           (same outputs as k_grad128)
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "dev.cuh"
+
+namespace pty {
+
+namespace hf {
+constexpr int N = 128, R = 16, T = 8, HALF = 64, NT = 256, NW = NT / 32;
+constexpr int SLD = N + 8;                       // row-scratch stride (complex), as fft.cuh LD
+constexpr int SROWS = NT / T;                    // 32 rows per row-pass round
+constexpr int BLK_ELEMS = N * HALF;              // 128 rows x 64 local columns
+constexpr int SCR_ELEMS = SROWS * SLD;
+constexpr size_t BLK_OFF = 0;
+constexpr size_t SCR_OFF = BLK_OFF + (size_t)BLK_ELEMS * 8;    // 65536
+constexpr size_t TW_OFF = SCR_OFF + (size_t)SCR_ELEMS * 8;     // +34816
+constexpr size_t TWR_OFF = TW_OFF + (size_t)N * 8;             // row-pass twiddles, [k1][t]
+constexpr size_t DYN_BYTES = TWR_OFF + (size_t)N * 8;          // 102400
+}  // namespace hf
+
+// block element (row i, local column cl): XOR swizzle of column bit 3 by row parity, so the
+// row pass's 4-row x 8-column warp stores hit 32 distinct banks per 128 B wavefront pair, while
+// the column pass (32 consecutive columns of one row per warp) stays conflict-free.
+__device__ __forceinline__ int hf_idx(int i, int cl) { return i * hf::HALF + (cl ^ ((i & 1) << 3)); }
+
+__device__ __forceinline__ uint32_t cl_mapa(uint32_t saddr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void cl_st2(uint32_t caddr, float2 v) {
+    asm volatile("st.shared::cluster.v2.f32 [%0], {%1, %2};" ::"r"(caddr), "f"(v.x), "f"(v.y) : "memory");
+}
+__device__ __forceinline__ uint32_t cl_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t cl_id() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t cl_count() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cl_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
+// arrive without release semantics: only orders this CTA's completed shared-memory READS before
+// the peer's later writes (the "my block is free" signal), no memory fence needed
+__device__ __forceinline__ void cl_arrive_relaxed() {
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cl_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+
+// Row pass of one frame row held by the 8 threads t of one row (consecutive lanes): x[n1] is the
+// input at column 8 n1 + t.  DFT over the row (unnormalised), then output column k goes to the
+// block of CTA k / 64 at (row, k % 64) through the cluster address window (bases caddr[2]).
+// twr[k1 * 8 + t] = W_N^{t k1}: the 8 sub-threads of a row read 8 consecutive entries (the
+// column-pass layout tw[t k1] made the row pass's twiddle loads 2..8-way bank conflicted).
+template <bool INV>
+__device__ __forceinline__ void hf_row(float2 (&x)[16], float2* srow, int t, const float2* twr, int row,
+                                       uint32_t cbase0, uint32_t cbase1) {
+    using namespace hf;
+    DFT<R, INV>::run(x);
+#pragma unroll
+    for (int k1 = 1; k1 < R; ++k1) x[k1] = twmul<INV>(x[k1], twr[k1 * T + t]);
+#pragma unroll
+    for (int k1 = 0; k1 < R; ++k1) srow[T * k1 + (t ^ (k1 & (T - 1)))] = x[k1];
+    __syncwarp();
+    float2 y[R];
+#pragma unroll
+    for (int j = 0; j < R / T; ++j) {
+        const int k1 = j * T + t;
+#pragma unroll
+        for (int n2 = 0; n2 < T; ++n2) y[j * T + n2] = srow[T * k1 + (n2 ^ t)];
+    }
+    __syncwarp();
+    const int sw = (row & 1) << 3;
+#pragma unroll
+    for (int j = 0; j < R / T; ++j) {
+        float2 b[T];
+#pragma unroll
+        for (int n2 = 0; n2 < T; ++n2) b[n2] = y[j * T + n2];
+        DFT<T, INV>::run(b);
+        const int k1 = j * T + t;
+#pragma unroll
+        for (int k2 = 0; k2 < T; ++k2) {
+            // column k1 + 16 k2: CTA k2 / 4, local column k1 + 16 (k2 % 4)
+            const uint32_t off = (uint32_t)(row * HALF + ((k1 + R * (k2 & 3)) ^ sw)) * 8u;
+            cl_st2((k2 < 4 ? cbase0 : cbase1) + off, b[k2]);
+        }
+    }
+}
+
+__device__ __forceinline__ void hf_row_twiddles(float2* twr) {
+    for (int i = threadIdx.x; i < hf::N; i += blockDim.x) {
+        const int k1 = i / hf::T, t = i % hf::T;
+        double sn, cs;
+        sincospi(2.0 * (double)(t * k1) / (double)hf::N, &sn, &cs);
+        twr[i] = make_float2((float)cs, (float)(-sn));
+    }
+}
+
+// Column pass phase 1 on the local block, column cl, sub-thread t (rows 8 n1 + t).
+template <bool INV>
+__device__ __forceinline__ void hf_col1(float2* blk, int cl, int t, const float2* tw) {
+    using namespace hf;
+    float2 x[R];
+#pragma unroll
+    for (int n1 = 0; n1 < R; ++n1) x[n1] = blk[hf_idx(T * n1 + t, cl)];
+    DFT<R, INV>::run(x);
+#pragma unroll
+    for (int k1 = 1; k1 < R; ++k1) x[k1] = twmul<INV>(x[k1], tw[t * k1]);
+#pragma unroll
+    for (int k1 = 0; k1 < R; ++k1) blk[hf_idx(T * k1 + t, cl)] = x[k1];
+}
+
+// Column pass phase 2: X[j*8 + k2] = output row (j*8 + t) + 16 k2 of column cl.
+template <bool INV>
+__device__ __forceinline__ void hf_col2(const float2* blk, int cl, int t, float2 (&X)[16]) {
+    using namespace hf;
+#pragma unroll
+    for (int j = 0; j < R / T; ++j) {
+        const int k1 = j * T + t;
+        float2 b[T];
+#pragma unroll
+        for (int n2 = 0; n2 < T; ++n2) b[n2] = blk[hf_idx(T * k1 + n2, cl)];
+        DFT<T, INV>::run(b);
+#pragma unroll
+        for (int k2 = 0; k2 < T; ++k2) X[j * T + k2] = b[k2];
+    }
+}
+
+// ----------------------------------------------------------------------------------------
+// k_ls_hf: LS pass 0 (see k_ls<N> in kernels_frame.cu for the screening contract).
+// ----------------------------------------------------------------------------------------
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2)
+    k_ls_hf(Geometry g, const float2* __restrict__ eta, const float2* __restrict__ probe_s,
+            const int2* __restrict__ pos, const int* __restrict__ order, const float2* __restrict__ u,
+            float2* __restrict__ v, const float* __restrict__ d, SolverCfg cfg, double* __restrict__ part,
+            const DevState* __restrict__ st) {
+    using namespace hf;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    float2* blk = reinterpret_cast<float2*>(smraw + BLK_OFF);
+    float2* scr = reinterpret_cast<float2*>(smraw + SCR_OFF);
+    float2* tw = reinterpret_cast<float2*>(smraw + TW_OFF);
+    float2* twr = reinterpret_cast<float2*>(smraw + TWR_OFF);
+    __shared__ double sred[NW][KC];
+    __shared__ double smom[NW][4];
+    __shared__ float sgam[KC];
+    __shared__ LsWarpQ wq[NW];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t rank = cl_rank();
+    const int64_t cid = cl_id(), ncl = cl_count();
+    const bool err = st->numeric_error != 0;
+    int base, cnt;
+    ls_pass_range(0, st->keff, cfg, base, cnt);
+    build_twiddles<N>(tw);
+    hf_row_twiddles(twr);
+    if (tid < KC) sgam[tid] = (float)trial_gamma(cfg.gamma0, cfg.tau, base + tid);
+    const uint32_t sblk = static_cast<uint32_t>(__cvta_generic_to_shared(blk));
+    const uint32_t cb0 = cl_mapa(sblk, 0), cb1 = cl_mapa(sblk, 1);
+    __syncthreads();
+    cl_arrive_relaxed();  // "my block is free" for the first frame
+    const int64_t nfr = err ? 0 : g.n_local;
+    const float eps2 = (float)(cfg.eps * cfg.eps);
+    double tot = 0.0;
+    double mom[4] = {0.0, 0.0, 0.0, 0.0};
+    const int rt = tid & 7, rrow = tid >> 3;       // row pass: sub-thread, row within the round
+    const int ct = warp, clane = lane;             // column pass: sub-thread t = warp, column lane
+    for (int64_t i = cid; i < nfr; i += ncl) {
+        const int j = order[i];
+        const int2 s = pos[j];
+        // ---- row pass: rows 64 rank + 32 rd + rrow of p_s * eta[window]
+#pragma unroll 1
+        for (int rd = 0; rd < 2; ++rd) {
+            const int row = (int)rank * HALF + rd * SROWS + rrow;
+            const float2* src = eta + (int64_t)(s.x + row) * g.W + s.y + rt;
+            const float2* pp = probe_s + row * N + rt;
+            float2 x[R];
+#pragma unroll
+            for (int n1 = 0; n1 < R; ++n1) x[n1] = cmul(ldg2(pp + T * n1), ldg2(src + T * n1));
+            if (rd == 0) cl_wait();  // peer finished reading its block (previous frame)
+            hf_row<false>(x, scr + rrow * SLD, rt, twr, row, cb0, cb1);
+        }
+        cl_arrive();
+        cl_wait();  // both halves of every row have landed
+        // ---- column pass on the local 64 columns
+#pragma unroll 1
+        for (int rd = 0; rd < 2; ++rd) hf_col1<false>(blk, rd * 32 + clane, ct, tw);
+        __syncthreads();
+#pragma unroll 1
+        for (int rd = 0; rd < 2; ++rd) {
+            const int cl = rd * 32 + clane;
+            {
+                float2 X[R];
+                hf_col2<false>(blk, cl, ct, X);
+                // park the outputs in the thread's own phase-2 rows 8 k1 + k2 (thread-private)
+#pragma unroll
+                for (int q = 0; q < R; ++q) blk[hf_idx(T * ((q / T) * T + ct) + q % T, cl)] = X[q];
+            }
+            float S[KC];
+            LsMom m;
+#pragma unroll
+            for (int k = 0; k < KC; ++k) S[k] = 0.f;
+            // frame base at (row ct, column 64 rank + cl); element (jj, k2) sits at row
+            // jj*8 + ct + 16 k2, i.e. offset jj*1024 + k2*2048
+            const int64_t fb = (int64_t)j * (N * N) + (int64_t)ct * N + (int64_t)rank * HALF + cl;
+            const float2* __restrict__ ub = u + fb;
+            const float* __restrict__ db = d + fb;
+            float2* __restrict__ vb = v + fb;
+            const float2* pk = blk + (T * ct) * HALF + cl;   // parked row 8 (jj*8 + ct) + k2
+            if (cnt > 0) trial_dispatch(cnt, cfg.est, [&]<int KT, bool LSE>() {
+                LsQState qs;
+                float2 un[4];
+                float dn[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    un[e] = ub[e * 2048];
+                    dn[e] = __ldg(db + e * 2048);
+                }
+                // groups g = 0..3: (jj = g >> 1, k2 = 4 (g & 1) + e)
+#pragma unroll 1
+                for (int gi = 0; gi < 4; ++gi) {
+                    const int go = ((gi >> 1) << 10) + ((gi & 1) << 13);
+                    const int gp = ((gi >> 1) * 64 + (gi & 1) * 4) * HALF;
+                    float2 uc[4];
+                    float dc[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        uc[e] = un[e];
+                        dc[e] = dn[e];
+                    }
+                    if (gi < 3) {
+                        const int gn = (((gi + 1) >> 1) << 10) + (((gi + 1) & 1) << 13);
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            un[e] = ub[gn + e * 2048];
+                            dn[e] = __ldg(db + gn + e * 2048);
+                        }
+                    }
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        // parked row 8 (jj*8 + ct) + 4 (gi & 1) + e has parity e & 1
+                        const float2 vv = pk[gp + e * HALF + (cl ^ ((e & 1) << 3)) - cl];
+                        vb[go + e * 2048] = vv;
+                        ls_push<KT, LSE>(wq[warp], qs, uc[e], vv, dc[e], sgam, eps2, S, m, lane);
+                    }
+                }
+                ls_flush<KT, LSE>(wq[warp], qs, sgam, eps2, S, m, lane);
+            });
+            double dv[KC];
+#pragma unroll
+            for (int k = 0; k < KC; ++k) dv[k] = (double)S[k];
+            tot += warp_reduce_scatter<KC>(dv, lane);
+            mom[0] += (double)m.A;
+            mom[1] += (double)m.D;
+            mom[2] += (double)m.sa;
+            mom[3] += (double)m.sb;
+        }
+        __syncthreads();       // parked outputs consumed before the next frame's stores land
+        cl_arrive_relaxed();   // my block is free for the peer's next row pass
+    }
+    cl_wait();  // pairs with the last arrive: the peer no longer touches this CTA's memory
+    ls_block_out<KC, NW>(tot, mom, sred, smom, part);
+}
+
+// ----------------------------------------------------------------------------------------
+// k_grad_hf: GRAD stage frame part (see k_grad<N> in kernels_frame.cu).
+// ----------------------------------------------------------------------------------------
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2)
+    k_grad_hf(Geometry g, float2* __restrict__ u, float2* __restrict__ v, const float* __restrict__ d,
+              const float2* __restrict__ probe_s, const DevState* __restrict__ st, float eps) {
+    using namespace hf;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    float2* blk = reinterpret_cast<float2*>(smraw + BLK_OFF);
+    float2* scr = reinterpret_cast<float2*>(smraw + SCR_OFF);
+    float2* tw = reinterpret_cast<float2*>(smraw + TW_OFF);
+    float2* twr = reinterpret_cast<float2*>(smraw + TWR_OFF);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t rank = cl_rank();
+    const int64_t cid = cl_id(), ncl = cl_count();
+    const bool err = st->numeric_error != 0;
+    const float gam = (float)st->gamma;
+    const bool upd = gam != 0.0f;
+    build_twiddles<N>(tw);
+    hf_row_twiddles(twr);
+    const uint32_t sblk = static_cast<uint32_t>(__cvta_generic_to_shared(blk));
+    const uint32_t cb0 = cl_mapa(sblk, 0), cb1 = cl_mapa(sblk, 1);
+    __syncthreads();
+    cl_arrive_relaxed();
+    const int64_t nfr = err ? 0 : g.n_local;
+    const float eps2 = eps * eps;
+    const int rt = tid & 7, rrow = tid >> 3;
+    const int ct = warp, clane = lane;
+    for (int64_t j = cid; j < nfr; j += ncl) {
+#pragma unroll 1
+        for (int rd = 0; rd < 2; ++rd) {
+            const int row = (int)rank * HALF + rd * SROWS + rrow;
+            const int64_t b0 = j * (N * N) + (int64_t)row * N + rt;
+            float2 uu[R];
+            float dd[R];
+#pragma unroll
+            for (int n1 = 0; n1 < R; ++n1) {
+                uu[n1] = u[b0 + T * n1];
+                dd[n1] = __ldg(d + b0 + T * n1);
+            }
+            if (upd) {
+                float2 vv[R];
+#pragma unroll
+                for (int n1 = 0; n1 < R; ++n1) vv[n1] = v[b0 + T * n1];
+#pragma unroll
+                for (int n1 = 0; n1 < R; ++n1) {
+                    uu[n1] = make_float2(fmaf(gam, vv[n1].x, uu[n1].x), fmaf(gam, vv[n1].y, uu[n1].y));
+                    u[b0 + T * n1] = uu[n1];
+                }
+            }
+            float2 x[R];
+#pragma unroll
+            for (int n1 = 0; n1 < R; ++n1) x[n1] = residual(uu[n1], dd[n1], eps2, g.est);
+            if (rd == 0) cl_wait();
+            hf_row<true>(x, scr + rrow * SLD, rt, twr, row, cb0, cb1);
+        }
+        cl_arrive();
+        cl_wait();
+#pragma unroll 1
+        for (int rd = 0; rd < 2; ++rd) hf_col1<true>(blk, rd * 32 + clane, ct, tw);
+        __syncthreads();
+#pragma unroll 1
+        for (int rd = 0; rd < 2; ++rd) {
+            const int cl = rd * 32 + clane;
+            const int c = (int)rank * HALF + cl;
+            float2 X[R];
+            hf_col2<true>(blk, cl, ct, X);
+#pragma unroll
+            for (int q = 0; q < R; ++q) {
+                const int k = (q / T) * T + ct + R * (q % T);
+                const float2 pk = ldg2(probe_s + k * N + c);
+                v[j * (N * N) + (int64_t)k * N + c] = cconjmul(pk, X[q]);
+            }
+        }
+        __syncthreads();
+        cl_arrive_relaxed();
+    }
+    cl_wait();
+}
+
+// ----------------------------------------------------------------------------------------
+// launchers: grid = 2 x (resident clusters, capped by the frame count)
+// ----------------------------------------------------------------------------------------
+template <typename K>
+static int hf_grid(K* kern, int64_t nfr) {
+    static int cached[2] = {0, 0};
+    const int slot = (void*)kern == (void*)k_ls_hf ? 0 : 1;
+    if (cached[slot] == 0) {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hf::DYN_BYTES) != cudaSuccess)
+            return -1;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(2 * 148 * 2, 1, 1);
+        cfg.blockDim = dim3(hf::NT, 1, 1);
+        cfg.dynamicSmemBytes = hf::DYN_BYTES;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int ncl = 0;
+        if (cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg) != cudaSuccess || ncl <= 0) {
+            cudaGetLastError();
+            ncl = 148;
+        }
+        cached[slot] = ncl;
+    }
+    const int64_t ncl = nfr < cached[slot] ? (nfr > 0 ? nfr : 1) : cached[slot];
+    return (int)(2 * ncl);
+}
+
+int hf_ls_parts(int64_t nfr) { return hf_grid(k_ls_hf, nfr); }
+
+int launch_ls_hf(const Geometry& g, const float2* eta, const float2* probe_s, const int2* pos, const int* order,
+                 const float2* u, float2* v, const float* d, const SolverCfg& c, double* part, const DevState* st,
+                 cudaStream_t s) {
+    const int grid = hf_grid(k_ls_hf, g.n_local);
+    if (grid < 0) return -1;
+    k_ls_hf<<<grid, hf::NT, hf::DYN_BYTES, s>>>(g, eta, probe_s, pos, order, u, v, d, c, part, st);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+int launch_grad_hf(const Geometry& g, float2* u, float2* v, const float* d, const float2* probe_s,
+                   const DevState* st, float eps, cudaStream_t s) {
+    const int grid = hf_grid(k_grad_hf, g.n_local);
+    if (grid < 0) return -1;
+    k_grad_hf<<<grid, hf::NT, hf::DYN_BYTES, s>>>(g, u, v, d, probe_s, st, eps);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+}  // namespace pty

@@ -1,5 +1,6 @@
 // Object-domain, reduction and decision kernels of the CG iteration (see kernels_frame.cu header).
 #include <cuda_runtime.h>
+#include <algorithm>
 #include <math.h>
 #include <stdint.h>
 
@@ -503,6 +504,16 @@ int launch_lsx(const Geometry& g, const float2* u, const float2* v, const float*
         k_lsx<true><<<grid, 256, 0, s>>>(count, u, v, d, c, pass, part, st);
     else
         k_lsx<false><<<grid, 256, 0, s>>>(count, u, v, d, c, pass, part, st);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+__global__ void k_scale_c(const float2* __restrict__ in, float2* __restrict__ out, int64_t n, float s) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = cscale(in[i], s);
+}
+
+int launch_scale_c(const float2* in, float2* out, int64_t n, float s, cudaStream_t st) {
+    k_scale_c<<<(int)std::min<int64_t>((n + 255) / 256, 1024), 256, 0, st>>>(in, out, n, s);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
