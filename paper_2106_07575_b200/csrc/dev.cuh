@@ -328,18 +328,25 @@ __device__ __forceinline__ void ls_flush(LsWarpQ& q, LsQState& qs, const G& sgam
     qs.za = qs.zb = 0.f;
 }
 
-// Run body.template operator()<KT>() with KT = cnt rounded up to an even count >= 4 (<= 16): the
-// trial count of a pass is uniform for the whole launch, so one branch at the top selects a
+// Run body.template operator()<KT>() with KT = cnt (4..10) or cnt rounded up to an even count (<= 16):
+// the trial count of a pass is uniform for the whole launch, so one branch at the top selects a
 // fully unrolled variant and only its code is executed (instruction-cache footprint of one).
+// Exact variants cover the adaptive pass-0 counts k*_prev + 3 around the typical k* = 4..7.
 template <bool LSE, typename F>
 __device__ __forceinline__ void trial_dispatch_k(int cnt, F& body) {
     if (cnt <= 4)
         body.template operator()<4, LSE>();
-    else if (cnt <= 6)
+    else if (cnt == 5)
+        body.template operator()<5, LSE>();
+    else if (cnt == 6)
         body.template operator()<6, LSE>();
-    else if (cnt <= 8)
+    else if (cnt == 7)
+        body.template operator()<7, LSE>();
+    else if (cnt == 8)
         body.template operator()<8, LSE>();
-    else if (cnt <= 10)
+    else if (cnt == 9)
+        body.template operator()<9, LSE>();
+    else if (cnt == 10)
         body.template operator()<10, LSE>();
     else if (cnt <= 12)
         body.template operator()<12, LSE>();

@@ -223,24 +223,43 @@ __global__ void __launch_bounds__(512, 1) k_ls(Geometry g, const float2* __restr
     double tot = 0.0;  // running total of entry lane >> 1 of S
     double mom[4] = {0.0, 0.0, 0.0, 0.0};
     for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
-#pragma unroll 1
-        for (int rd = 0; rd < C::ROUNDS; ++rd) {
+        // row pass input of round rd: x[n1] = (p / N)[row, T n1 + t] * eta[s + (row, T n1 + t)]
+        // (p / N: the unitary scale folded into the probe)
+        auto load_row = [&](int rd, float2 (&x)[R]) {
             const int line = rd * C::LPR + tid / T, t = tid % T;
             const int f = line / N, row = line % N;
             const int64_t i = grp * C::FPB + f;
-            float2 x[R];
             if (i < nfr) {
                 const int j = order[i];
                 const int2 s = pos[j];
                 const float2* src = eta + (int64_t)(s.x + row) * g.W + s.y + t;
-                const float2* pp = probe_s + row * N + t;   // p / N: unitary scale folded in
+                const float2* pp = probe_s + row * N + t;
 #pragma unroll
                 for (int n1 = 0; n1 < R; ++n1) x[n1] = cmul(ldg2(pp + T * n1), ldg2(src + T * n1));
             } else {
 #pragma unroll
                 for (int n1 = 0; n1 < R; ++n1) x[n1] = make_float2(0.f, 0.f);
             }
-            row_fft<N, false>(x, sf + f * C::FRAME_ELEMS + row * LD, t, tw);
+        };
+        auto fft_row = [&](int rd, float2 (&x)[R]) {
+            const int line = rd * C::LPR + tid / T, t = tid % T;
+            row_fft<N, false>(x, sf + (line / N) * C::FRAME_ELEMS + (line % N) * LD, t, tw);
+        };
+        if constexpr (C::ROUNDS == 2) {
+            // both rounds' gathers in flight before the first transform (hides the L2 latency of
+            // the eta window once per frame instead of twice)
+            float2 xa[R], xb[R];
+            load_row(0, xa);
+            load_row(1, xb);
+            fft_row(0, xa);
+            fft_row(1, xb);
+        } else {
+#pragma unroll 1
+            for (int rd = 0; rd < C::ROUNDS; ++rd) {
+                float2 x[R];
+                load_row(rd, x);
+                fft_row(rd, x);
+            }
         }
         __syncthreads();
 #pragma unroll 1
