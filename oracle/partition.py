@@ -57,19 +57,28 @@ def max_feasible_P(scan, N: int, P_limit: int = 64) -> int:
     return best
 
 
-def partition(scan, H: int, N: int, P: int):
+def split_subpixel(scan):
+    """Fractional positions (R#22): integer corners floor(x) and whether any fraction is nonzero."""
+    s = np.asarray(scan, dtype=np.float64)
+    base = np.floor(s).astype(np.int64)
+    return base, bool(np.any(s != base))
+
+
+def partition(scan, H: int, N: int, P: int, foot: int | None = None):
     """Return (frame_rank[n], rows[P][6]) with rows = own_lo, own_hi, ext_lo, ext_hi,
     store_lo, store_hi (half-open row ranges).
 
     frame rank: the i whose [b_i, b_{i+1}) holds the centre row (b_0 = -inf, b_P = +inf;
     ties at b_i go to stripe i).
-    ext_i = [min owned r_j, max owned r_j + N).
+    ext_i = [min owned r_j, min(max owned r_j + foot, H)), foot = N (N + 1 rows for the
+    bilinear windows of fractional positions, R#22: ``partition_subpixel``).
     own: o_0 = 0, o_P = H, o_i = clamp(b_i, ext_i.lo, ext_{i-1}.hi) when ext_{i-1}
     and ext_i overlap or touch, else o_i = ext_i.lo.
     store_i = [min(ext_i.lo, o_i), max(ext_i.hi, o_{i+1})).
     """
     scan = np.asarray(scan)
     n = len(scan)
+    foot = N if foot is None else foot
     if not feasible(scan, N, P):
         raise ValueError(f"P={P} infeasible; max feasible P = {max_feasible_P(scan, N)}")
     b = stripe_bounds(scan, N, P)
@@ -83,7 +92,7 @@ def partition(scan, H: int, N: int, P: int):
     ext = []
     for i in range(P):
         rs = [int(scan[j, 0]) for j in range(n) if rank[j] == i]
-        ext.append((min(rs), max(rs) + N))
+        ext.append((min(rs), min(max(rs) + foot, H)))
     o = [0] * (P + 1)
     o[P] = H
     for i in range(1, P):
@@ -98,6 +107,12 @@ def partition(scan, H: int, N: int, P: int):
         st_hi = max(ext[i][1], o[i + 1])
         rows.append((o[i], o[i + 1], ext[i][0], ext[i][1], st_lo, st_hi))
     return rank, rows
+
+
+def partition_subpixel(scan_f, H: int, N: int, P: int):
+    """Partition of fractional positions: rows by floor(x), footprint N + 1 if any fraction != 0."""
+    base, sub = split_subpixel(scan_f)
+    return partition(base, H, N, P, N + 1 if sub else N)
 
 
 def band(rows, i: int):
@@ -121,7 +136,9 @@ def local_gradient(psi, probe, scan, d, rank, rows, i, eps=EPS):
     r = residual(far, np.asarray(d)[idx], eps)
     pc = np.conj(probe)
     for k, s in enumerate(sc):
-        scatter_add(acc, pc * uifft2(r[k]), (int(s[0]) - st_lo, int(s[1])))
+        # storage-local position (a floating-point position keeps its fraction: bilinear, R#22)
+        loc = np.array([s[0] - st_lo, s[1]], dtype=sc.dtype)
+        scatter_add(acc, pc * uifft2(r[k]), loc)
     return acc
 
 
@@ -129,7 +146,10 @@ def exchanged_gradients(psi, probe, scan, d, P, eps=EPS):
     """All ranks' gradients after the band exchange (pure Python, no transport)."""
     H = psi.shape[0]
     N = probe.shape[0]
-    rank, rows = partition(scan, H, N, P)
+    if np.issubdtype(np.asarray(scan).dtype, np.floating):
+        rank, rows = partition_subpixel(scan, H, N, P)
+    else:
+        rank, rows = partition(scan, H, N, P)
     parts = [local_gradient(psi, probe, scan, d, rank, rows, i, eps) for i in range(P)]
     out = [p.copy() for p in parts]
     for i in range(P - 1):

@@ -40,12 +40,20 @@ DIR_FR = 2           # Fletcher-Reeves ||g||^2/||g_prev||^2 (north_star)
 # Operators Q, F, G = F Q and G^H = Q^H F^H           (Eq.1)
 # --------------------------------------------------------------------------
 
+def is_subpixel(scan) -> bool:
+    """A floating-point scan array selects the fractional-position operators (R#22)."""
+    return np.issubdtype(np.asarray(scan).dtype, np.floating)
+
+
 def extract(psi: np.ndarray, pos, N: int) -> np.ndarray:
     """Window of psi at integer top-left corner pos=(row, col), N x N (R#3).
 
     Q's windowing half ("element-wise multiplication of probe p and
-    exit wave psi at all scan positions").
+    exit wave psi at all scan positions").  A floating-point pos selects the
+    bilinear window of R#22 (``extract_bilinear``).
     """
+    if np.issubdtype(np.asarray(pos).dtype, np.floating):
+        return extract_bilinear(psi, pos, N)
     r, c = int(pos[0]), int(pos[1])
     H, W = psi.shape
     if not (0 <= r <= H - N and 0 <= c <= W - N):
@@ -55,12 +63,55 @@ def extract(psi: np.ndarray, pos, N: int) -> np.ndarray:
 
 def scatter_add(acc: np.ndarray, patch: np.ndarray, pos) -> None:
     """acc[r+i, c+k] += patch[i, k]: adjoint of ``extract`` (Q^H windowing)."""
+    if np.issubdtype(np.asarray(pos).dtype, np.floating):
+        scatter_add_bilinear(acc, patch, pos)
+        return
     r, c = int(pos[0]), int(pos[1])
     N = patch.shape[0]
     H, W = acc.shape
     if not (0 <= r <= H - N and 0 <= c <= W - N):
         raise IndexError(f"window at {pos} out of bounds for {acc.shape} with N={N}")
     acc[r:r + N, c:c + N] += patch
+
+
+# Fractional scan positions (SURVEY 8(f) f4).  Alg.1 takes the positions as float32 h_s
+# (P:637) but the paper never says how a non-integer position samples the object; reading
+# R#22: the window is the BILINEAR interpolation of psi at (y + i, x + k), i.e. with
+# r0 = floor(y), fy = y - r0 (same for x):
+#   window[i, k] = sum_{a, b in {0, 1}} wy_a wx_b psi[r0 + i + a, c0 + k + b],
+#   wy_0 = 1 - fy, wy_1 = fy, wx_0 = 1 - fx, wx_1 = fx.
+# Taps with weight 0 are not read, so an integral position reproduces ``extract`` exactly.
+
+def _bilinear_taps(pos):
+    y, x = float(pos[0]), float(pos[1])
+    r0, c0 = math.floor(y), math.floor(x)
+    fy, fx = y - r0, x - c0
+    taps = []
+    for a, wy in ((0, 1.0 - fy), (1, fy)):
+        for b, wx in ((0, 1.0 - fx), (1, fx)):
+            if wy * wx != 0.0:
+                taps.append((r0 + a, c0 + b, wy * wx))
+    return taps
+
+
+def extract_bilinear(psi: np.ndarray, pos, N: int) -> np.ndarray:
+    H, W = psi.shape
+    out = np.zeros((N, N), dtype=np.result_type(psi.dtype, np.float64))
+    for r, c, w in _bilinear_taps(pos):
+        if not (0 <= r <= H - N and 0 <= c <= W - N):
+            raise IndexError(f"bilinear window at {tuple(pos)} out of bounds for {psi.shape} with N={N}")
+        out += w * psi[r:r + N, c:c + N]
+    return out
+
+
+def scatter_add_bilinear(acc: np.ndarray, patch: np.ndarray, pos) -> None:
+    """Adjoint of ``extract_bilinear``: the same real weights, scattered (Q^H)."""
+    N = patch.shape[0]
+    H, W = acc.shape
+    for r, c, w in _bilinear_taps(pos):
+        if not (0 <= r <= H - N and 0 <= c <= W - N):
+            raise IndexError(f"bilinear window at {tuple(pos)} out of bounds for {acc.shape} with N={N}")
+        acc[r:r + N, c:c + N] += w * patch
 
 
 def ufft2(x: np.ndarray) -> np.ndarray:
@@ -411,15 +462,28 @@ def gradient_f32(psi, probe, scan, d, eps: float = EPS, est: int = EST_ML):
     probe = np.asarray(probe, np.complex64)
     d = np.asarray(d, np.float32)
     N = probe.shape[0]
+    sub = is_subpixel(scan)
     acc = np.zeros(psi.shape, np.complex64)
     for j, s in enumerate(scan):
-        r, c = int(s[0]), int(s[1])
-        u = np.fft.fft2(probe * psi[r:r + N, c:c + N], norm="ortho").astype(np.complex64)
+        if sub:   # R#22 bilinear window, weights and taps in float32
+            taps = [(r, c, np.float32(w)) for r, c, w in _bilinear_taps(np.asarray(s, np.float32))]
+            win = np.zeros((N, N), np.complex64)
+            for r, c, w in taps:
+                win = (win + w * psi[r:r + N, c:c + N]).astype(np.complex64)
+        else:
+            r, c = int(s[0]), int(s[1])
+            win = psi[r:r + N, c:c + N]
+        u = np.fft.fft2(probe * win, norm="ortho").astype(np.complex64)
         a2 = (u.real * u.real + u.imag * u.imag).astype(np.float32)
         ok = a2 >= np.float32(eps) * np.float32(eps)
         q = np.where(ok, d[j] / np.where(ok, a2, np.float32(1)), np.float32(0)).astype(np.float32)
         if est == EST_LS:
             q = np.sqrt(q).astype(np.float32)
         res = (u - q * u).astype(np.complex64)
-        acc[r:r + N, c:c + N] += np.conj(probe) * np.fft.ifft2(res, norm="ortho").astype(np.complex64)
+        y = (np.conj(probe) * np.fft.ifft2(res, norm="ortho")).astype(np.complex64)
+        if sub:
+            for r, c, w in taps:
+                acc[r:r + N, c:c + N] += w * y
+        else:
+            acc[r:r + N, c:c + N] += y
     return acc.astype(np.complex128)

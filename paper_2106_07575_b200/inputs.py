@@ -110,3 +110,17 @@ def view_inputs(w: Workload, v: int):
     """View v of a 3-D batch workload: the phantom rotated by v pi / views, scan seed seed + v."""
     img = siemens_star(w.H, w.W, rotation=v * np.pi / max(w.views, 1))
     return make_object(img), make_probe(w.N), make_scan(w.H, w.W, w.N, w.k, w.step, w.jitter, w.seed + v)
+
+
+def make_scan_subpixel(H: int, W: int, N: int, k: int, step: int, jitter: float, seed: int) -> np.ndarray:
+    """Fractional positions: k x k raster + uniform real jitter in
+    [-jitter, jitter], clamped so the bilinear window (N + 1 footprint) stays inside; float32."""
+    if (k - 1) * step > min(H, W) - N - 1:
+        raise ValueError("raster does not fit")
+    rng = np.random.default_rng(seed)
+    rr, cc = np.meshgrid(np.arange(k) * step, np.arange(k) * step, indexing="ij")
+    pos = np.stack([rr.ravel(), cc.ravel()], axis=1).astype(np.float64)
+    pos = pos + rng.uniform(-jitter, jitter, size=pos.shape)
+    pos[:, 0] = np.clip(pos[:, 0], 0.0, H - N - 1)
+    pos[:, 1] = np.clip(pos[:, 1], 0.0, W - N - 1)
+    return pos.astype(np.float32)
