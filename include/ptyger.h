@@ -121,6 +121,27 @@ ptyger_status ptyger_init(ptyger_ctx** out, const ptyger_config* cfg,
                           const float* intensities);
 
 /*
+ * ptyger_init with FRACTIONAL scan positions (Alg.1 input 'float32 h_s').
+ * The paper does not say how a non-integer position samples the object; reading R#22: frame j's
+ * window is the BILINEAR interpolation of psi at (y_j + i, x_j + k), i.e. with r0 = floor(y_j),
+ * fy = y_j - r0 (same for x):
+ *     Q_j psi[i, k] = p[i, k] sum_{a, b in {0,1}} wy_a wx_b psi[r0 + i + a, c0 + k + b],
+ *     wy_0 = 1 - fy, wy_1 = fy, wx_0 = 1 - fx, wx_1 = fx,
+ * and the adjoint Q_j^H scatters with the same real weights.  Integral positions reproduce
+ * ptyger_init exactly (the all-integer case runs the integer kernels).
+ *   scan  n*(row, col) float32 top-left positions, host; 0 <= row, floor(row) + N + (fy > 0) <= H,
+ *         likewise for col / W.
+ * Every other argument, the ownership rules and the errors are those of ptyger_init; with
+ * world > 1 the partition uses the integer corners floor(x) and an N + 1 row footprint
+ * (ptyger_partition_subpixel).  E_DATA: a negative, non-finite or out-of-bounds position.
+ */
+ptyger_status ptyger_init_subpixel(ptyger_ctx** out, const ptyger_config* cfg,
+                                   const float* object, int64_t H, int64_t W,
+                                   const float* probe, int32_t N,
+                                   const float* scan, int64_t n,
+                                   const float* intensities);
+
+/*
  * Run n_iter CG iterations (Alg.1) as CUDA-graph launches with no host
  * synchronisation inside; traces (nullable) receives n_iter entries.  Collective when
  * world > 1.  Errors: E_NUMERIC (non-finite F/alpha/gamma: message names iteration
@@ -168,6 +189,12 @@ ptyger_status ptyger_get_ls_partials(ptyger_ctx* ctx, double* dF, double* bound,
  * feasible P), E_DATA for a window out of bounds. */
 ptyger_status ptyger_partition(const int32_t* scan, int64_t n, int64_t H, int32_t N, int32_t P,
                                int32_t* frame_rank, int64_t* rows);
+
+/* ptyger_partition for fractional positions (R#22): rows by the integer corners floor(x) and,
+ * when any fraction is nonzero, ext_hi = min(max owned floor(row) + N + 1, H) (the bilinear
+ * window's footprint).  scan: n*(row, col) float32.  Errors as ptyger_partition. */
+ptyger_status ptyger_partition_subpixel(const float* scan, int64_t n, int64_t H, int32_t N, int32_t P,
+                                        int32_t* frame_rank, int64_t* rows);
 
 /* Float scan positions (Alg.1 'float32 h_s') -> int32 corners, round half-up
  * in double: floor((double)x + 0.5) (R#3).  raw and out hold 2*n values. */

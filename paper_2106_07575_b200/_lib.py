@@ -49,6 +49,8 @@ def _load():
     sig = {
         "ptyger_config_default": (None, [C.POINTER(Config)]),
         "ptyger_init": (I32, [C.POINTER(P), C.POINTER(Config), P, I64, I64, P, I32, P, I64, P]),
+        "ptyger_init_subpixel": (I32, [C.POINTER(P), C.POINTER(Config), P, I64, I64, P, I32, P, I64, P]),
+        "ptyger_partition_subpixel": (I32, [P, I64, I64, I32, I32, P, P]),
         "ptyger_cg_iterate": (I32, [P, I32, P]),
         "ptyger_get_object": (I32, [P, P]),
         "ptyger_get_gradient": (I32, [P, P]),
@@ -129,6 +131,15 @@ def partition(scan, H: int, N: int, P: int):
     return rank, rows
 
 
+def partition_subpixel(scan, H: int, N: int, P: int):
+    scan = np.ascontiguousarray(scan, dtype=np.float32)
+    n = len(scan)
+    rank = np.zeros(n, np.int32)
+    rows = np.zeros((P, 6), np.int64)
+    _check(lib.ptyger_partition_subpixel(scan.ctypes.data, n, H, N, P, rank.ctypes.data, rows.ctypes.data))
+    return rank, rows
+
+
 def round_positions(raw):
     raw = np.ascontiguousarray(raw, dtype=np.float32)
     out = np.zeros(raw.shape, np.int32)
@@ -170,15 +181,17 @@ class Ptyger:
         p = as_c64(probe)
         self.H, self.W = (o.shape[0], o.shape[1]) if o.ndim == 3 else (obj.shape[0], obj.shape[1])
         self.N = int(probe.shape[0])
-        sc = np.ascontiguousarray(np.asarray(scan), dtype=np.int32)
+        # a floating-point scan array selects the fractional-position (bilinear window) entry point
+        self.subpixel = np.issubdtype(np.asarray(scan).dtype, np.floating)
+        sc = np.ascontiguousarray(np.asarray(scan), dtype=np.float32 if self.subpixel else np.int32)
         self.n = len(sc)
         dd = d if hasattr(d, "data_ptr") else np.ascontiguousarray(d, dtype=np.float32)
         po, ko = _ptr(o)
         pp, kp = _ptr(p)
         pd, kd = _ptr(dd)
         self.ctx = C.c_void_p()
-        st = lib.ptyger_init(C.byref(self.ctx), C.byref(self.cfg), po, self.H, self.W, pp, self.N,
-                             sc.ctypes.data, self.n, pd)
+        init = lib.ptyger_init_subpixel if self.subpixel else lib.ptyger_init
+        st = init(C.byref(self.ctx), C.byref(self.cfg), po, self.H, self.W, pp, self.N, sc.ctypes.data, self.n, pd)
         _check(st, None)
         self.K = self.cfg.ls_batch
 

@@ -128,6 +128,8 @@ struct ptyger_ctx {
     int* order = nullptr;
     int* tile_ptr = nullptr;
     int* entries = nullptr;
+    float2* frac = nullptr;      // per storage frame fractional offsets (subpixel mode only)
+    bool subpx = false;
     int ntx = 0, nty = 0;
     double *part_adj = nullptr, *part_fr = nullptr, *part_el = nullptr, *scratch = nullptr;
     int band_grid = 0;
@@ -337,7 +339,7 @@ static void free_ctx(ptyger_ctx* c) {
     for (int p = 0; p < 2; ++p)
         if (c->graph[p]) cudaGraphExecDestroy(c->graph[p]);
     void* ptrs[] = {c->psi, c->g[0], c->g[1], c->eta, c->u, c->v, c->probe, c->probe_s, c->full, c->recv[0], c->recv[1], c->d,
-                    c->pos, c->order, c->tile_ptr, c->entries, c->part_adj, c->part_fr, c->part_el, c->scratch, c->st,
+                    c->pos, c->order, c->frac, c->tile_ptr, c->entries, c->part_adj, c->part_fr, c->part_el, c->scratch, c->st,
                     c->d_tr};
     if (c->stream) cudaStreamSynchronize(c->stream);
     for (void* p : ptrs)
@@ -422,14 +424,20 @@ ptyger_status ptyger_fft2(const float* in, float* out, int32_t N, int64_t batch,
     return PTYGER_OK;
 }
 
+// fr: nullptr, or 2n fractional offsets (row, col) in [0, 1) of bilinear windows at the integer
+// corners scan (ptyger_init_subpixel, R#22); all-zero offsets take the integer path unchanged.
 static ptyger_status init_impl(ptyger_ctx* c, const float* object, const float* probe, const int32_t* scan,
-                               const float* intensities) {
+                               const float* intensities, const float* fr = nullptr) {
     std::string& err = c->err;
     const ptyger_config& cfg = c->cfg;
     const int N = c->N;
     const int64_t H = c->H, W = c->W, n = c->n;
+    if (fr)
+        for (int64_t i = 0; i < 2 * n; ++i)
+            if (fr[i] != 0.0f) c->subpx = true;
     // ---- partition (host) ----
-    const int rc = partition(scan, n, H, N, cfg.world, c->frame_rank, c->rows, err);
+    const int foot = N + (c->subpx ? 1 : 0);
+    const int rc = partition(scan, n, H, N, cfg.world, c->frame_rank, c->rows, err, foot);
     if (rc) return (ptyger_status)rc;
     const int me = cfg.rank;
     const int64_t* R = &c->rows[6 * me];
@@ -476,7 +484,7 @@ static ptyger_status init_impl(ptyger_ctx* c, const float* object, const float* 
     canonical_order(sub.data(), nl, N, ord64);
     std::vector<int32_t> ord(ord64.begin(), ord64.end());
     std::vector<int32_t> tptr, ent;
-    build_tiles(lpos, ord, N, c->SH, W, c->ntx, c->nty, tptr, ent);
+    build_tiles(lpos, ord, foot, c->SH, W, c->ntx, c->nty, tptr, ent);
 
     // ---- device ----
     int ndev = 0;
@@ -517,13 +525,14 @@ static ptyger_status init_impl(ptyger_ctx* c, const float* object, const float* 
     AL(c->probe, float2, NN);
     AL(c->pos, int2, nl);
     AL(c->order, int, nl);
+    if (c->subpx) AL(c->frac, float2, nl);
     AL(c->tile_ptr, int, tptr.size());
     AL(c->entries, int, ent.size());
     c->grid_fr = (int)std::max<int64_t>(1, std::min<int64_t>(c->sms, nl));
     c->grid_el = c->sms * 8;
     c->band_grid = c->sms * 2;
     AL(c->part_adj, double, ((int64_t)c->ntx * c->nty + 2 * c->band_grid) * NDY);
-    c->hf = N == 128 && getenv("PTYGER_HF") && atoi(getenv("PTYGER_HF")) == 1;   // opt-in (see r1_history)
+    c->hf = N == 128 && !c->subpx && getenv("PTYGER_HF") && atoi(getenv("PTYGER_HF")) == 1;   // opt-in (r1_history)
     c->parts_ls = c->hf ? hf_ls_parts(nl) : c->grid_fr;
     if (c->parts_ls <= 0) {
         err = "half-frame kernel setup failed";
@@ -556,6 +565,15 @@ static ptyger_status init_impl(ptyger_ctx* c, const float* object, const float* 
     for (int64_t i = 0; i < nl; ++i) p2[i] = make_int2(lpos[2 * i], lpos[2 * i + 1]);
     CK(cudaMemcpy(c->pos, p2.data(), sizeof(int2) * nl, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(c->order, ord.data(), sizeof(int) * nl, cudaMemcpyHostToDevice));
+    if (c->subpx) {
+        std::vector<float2> fl(nl);
+        for (int64_t i = 0; i < nl; ++i) {
+            const int64_t j = c->local_global[i];
+            fl[i] = make_float2(fr[2 * j], fr[2 * j + 1]);
+        }
+        CK(cudaMemcpy(c->frac, fl.data(), sizeof(float2) * nl, cudaMemcpyHostToDevice));
+        c->geo.frac = c->frac;
+    }
     CK(cudaMemcpy(c->tile_ptr, tptr.data(), sizeof(int) * tptr.size(), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(c->entries, ent.data(), sizeof(int) * ent.size(), cudaMemcpyHostToDevice));
     // validate d on the device
@@ -586,8 +604,9 @@ static ptyger_status init_impl(ptyger_ctx* c, const float* object, const float* 
     return PTYGER_OK;
 }
 
-ptyger_status ptyger_init(ptyger_ctx** out, const ptyger_config* cfg_in, const float* object, int64_t H, int64_t W,
-                          const float* probe, int32_t N, const int32_t* scan, int64_t n, const float* intensities) {
+static ptyger_status create_ctx(ptyger_ctx** out, const ptyger_config* cfg_in, const float* object, int64_t H,
+                                int64_t W, const float* probe, int32_t N, const int32_t* scan, int64_t n,
+                                const float* intensities, const float* fr) {
     if (!out) return set_err(nullptr, PTYGER_E_ARG, "init: out is NULL");
     *out = nullptr;
     ptyger_config cfg;
@@ -610,7 +629,9 @@ ptyger_status ptyger_init(ptyger_ctx** out, const ptyger_config* cfg_in, const f
     if (n < 1) return set_err(nullptr, PTYGER_E_DATA, "init: need at least one scan position");
     for (int64_t j = 0; j < n; ++j) {
         const int64_t r = scan[2 * j], cc = scan[2 * j + 1];
-        if (r < 0 || r > H - N || cc < 0 || cc > W - N)
+        // a bilinear window with a nonzero fraction also reads the row / column after the window
+        const int64_t er = fr && fr[2 * j] != 0.0f ? 1 : 0, ec = fr && fr[2 * j + 1] != 0.0f ? 1 : 0;
+        if (r < 0 || r + er > H - N || cc < 0 || cc + ec > W - N)
             return set_err(nullptr, PTYGER_E_DATA,
                            "init: scan position of frame " + std::to_string(j) + " (" + std::to_string(r) + ", " +
                                std::to_string(cc) + ") puts the window outside the object");
@@ -630,13 +651,68 @@ ptyger_status ptyger_init(ptyger_ctx** out, const ptyger_config* cfg_in, const f
     c->W = W;
     c->N = N;
     c->n = n;
-    const ptyger_status s = init_impl(c, object, probe, scan, intensities);
+    const ptyger_status s = init_impl(c, object, probe, scan, intensities, fr);
     if (s != PTYGER_OK) {
         g_last_error = c->err;
         free_ctx(c);
         return s;
     }
     *out = c;
+    return PTYGER_OK;
+}
+
+ptyger_status ptyger_init(ptyger_ctx** out, const ptyger_config* cfg_in, const float* object, int64_t H, int64_t W,
+                          const float* probe, int32_t N, const int32_t* scan, int64_t n, const float* intensities) {
+    return create_ctx(out, cfg_in, object, H, W, probe, N, scan, n, intensities, nullptr);
+}
+
+// Fractional positions (R#22): integer corner floor(x) (exact in double) and fraction x - floor(x)
+// (exact in float32: x and floor(x) share the exponent range).
+static ptyger_status split_positions(const float* scan_f, int64_t n, std::vector<int32_t>& base,
+                                     std::vector<float>& frac) {
+    base.resize(2 * n);
+    frac.resize(2 * n);
+    for (int64_t i = 0; i < 2 * n; ++i) {
+        const double x = (double)scan_f[i];
+        if (!std::isfinite(x) || x < 0.0 || x > 2.0e9)
+            return set_err(nullptr, PTYGER_E_DATA,
+                           "init_subpixel: scan position of frame " + std::to_string(i / 2) + " is negative or not finite");
+        const double f = std::floor(x);
+        base[i] = (int32_t)f;
+        frac[i] = (float)(x - f);
+    }
+    return PTYGER_OK;
+}
+
+ptyger_status ptyger_init_subpixel(ptyger_ctx** out, const ptyger_config* cfg, const float* object, int64_t H,
+                                   int64_t W, const float* probe, int32_t N, const float* scan, int64_t n,
+                                   const float* intensities) {
+    if (!out) return set_err(nullptr, PTYGER_E_ARG, "init: out is NULL");
+    if (!scan) return set_err(nullptr, PTYGER_E_ARG, "init: null input array");
+    if (n < 1) return set_err(nullptr, PTYGER_E_DATA, "init: need at least one scan position");
+    std::vector<int32_t> base;
+    std::vector<float> frac;
+    const ptyger_status s = split_positions(scan, n, base, frac);
+    if (s != PTYGER_OK) return s;
+    return create_ctx(out, cfg, object, H, W, probe, N, base.data(), n, intensities, frac.data());
+}
+
+ptyger_status ptyger_partition_subpixel(const float* scan, int64_t n, int64_t H, int32_t N, int32_t P,
+                                        int32_t* frame_rank, int64_t* rows) {
+    if (!scan || !frame_rank || !rows) return set_err(nullptr, PTYGER_E_ARG, "partition: null pointer");
+    std::vector<int32_t> base;
+    std::vector<float> frac;
+    ptyger_status s = split_positions(scan, n, base, frac);
+    if (s != PTYGER_OK) return s;
+    bool sub = false;
+    for (float f : frac) sub |= f != 0.0f;
+    std::vector<int32_t> rk;
+    std::vector<int64_t> rw;
+    std::string err;
+    const int rc = partition(base.data(), n, H, N, P, rk, rw, err, N + (sub ? 1 : 0));
+    if (rc) return set_err(nullptr, (ptyger_status)rc, err);
+    std::memcpy(frame_rank, rk.data(), sizeof(int32_t) * n);
+    std::memcpy(rows, rw.data(), sizeof(int64_t) * rw.size());
     return PTYGER_OK;
 }
 

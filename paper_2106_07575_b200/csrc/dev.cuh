@@ -67,6 +67,35 @@ __device__ __forceinline__ double warp_reduce_scatter(double (&v)[K], int lane) 
 
 __device__ __forceinline__ float2 ldg2(const float2* p) { return __ldg(p); }
 
+// Row-pass input of a window: x[n1] = p[row, T n1 + t] * psi~(s + (row, T n1 + t)).
+// Integer positions (R#3): psi~ = psi.  Fractional positions (R#22, g.frac set): psi~ is the bilinear
+// interpolation at (s.x + fy + row, s.y + fx + col):
+//     (1 - fy) [(1 - fx) psi[r, c] + fx psi[r, c + 1]] + fy [(1 - fx) psi[r + 1, c] + fx psi[r + 1, c + 1]].
+// A +1 tap past the last stored row / column only occurs with weight 0 (init validation and the
+// partition's N + 1 footprint) and is clamped in bounds.
+template <int R, int T>
+__device__ __forceinline__ void window_row(const float2* __restrict__ obj, const Geometry& g, int2 s, int64_t j,
+                                           int row, int t, const float2* __restrict__ pp, float2 (&x)[R]) {
+    const float2* src = obj + (int64_t)(s.x + row) * g.W + s.y + t;
+    if (!g.frac) {
+#pragma unroll
+        for (int n1 = 0; n1 < R; ++n1) x[n1] = cmul(ldg2(pp + T * n1), ldg2(src + T * n1));
+        return;
+    }
+    const float2 fr = g.frac[j];
+    const float wy0 = 1.0f - fr.x, wy1 = fr.x, wx0 = 1.0f - fr.y, wx1 = fr.y;
+    const int64_t dn = ((int64_t)s.x + row + 1 < g.SH) ? g.W : 0;
+#pragma unroll
+    for (int n1 = 0; n1 < R; ++n1) {
+        const int dc = ((int64_t)s.y + t + T * n1 + 1 < g.W) ? 1 : 0;
+        const float2* q = src + T * n1;
+        const float2 a = ldg2(q), b = ldg2(q + dc), c = ldg2(q + dn), e = ldg2(q + dn + dc);
+        const float2 top = make_float2(fmaf(wx1, b.x, wx0 * a.x), fmaf(wx1, b.y, wx0 * a.y));
+        const float2 bot = make_float2(fmaf(wx1, e.x, wx0 * c.x), fmaf(wx1, e.y, wx0 * c.y));
+        x[n1] = cmul(ldg2(pp + T * n1), make_float2(fmaf(wy1, bot.x, wy0 * top.x), fmaf(wy1, bot.y, wy0 * top.y)));
+    }
+}
+
 // gamma_k = gamma0 tau^k by repeated multiplication in double: exactly the trial sequence of
 // Eq.7's backtracking (gamma <- gamma tau, Alg.1 662) and of the oracle's line_search.
 __device__ __forceinline__ double trial_gamma(double gamma0, double tau, int k) {

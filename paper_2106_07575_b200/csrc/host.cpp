@@ -9,7 +9,7 @@
 //   3. frame j -> the stripe i with b_i <= centre_j < b_{i+1} (b_0 = -inf, b_P = +inf);
 //   4. feasible iff every stripe's centre-row height (from min centre to max centre + 1) >= N,
 //      so a band is shared by two neighbouring ranks only;
-//   5. ext_i = [min owned r_j, max owned r_j + N);  own rows o_0 = 0, o_P = H,
+//   5. ext_i = [min owned r_j, min(max owned r_j + foot, H)), foot = N (N + 1 for bilinear windows);  own rows o_0 = 0, o_P = H,
 //      o_i = clamp(b_i, ext_i.lo, ext_{i-1}.hi) if ext_{i-1}, ext_i overlap/touch else ext_i.lo;
 //      storage_i = [min(ext_i.lo, o_i), max(ext_i.hi, o_{i+1})).
 #include <algorithm>
@@ -63,7 +63,8 @@ int max_feasible_P(const int32_t* scan, int64_t n, int N, int limit) {
 }
 
 int partition(const int32_t* scan, int64_t n, int64_t H, int N, int P, std::vector<int32_t>& rank,
-              std::vector<int64_t>& rows, std::string& err) {
+              std::vector<int64_t>& rows, std::string& err, int foot) {
+    if (foot < 0) foot = N;
     if (n < 1 || N < 2 || H < N || P < 1) {
         err = "partition: need n >= 1, N >= 2, H >= N, P >= 1";
         return PTYGER_E_ARG;
@@ -93,7 +94,7 @@ int partition(const int32_t* scan, int64_t n, int64_t H, int N, int P, std::vect
         const int r = (int)(std::upper_bound(b.begin(), b.end(), c) - b.begin());
         rank[j] = r;
         elo[r] = std::min<int64_t>(elo[r], scan[2 * j]);
-        ehi[r] = std::max<int64_t>(ehi[r], (int64_t)scan[2 * j] + N);
+        ehi[r] = std::max<int64_t>(ehi[r], std::min<int64_t>((int64_t)scan[2 * j] + foot, H));
     }
     std::vector<int64_t> o(P + 1, 0);
     o[P] = H;
@@ -124,9 +125,10 @@ void round_positions(const float* raw, int64_t n, int32_t* out) {
 }
 
 // Tile -> frame lists for k_adj: 32x32 tiles over the storage rows; for every tile the frames
-// whose window intersects it, in canonical order, as int4 {storage frame, row, col, 0}.
+// whose window footprint (foot x foot: N, or N + 1 for bilinear windows) intersects it, in
+// canonical order, as int4 {storage frame, row, col, 0}.
 void build_tiles(const std::vector<int32_t>& lpos /* 2 per local frame, storage-local */,
-                 const std::vector<int32_t>& order, int N, int64_t SH, int64_t W, int& ntx, int& nty,
+                 const std::vector<int32_t>& order, int foot, int64_t SH, int64_t W, int& ntx, int& nty,
                  std::vector<int32_t>& tile_ptr, std::vector<int32_t>& entries) {
     ntx = (int)((W + 31) / 32);
     nty = (int)((SH + 31) / 32);
@@ -134,8 +136,8 @@ void build_tiles(const std::vector<int32_t>& lpos /* 2 per local frame, storage-
     std::vector<int64_t> cnt(nt + 1, 0);
     for (int32_t j : order) {
         const int64_t r = lpos[2 * j], c = lpos[2 * j + 1];
-        for (int64_t ty = r / 32; ty <= (r + N - 1) / 32 && ty < nty; ++ty)
-            for (int64_t tx = c / 32; tx <= (c + N - 1) / 32 && tx < ntx; ++tx) cnt[ty * ntx + tx + 1]++;
+        for (int64_t ty = r / 32; ty <= (r + foot - 1) / 32 && ty < nty; ++ty)
+            for (int64_t tx = c / 32; tx <= (c + foot - 1) / 32 && tx < ntx; ++tx) cnt[ty * ntx + tx + 1]++;
     }
     for (int64_t t = 0; t < nt; ++t) cnt[t + 1] += cnt[t];
     tile_ptr.resize(nt + 1);
@@ -144,8 +146,8 @@ void build_tiles(const std::vector<int32_t>& lpos /* 2 per local frame, storage-
     std::vector<int64_t> fill(cnt.begin(), cnt.end() - 1);
     for (int32_t j : order) {
         const int64_t r = lpos[2 * j], c = lpos[2 * j + 1];
-        for (int64_t ty = r / 32; ty <= (r + N - 1) / 32 && ty < nty; ++ty)
-            for (int64_t tx = c / 32; tx <= (c + N - 1) / 32 && tx < ntx; ++tx) {
+        for (int64_t ty = r / 32; ty <= (r + foot - 1) / 32 && ty < nty; ++ty)
+            for (int64_t tx = c / 32; tx <= (c + foot - 1) / 32 && tx < ntx; ++tx) {
                 const int64_t e = fill[ty * ntx + tx]++;
                 entries[4 * e + 0] = j;
                 entries[4 * e + 1] = (int32_t)r;

@@ -51,6 +51,8 @@ struct Geometry {
     int64_t band_lo0, band_hi0, band_lo1, band_hi1;  // storage-local band rows excluded from k_adj partials
     int64_t n_local;         // frames stored on this rank
     int est;                 // estimator (PTYGER_EST_ML / PTYGER_EST_LS) for the residual and F terms
+    const float2* frac;      // per storage frame (row, col) fractional offsets of a bilinear window
+                             // (R#22, ptyger_init_subpixel); nullptr = integer positions
 };
 
 struct SolverCfg {

@@ -52,11 +52,7 @@ __global__ void __launch_bounds__(512, 1) k_fwd(Geometry g, const float2* __rest
             float2 x[R];
             if (i < nfr) {
                 const int j = order[i];
-                const int2 s = pos[j];
-                const float2* src = psi + (int64_t)(s.x + row) * g.W + s.y + t;
-                const float2* pp = probe + row * N + t;
-#pragma unroll
-                for (int n1 = 0; n1 < R; ++n1) x[n1] = cmul(ldg2(pp + T * n1), ldg2(src + T * n1));
+                window_row<R, T>(psi, g, pos[j], j, row, t, probe + row * N + t, x);
             } else {
 #pragma unroll
                 for (int n1 = 0; n1 < R; ++n1) x[n1] = make_float2(0.f, 0.f);
@@ -231,11 +227,7 @@ __global__ void __launch_bounds__(512, 1) k_ls(Geometry g, const float2* __restr
             const int64_t i = grp * C::FPB + f;
             if (i < nfr) {
                 const int j = order[i];
-                const int2 s = pos[j];
-                const float2* src = eta + (int64_t)(s.x + row) * g.W + s.y + t;
-                const float2* pp = probe_s + row * N + t;
-#pragma unroll
-                for (int n1 = 0; n1 < R; ++n1) x[n1] = cmul(ldg2(pp + T * n1), ldg2(src + T * n1));
+                window_row<R, T>(eta, g, pos[j], j, row, t, probe_s + row * N + t, x);
             } else {
 #pragma unroll
                 for (int n1 = 0; n1 < R; ++n1) x[n1] = make_float2(0.f, 0.f);

@@ -40,6 +40,39 @@ __global__ void __launch_bounds__(256) k_adj(Geometry g, const float2* __restric
         __syncthreads();
         if ((int)threadIdx.x < ne) sent[threadIdx.x] = __ldg(ent + e0 + threadIdx.x);
         __syncthreads();
+        if (g.frac) {
+            // bilinear windows (R#22): frame pixel (i, k) was sampled from psi[r0 + i + a, c0 + k + b]
+            // with weight wy_a wx_b, so g[R, C] += sum_{a, b} wy_a wx_b y[R - r0 - a, C - c0 - b]
+            for (int e = 0; e < ne; ++e) {
+                const int4 en = sent[e];
+                const float2 fr = __ldg(g.frac + en.x);
+                const float wy[2] = {1.0f - fr.x, fr.x}, wx[2] = {1.0f - fr.y, fr.y};
+                const float2* yb = y + (int64_t)en.x * NN;
+                const int dc = (int)(col - en.z);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int dr = (int)(row0 + 8 * i - en.y);
+                    float2 sacc = make_float2(0.f, 0.f);
+#pragma unroll
+                    for (int a = 0; a < 2; ++a) {
+                        float2 rs = make_float2(0.f, 0.f);
+#pragma unroll
+                        for (int b = 0; b < 2; ++b) {
+                            const int rr = dr - a, cc = dc - b;
+                            if ((unsigned)rr < (unsigned)N && (unsigned)cc < (unsigned)N) {
+                                const float2 yv = ldg2(yb + (int64_t)rr * N + cc);
+                                rs.x = fmaf(wx[b], yv.x, rs.x);
+                                rs.y = fmaf(wx[b], yv.y, rs.y);
+                            }
+                        }
+                        sacc.x = fmaf(wy[a], rs.x, sacc.x);
+                        sacc.y = fmaf(wy[a], rs.y, sacc.y);
+                    }
+                    acc[i] = cadd(acc[i], sacc);
+                }
+            }
+            continue;
+        }
         int e = 0;
         for (; e + 4 <= ne; e += 4) {
             float2 val[4][4];

@@ -162,11 +162,8 @@ __global__ void __launch_bounds__(512, 1) k_lsfwd256(Geometry g, const float2* _
 #pragma unroll 1
         for (int rb = 0; rb < N / ROWB; ++rb) {
             const int row = rb * ROWB + tid / T, t = tid % T;
-            const float2* src = obj + (int64_t)(s.x + row) * g.W + s.y + t;
-            const float2* pp = probe + row * N + t;
             float2 x[R];
-#pragma unroll
-            for (int n1 = 0; n1 < R; ++n1) x[n1] = cmul(ldg2(pp + T * n1), ldg2(src + T * n1));
+            window_row<R, T>(obj, g, s, j, row, t, probe + row * N + t, x);
             float2* srow = buf + (tid / T) * LD;
             __syncwarp();
             row_fft_regs<N, false>(x, srow, t, tw);
