@@ -18,6 +18,7 @@
 #include <stdlib.h>
 
 #include "dev.cuh"
+#include "tma.cuh"
 
 namespace pty {
 
@@ -155,6 +156,7 @@ __global__ void __launch_bounds__(512, 1) k_grad(Geometry g, float2* __restrict_
             row_fft<N, true>(x, sf + f * C::FRAME_ELEMS + row * LD, t, tw);
         }
         __syncthreads();
+
 #pragma unroll 1
         for (int rd = 0; rd < C::ROUNDS; ++rd) {
             const int t = warp % T;
@@ -196,7 +198,7 @@ __global__ void __launch_bounds__(512, 1) k_ls(Geometry g, const float2* __restr
                                                const int* __restrict__ order, const float2* __restrict__ u,
                                                float2* __restrict__ v, const float* __restrict__ d,
                                                SolverCfg cfg, double* __restrict__ part,
-                                               const DevState* __restrict__ st) {
+                                               const DevState* __restrict__ st, int pf) {
     using C = FFTCfg<N>;
     constexpr int R = C::R, T = C::T, LD = C::LD;
     extern __shared__ float2 smem[];
@@ -219,6 +221,14 @@ __global__ void __launch_bounds__(512, 1) k_ls(Geometry g, const float2* __restr
     double tot = 0.0;  // running total of entry lane >> 1 of S
     double mom[4] = {0.0, 0.0, 0.0, 0.0};
     for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+        if constexpr (C::FPB == 1) {
+            // this frame's u, d into L2 now: the epilogue reads them after both transforms
+            if (pf && grp < nfr) {
+                const int64_t jp = order[grp];
+                if (tid < 32) prefetch_l2_frame(u + jp * N * N, N * N * 8, tid);
+                else if (tid < 64) prefetch_l2_frame(d + jp * N * N, N * N * 4, tid - 32);
+            }
+        }
         // row pass input of round rd: x[n1] = (p / N)[row, T n1 + t] * eta[s + (row, T n1 + t)]
         // (p / N: the unitary scale folded into the probe)
         auto load_row = [&](int rd, float2 (&x)[R]) {
@@ -416,7 +426,10 @@ int launch_grad(const Geometry& g, float2* u, float2* v, const float* d, const f
         case 32: return grad_n<32>(g, u, v, d, probe_s, st, eps, grid, s);
         case 64: return grad_n<64>(g, u, v, d, probe_s, st, eps, grid, s);
         case 128:
-            if (!getenv("PTYGER_GRAD_V1")) return launch_grad128(g, u, v, d, probe_s, st, eps, grid, s);
+            // direct-load k_grad<128> (2.57 ms, 88 % of HBM at paper scale) beats the TMA-ring
+            // k_grad128 (3.13 ms) since the residual lost its division slow path; the ring kernel
+            // stays selectable for comparison (PTYGER_GRAD_TMA=1)
+            if (getenv("PTYGER_GRAD_TMA")) return launch_grad128(g, u, v, d, probe_s, st, eps, grid, s);
             return grad_n<128>(g, u, v, d, probe_s, st, eps, grid, s);
         case 256: return launch_grad256(g, u, v, d, probe, st, eps, grid, s);
     }
@@ -429,7 +442,9 @@ static int ls_n(const Geometry& g, const float2* eta, const float2* probe, const
                 double* part, int grid, const DevState* st, cudaStream_t s) {
     using C = FFTCfg<N>;
     if (set_smem(k_ls<N>, C::SMEM_BYTES)) return -1;
-    k_ls<N><<<grid, C::NT, C::SMEM_BYTES, s>>>(g, eta, probe, pos, order, u, v, d, c, part, st);
+    // L2 prefetch of each frame's u, d at its start (measured: k_ls 3.29 -> 3.23 ms at paper scale)
+    static const int pf = getenv("PTYGER_PF") ? atoi(getenv("PTYGER_PF")) : 1;
+    k_ls<N><<<grid, C::NT, C::SMEM_BYTES, s>>>(g, eta, probe, pos, order, u, v, d, c, part, st, pf != 0);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 

@@ -12,6 +12,7 @@
 // free.  Everything else (FFT, residual, epilogue) is the generic k_grad path.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "dev.cuh"
 #include "tma.cuh"

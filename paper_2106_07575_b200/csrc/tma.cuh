@@ -54,6 +54,21 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 
+// Bulk L2 prefetch (TMA engine, no shared memory / registers involved); bytes multiple of 16.
+__device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
+// Threads 0..pieces-1 of the CTA each prefetch one 16 KB piece of [src, src + bytes).
+__device__ __forceinline__ void prefetch_l2_frame(const void* src, uint32_t bytes, int tid) {
+    constexpr uint32_t PIECE = 16384;
+    const uint32_t pieces = (bytes + PIECE - 1) / PIECE;
+    if ((uint32_t)tid < pieces) {
+        const uint32_t off = (uint32_t)tid * PIECE;
+        prefetch_l2(static_cast<const char*>(src) + off, bytes - off < PIECE ? bytes - off : PIECE);
+    }
+}
+
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
