@@ -278,16 +278,29 @@ __device__ __forceinline__ void ls_screen_nz(float2 uu, float2 vv, float dd, con
         const float rc = (c >= eps2) ? __fdividef(1.0f, c) : 0.0f;
         const float dl = dd * 0.693147182464599609375f;
         float amax = 0.f;
+        // only the log part: q_k = gamma_k a + gamma_k^2 b of EVERY pixel goes to the (za, zb)
+        // moments in ls_push (one op per trial less than forming cn - c here).  No clamp of cn:
+        // cn * rc = 0 (|u + gamma v| or |u| below eps, or an FTZ underflow) gives log2 = -inf, a
+        // non-finite S and therefore the exact pass, which applies the guarded definition R#4.
+        // Trials run in pairs on the paired FP32 pipe (FFMA2 / FMUL2: per lane the same fp32
+        // operations as the scalar form, so the screened sums are bit-identical to it).
 #pragma unroll
-        for (int k = 0; k < KT; ++k) {
-            // only the log part: q_k = gamma_k a + gamma_k^2 b of EVERY pixel goes to the (za, zb)
-            // moments in ls_push (one op per trial less than forming cn - c here).  No clamp of cn:
-            // cn * rc = 0 (|u + gamma v| or |u| below eps, or an FTZ underflow) gives log2 = -inf, a
-            // non-finite S and therefore the exact pass, which applies the guarded definition R#4.
+        for (int k = 0; k + 1 < KT; k += 2) {
+            const float2 g2 = make_float2(sgam[k], sgam[k + 1]);
+            const float2 ex = fma2(g2, bc2(vv.x), bc2(uu.x));
+            const float2 ey = fma2(g2, bc2(vv.y), bc2(uu.y));
+            const float2 w = mul2(fma2(ex, ex, mul2(ey, ey)), bc2(rc));
+            const float L0 = lg2_ftz(w.x), L1 = lg2_ftz(w.y);
+            const float2 s2 = fma2(bc2(-dl), make_float2(L0, L1), make_float2(S[k], S[k + 1]));
+            S[k] = s2.x;
+            S[k + 1] = s2.y;
+            amax = fmaxf(amax, fmaxf(fabsf(L0), fabsf(L1)));
+        }
+        if constexpr (KT & 1) {
+            constexpr int k = KT - 1;
             const float gam = sgam[k];
             const float ex = fmaf(gam, vv.x, uu.x), ey = fmaf(gam, vv.y, uu.y);
-            const float cn = fmaf(ex, ex, ey * ey);
-            const float L2 = lg2_ftz(cn * rc);
+            const float L2 = lg2_ftz(fmaf(ex, ex, ey * ey) * rc);
             S[k] = fmaf(-dl, L2, S[k]);
             amax = fmaxf(amax, fabsf(L2));
         }

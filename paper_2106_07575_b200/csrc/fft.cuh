@@ -22,20 +22,56 @@
 
 namespace pty {
 
-__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
-__device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
-// a * b
+// Complex arithmetic on Blackwell's paired FP32 instructions (PTX add/sub/mul/fma .rn.f32x2 ->
+// SASS FADD2 / FMUL2 / FFMA2, one issue slot for both components; a float2 is a 64-bit register
+// pair, so packing is free).  Each lane is an IEEE fp32 operation (round to nearest), so accuracy
+// is that of the scalar forms; the products of a complex multiply round in a different order.
+__device__ __forceinline__ uint64_t f2u(float2 a) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a.x), "f"(a.y));
+    return r;
+}
+__device__ __forceinline__ float2 u2f(uint64_t r) {
+    float2 a;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a.x), "=f"(a.y) : "l"(r));
+    return a;
+}
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+    uint64_t r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2u(a)), "l"(f2u(b)));
+    return u2f(r);
+}
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+    uint64_t r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2u(a)), "l"(f2u(b)));
+    return u2f(r);
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+    uint64_t r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2u(a)), "l"(f2u(b)));
+    return u2f(r);
+}
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+    uint64_t r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(f2u(a)), "l"(f2u(b)), "l"(f2u(c)));
+    return u2f(r);
+}
+__device__ __forceinline__ float2 bc2(float a) { return make_float2(a, a); }
+
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return add2(a, b); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return sub2(a, b); }
+__device__ __forceinline__ float2 cscale(float2 a, float s) { return mul2(a, bc2(s)); }
+// a * b = a.x (b.x, b.y) + a.y (-b.y, b.x)
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
-    return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+    return fma2(bc2(a.y), make_float2(-b.y, b.x), mul2(bc2(a.x), b));
 }
-// a * conj(b)
+// a * conj(b) = a.x (b.x, -b.y) + a.y (b.y, b.x)
 __device__ __forceinline__ float2 cmulc(float2 a, float2 b) {
-    return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -a.x * b.y));
+    return fma2(bc2(a.y), make_float2(b.y, b.x), mul2(bc2(a.x), make_float2(b.x, -b.y)));
 }
-// conj(a) * b
+// conj(a) * b = a.x (b.x, b.y) + a.y (b.y, -b.x)
 __device__ __forceinline__ float2 cconjmul(float2 a, float2 b) {
-    return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.x, b.y, -a.y * b.x));
+    return fma2(bc2(a.y), make_float2(b.y, -b.x), mul2(bc2(a.x), b));
 }
 
 // cos / sin of 2 pi q / 16 for q in [0, 16) (compile-time after unrolling)
@@ -62,7 +98,7 @@ __device__ __forceinline__ float2 twr(float2 x, int m) {
     if (q == 12) return INV ? make_float2(x.y, -x.x) : make_float2(-x.y, x.x);
     const float c = cos16(q);
     const float s = INV ? sin16(q) : -sin16(q);
-    return make_float2(fmaf(x.x, c, -x.y * s), fmaf(x.x, s, x.y * c));
+    return cmul(x, make_float2(c, s));
 }
 
 template <int R, bool INV> struct DFT;
