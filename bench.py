@@ -91,13 +91,42 @@ def synth_device(w: I.Workload, device, view: int | None = None):
 # ----------------------------------------------------------------------------- clocks
 
 class ClockSampler:
+    """SM clock and throttle reasons sampled DURING the timed region: NVML every 2 ms in a thread
+    (nvidia-smi -lms 100 as a fallback)."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
+
     def __init__(self, index: int):
         self.index = index
-        self.samples = []
+        self.samples = []          # (sm_mhz, reasons bitmask)
+        self.max_mhz = None
         self.proc = None
         self.thread = None
+        self.stop_flag = False
+        self.nvml = None
 
     def start(self):
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            self.nvml = (nv, h)
+            self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+
+            def poll():
+                while not self.stop_flag:
+                    try:
+                        self.samples.append((float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)),
+                                             int(nv.nvmlDeviceGetCurrentClocksEventReasons(h))))
+                    except Exception:
+                        pass
+                    time.sleep(0.002)
+            self.thread = threading.Thread(target=poll, daemon=True)
+            self.thread.start()
+            return
+        except Exception:
+            self.nvml = None
         q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
@@ -108,33 +137,39 @@ class ClockSampler:
         except Exception:
             self.proc = None
             return
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
         def rd():
             for line in self.proc.stdout:
-                self.samples.append([x.strip() for x in line.split(",")])
+                f = [x.strip() for x in line.split(",")]
+                if len(f) < 7 or not f[0].replace(".", "").isdigit():
+                    continue
+                mask = 0
+                for i, nm in enumerate(names):
+                    if f[3 + i].lower().startswith("active"):
+                        mask |= self.REASONS[nm]
+                self.samples.append((float(f[0]), mask))
+                if f[1].replace(".", "").isdigit():
+                    self.max_mhz = float(f[1])
         self.thread = threading.Thread(target=rd, daemon=True)
         self.thread.start()
 
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(2)
-        except Exception:
-            self.proc.kill()
-        sm = [float(s[0]) for s in self.samples if len(s) >= 7 and s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if len(s) >= 7 and s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = set()
-        for s in self.samples:
-            if len(s) < 7:
-                continue
-            for i, nm in enumerate(names):
-                if s[3 + i].lower().startswith("active"):
-                    reasons.add(nm)
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        self.stop_flag = True
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+        if self.thread is not None:
+            self.thread.join(1.0)
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["no clock samples"], "samples": 0}
+        reasons = sorted({nm for _, m in self.samples for nm, bit in self.REASONS.items() if m & bit})
+        return {"sm_mhz": float(np.median([c for c, _ in self.samples])), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.samples),
+                "source": "nvml" if self.nvml else "nvidia-smi"}
 
 
 # ----------------------------------------------------------------------------- CPU oracle
@@ -220,6 +255,7 @@ def main():
     # warm-up (real iterations)
     pt.iterate(args.warmup, traces=False)
     barrier()
+    pt.kernel_times(reset=True)
     clk = ClockSampler(local)
     clk.start()
     t_host0 = time.perf_counter()
@@ -228,6 +264,9 @@ def main():
     t_host = time.perf_counter() - t_host0
     barrier()
     clocks = clk.stop()
+    # per-launch durations of the two frame kernels over the timed region, measured on the GPU by
+    # the kernels themselves (global ns timer; graph launches on the library stream)
+    ktimes = pt.kernel_times(reset=True)
     if world > 1:
         tt = torch.tensor([ms], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -243,7 +282,12 @@ def main():
     n_local_bytes_grad = 36.0 * n * N * N / world      # u r/w 16, v r 8, d r 4, y w 8
     n_local_bytes_ls = 20.0 * n * N * N / world + 8.0 * w.H * w.W / world  # v w, u r, d r + eta once
     pk, pk_kind = peaks()
-    cand = {"k_grad": (stage[1], n_local_bytes_grad), "k_ls": (stage[4], n_local_bytes_ls)}
+    kt = {k: (v[0] / v[1] if v[1] else stage[1 if k == "k_grad" else 4]) for k, v in ktimes.items()}
+    if world > 1:
+        tt = torch.tensor([kt["k_grad"], kt["k_ls"]], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        kt = {"k_grad": float(tt[0]), "k_ls": float(tt[1])}
+    cand = {"k_grad": (kt["k_grad"], n_local_bytes_grad), "k_ls": (kt["k_ls"], n_local_bytes_ls)}
     dom = max(cand, key=lambda k: cand[k][0])
     dur_ms, algo_bytes = cand[dom]
     achieved = algo_bytes / (dur_ms / 1e3) / 1e9
@@ -314,7 +358,9 @@ def main():
                    "l2": "inputs larger than L2 (u, v, d resident in HBM: %.1f GB)" % (n * N * N * 20 / 1e9)},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": pk, "peak_kind": pk_kind,
                      "unit": "GB/s", "frac": achieved / pk, "traffic": traffic,
-                     "algorithmic_bytes_per_launch": algo_bytes, "avg_launch_ms": dur_ms},
+                     "algorithmic_bytes_per_launch": algo_bytes, "avg_launch_ms": dur_ms,
+                     "timing": "device globaltimer per launch, timed region (%d launches)" % ktimes[dom][1],
+                     "k_grad_avg_ms": kt["k_grad"], "k_ls_avg_ms": kt["k_ls"]},
         "stage_ms": {"begin": stage[0], "k_grad": stage[1], "k_adj": stage[2], "dir_eta": stage[3],
                      "k_ls": stage[4], "ls_rest_upd": stage[5], "iteration_eager": stage[6]},
         "mean_shrinks": float(np.mean(shrinks)),

@@ -180,6 +180,13 @@ ptyger_status ptyger_set_state(ptyger_ctx* ctx, const float* psi, const float* g
  * Returns the number evaluated in *n_eval (nullable). */
 ptyger_status ptyger_get_ls_partials(ptyger_ctx* ctx, double* dF, double* bound, int32_t K, int32_t* n_eval);
 
+/* Device-measured durations of the two frame kernels, summed over every launch since the last
+ * reset: ms[0] / count[0] the GRAD-stage frame kernel (k_grad), ms[1] / count[1] the LS pass-0
+ * frame kernel (k_ls).  One launch = max CTA end - min CTA start on the GPU's global nanosecond
+ * timer, recorded by the kernels themselves, so the numbers cover graph-launched iterations
+ * (ptyger_cg_iterate) exactly as they ran.  reset != 0 zeroes the sums after reading. */
+ptyger_status ptyger_kernel_times(ptyger_ctx* ctx, double* ms, int32_t* count, int32_t reset);
+
 /* Host-only helpers (no GPU needed) --------------------------------------------------- */
 
 /* Integer stripe partition (R#18; PAPER.md:493-503 workload distribution).

@@ -66,6 +66,7 @@ def _load():
         "ptyger_kernel_launches": (I64, [P]),
         "ptyger_last_iterate_ms": (C.c_float, [P]),
         "ptyger_stage_times": (I32, [P, I32, P]),
+        "ptyger_kernel_times": (I32, [P, P, P, I32]),
         "ptyger_destroy": (None, [P]),
         "ptyger_version": (C.c_char_p, []),
     }
@@ -259,6 +260,13 @@ class Ptyger:
         _check(lib.ptyger_stage_times(self.ctx, n_iter, ms.ctypes.data), self.ctx)
         return ms
 
+    def kernel_times(self, reset: bool = True):
+        """{"k_grad": (total ms, launches), "k_ls": (total ms, launches)} since the last reset."""
+        ms = np.zeros(2, np.float64)
+        cnt = np.zeros(2, np.int32)
+        _check(lib.ptyger_kernel_times(self.ctx, ms.ctypes.data, cnt.ctypes.data, int(reset)), self.ctx)
+        return {"k_grad": (float(ms[0]), int(cnt[0])), "k_ls": (float(ms[1]), int(cnt[1]))}
+
     def kernel_launches(self) -> int:
         return int(lib.ptyger_kernel_launches(self.ctx))
 
@@ -278,6 +286,13 @@ class ViewBatch:
 
     def last_iterate_ms(self) -> float:
         return sum(v.last_iterate_ms() for v in self.views)
+
+    def kernel_times(self, reset: bool = True):
+        """{"k_grad": (total ms, launches), "k_ls": (total ms, launches)} since the last reset."""
+        ms = np.zeros(2, np.float64)
+        cnt = np.zeros(2, np.int32)
+        _check(lib.ptyger_kernel_times(self.ctx, ms.ctypes.data, cnt.ctypes.data, int(reset)), self.ctx)
+        return {"k_grad": (float(ms[0]), int(cnt[0])), "k_ls": (float(ms[1]), int(cnt[1]))}
 
     def kernel_launches(self) -> int:
         return sum(v.kernel_launches() for v in self.views)

@@ -596,6 +596,7 @@ static ptyger_status init_impl(ptyger_ctx* c, const float* object, const float* 
     // F(psi_0), u_0
     DevState hs;
     std::memset(&hs, 0, sizeof(hs));
+    hs.tk_start[0] = hs.tk_start[1] = ~0ull;   // disarmed frame-kernel timers
     CK(cudaMemcpy(c->st, &hs, sizeof(hs), cudaMemcpyHostToDevice));
     int rc2 = run_forward(c, err);
     if (rc2) return (ptyger_status)rc2;
@@ -852,6 +853,7 @@ ptyger_status ptyger_set_state(ptyger_ctx* c, const float* psi, const float* g_p
     DevState hs;
     std::memset(&hs, 0, sizeof(hs));
     hs.m = m;
+    hs.tk_start[0] = hs.tk_start[1] = ~0ull;
     CK(cudaMemcpy(c->st, &hs, sizeof(hs), cudaMemcpyHostToDevice));
     c->m_host = m;
     c->failed_numeric = false;
@@ -901,6 +903,21 @@ ptyger_status ptyger_stage_times(ptyger_ctx* c, int32_t n_iter, double* ms) {
     }
     for (int i = 0; i < 7; ++i) cudaEventDestroy(ev[i]);
     return check_numeric(c);
+}
+
+ptyger_status ptyger_kernel_times(ptyger_ctx* c, double* ms, int32_t* count, int32_t reset) {
+    if (!c || !ms || !count) return set_err(c, PTYGER_E_ARG, "kernel_times: null pointer");
+    std::string& err = c->err;
+    CK(cudaSetDevice(c->cfg.device));
+    LK(launch_timers(c->st, c->scratch, reset != 0, c->stream));
+    double h[4];
+    CK(cudaMemcpyAsync(h, c->scratch, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    ms[0] = h[0];
+    ms[1] = h[1];
+    count[0] = (int32_t)h[2];
+    count[1] = (int32_t)h[3];
+    return PTYGER_OK;
 }
 
 void ptyger_destroy(ptyger_ctx* c) { free_ctx(c); }

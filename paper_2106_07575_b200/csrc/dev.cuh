@@ -67,6 +67,21 @@ __device__ __forceinline__ double warp_reduce_scatter(double (&v)[K], int lane) 
 
 __device__ __forceinline__ float2 ldg2(const float2* p) { return __ldg(p); }
 
+// Frame-kernel timers (DevState::tk_*): thread 0 of every CTA marks its start / end with the
+// global nanosecond timer, so one launch's duration is max(end) - min(start) over its CTAs.
+// The timer words are the only DevState fields these kernels write (hence the const_cast).
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void ktime_start(const DevState* st, int i) {
+    if (threadIdx.x == 0) atomicMin(const_cast<unsigned long long*>(&st->tk_start[i]), gtimer());
+}
+__device__ __forceinline__ void ktime_end(const DevState* st, int i) {
+    if (threadIdx.x == 0) atomicMax(const_cast<unsigned long long*>(&st->tk_end[i]), gtimer());
+}
+
 // Row-pass input of a window: x[n1] = p[row, T n1 + t] * psi~(s + (row, T n1 + t)).
 // Integer positions (R#3): psi~ = psi.  Fractional positions (R#22, g.frac set): psi~ is the bilinear
 // interpolation at (s.x + fy + row, s.y + fx + col):

@@ -38,6 +38,11 @@ struct DevState {
     int need_exact;          // pass + 1 when the screening pick left that pass undecided
     int k_unc;               // first undecided trial
     int n_exact;             // exact re-evaluations so far (diagnostic)
+    // device-side kernel timers (globaltimer ns) of the two frame kernels, [0] GRAD, [1] LS pass 0:
+    // first CTA start / last CTA end of the current launch, folded into sums by k_begin_iter
+    unsigned long long tk_start[2], tk_end[2];
+    double tk_sum_ms[2];
+    int tk_cnt[2];
     int trace_idx;           // slot of the current iteration in the trace buffer
     int trace_cap;           // capacity of trace_ptr
     ptyger_trace* trace_ptr; // device trace buffer of the current ptyger_cg_iterate call
@@ -104,6 +109,7 @@ int launch_pick(DevState* st, const SolverCfg& c, int pass, int exact_mode, int 
 int launch_upd(const Geometry& g, float2* psi, const float2* eta, const DevState* st, int grid,
                cudaStream_t s);
 int launch_begin_iter(DevState* st, cudaStream_t s);
+int launch_timers(DevState* st, double* out, int reset, cudaStream_t s);
 int launch_fold(const Geometry& g, float2* u, const float2* v, DevState* st, int grid, cudaStream_t s);
 int launch_validate_d(const float* d, int64_t count, int64_t frame_elems, unsigned long long* bad,
                       cudaStream_t s);

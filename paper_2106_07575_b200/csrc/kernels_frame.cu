@@ -113,6 +113,7 @@ __global__ void __launch_bounds__(512, 1) k_grad(Geometry g, float2* __restrict_
     float2* sf = smem;
     float2* tw = smem + C::FPB * C::FRAME_ELEMS;
     if (st->numeric_error) return;
+    ktime_start(st, 0);
     build_twiddles<N>(tw);
     __syncthreads();
     const float gam = (float)st->gamma;
@@ -183,6 +184,8 @@ __global__ void __launch_bounds__(512, 1) k_grad(Geometry g, float2* __restrict_
         }
         __syncthreads();
     }
+    __syncthreads();
+    ktime_end(st, 0);
 }
 
 
@@ -212,6 +215,7 @@ __global__ void __launch_bounds__(512, 1) k_ls(Geometry g, const float2* __restr
     const bool err = st->numeric_error != 0;
     int base, cnt;
     ls_pass_range(0, st->keff, cfg, base, cnt);
+    ktime_start(st, 1);
     build_twiddles<N>(tw);
     if (tid < KC) sgam[tid] = (float)trial_gamma(cfg.gamma0, cfg.tau, base + tid);
     __syncthreads();
@@ -375,6 +379,7 @@ __global__ void __launch_bounds__(512, 1) k_ls(Geometry g, const float2* __restr
         }
         __syncthreads();
     }
+    ktime_end(st, 1);
     ls_block_out<KC, 16>(tot, mom, sred, smom, part);
 }
 

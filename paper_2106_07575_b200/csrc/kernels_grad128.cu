@@ -70,6 +70,7 @@ __global__ void __launch_bounds__(512, 1) k_grad128(Geometry g, float2* __restri
         }
     };
 
+    ktime_start(st, 0);
     build_twiddles<N>(tw);
     if (tid == 0) {
         for (int i = 0; i < 4; ++i) mbar_init(&bar[i], 1);
@@ -156,6 +157,7 @@ __global__ void __launch_bounds__(512, 1) k_grad128(Geometry g, float2* __restri
         }
         __syncthreads();
     }
+    ktime_end(st, 0);
 }
 
 int launch_grad128(const Geometry& g, float2* u, float2* v, const float* d, const float2* probe_s,

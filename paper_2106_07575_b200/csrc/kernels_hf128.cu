@@ -180,6 +180,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2)
     const bool err = st->numeric_error != 0;
     int base, cnt;
     ls_pass_range(0, st->keff, cfg, base, cnt);
+    ktime_start(st, 1);
     build_twiddles<N>(tw);
     hf_row_twiddles(twr);
     if (tid < KC) sgam[tid] = (float)trial_gamma(cfg.gamma0, cfg.tau, base + tid);
@@ -287,6 +288,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2)
         cl_arrive_relaxed();   // my block is free for the peer's next row pass
     }
     cl_wait();  // pairs with the last arrive: the peer no longer touches this CTA's memory
+    ktime_end(st, 1);
     ls_block_out<KC, NW>(tot, mom, sred, smom, part);
 }
 
@@ -308,6 +310,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2)
     const bool err = st->numeric_error != 0;
     const float gam = (float)st->gamma;
     const bool upd = gam != 0.0f;
+    ktime_start(st, 0);
     build_twiddles<N>(tw);
     hf_row_twiddles(twr);
     const uint32_t sblk = static_cast<uint32_t>(__cvta_generic_to_shared(blk));
@@ -368,6 +371,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2)
         cl_arrive_relaxed();
     }
     cl_wait();
+    ktime_end(st, 0);
 }
 
 // ----------------------------------------------------------------------------------------

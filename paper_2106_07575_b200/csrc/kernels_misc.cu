@@ -216,7 +216,37 @@ __global__ void k_set_F(DevState* st, const double* src, int keff0) {
     st->keff = keff0;  // no previous k*: the first line search evaluates the full pass capacity
 }
 
+// fold the previous launch of each timed frame kernel into the running sums, re-arm the timers
+__device__ __forceinline__ void fold_timers(DevState* st) {
+    for (int i = 0; i < 2; ++i) {
+        if (st->tk_start[i] != ~0ull && st->tk_end[i] > st->tk_start[i]) {
+            st->tk_sum_ms[i] += (double)(st->tk_end[i] - st->tk_start[i]) * 1e-6;
+            st->tk_cnt[i] += 1;
+        }
+        st->tk_start[i] = ~0ull;
+        st->tk_end[i] = 0ull;
+    }
+}
+
+__global__ void k_timers(DevState* st, double* out, int reset) {
+    fold_timers(st);
+    out[0] = st->tk_sum_ms[0];
+    out[1] = st->tk_sum_ms[1];
+    out[2] = (double)st->tk_cnt[0];
+    out[3] = (double)st->tk_cnt[1];
+    if (reset) {
+        st->tk_sum_ms[0] = st->tk_sum_ms[1] = 0.0;
+        st->tk_cnt[0] = st->tk_cnt[1] = 0;
+    }
+}
+
+int launch_timers(DevState* st, double* out, int reset, cudaStream_t s) {
+    k_timers<<<1, 1, 0, s>>>(st, out, reset);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
 __global__ void k_begin_iter(DevState* st) {
+    fold_timers(st);
     st->accepted = 0;
     st->kstar = -1;
     st->n_eval = 0;

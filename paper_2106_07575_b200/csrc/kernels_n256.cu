@@ -65,6 +65,7 @@ __global__ void __launch_bounds__(512, 1) k_grad256(Geometry g, float2* __restri
     float2* buf = smem;
     float2* tw = smem + BUF;
     if (st->numeric_error) return;
+    ktime_start(st, 0);
     build_twiddles<N>(tw);
     __syncthreads();
     const float gam = (float)st->gamma;
@@ -122,6 +123,8 @@ __global__ void __launch_bounds__(512, 1) k_grad256(Geometry g, float2* __restri
         }
         __syncthreads();
     }
+    __syncthreads();
+    ktime_end(st, 0);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -147,6 +150,7 @@ __global__ void __launch_bounds__(512, 1) k_lsfwd256(Geometry g, const float2* _
     const bool err = !FWD && st->numeric_error != 0;
     int base = 0, cnt = 0;
     if (!FWD) ls_pass_range(0, st->keff, cfg, base, cnt);
+    if (!FWD) ktime_start(st, 1);
     build_twiddles<N>(tw);
     if (tid < K) sgam[tid] = (float)trial_gamma(cfg.gamma0, cfg.tau, base + tid);
     __syncthreads();
@@ -227,6 +231,7 @@ __global__ void __launch_bounds__(512, 1) k_lsfwd256(Geometry g, const float2* _
         if (tid == 0) part[blockIdx.x] = s2;
         return;
     }
+    if (!FWD) ktime_end(st, 1);
     ls_block_out<K, 16>(tot, mom, sred, smom, part);
 }
 

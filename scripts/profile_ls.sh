@@ -9,7 +9,7 @@ timeout 900 ncu --set full --clock-control none --import-source on -k 'regex:^k_
     -o gpurun_out/prof_ls_${TAG} -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --e2e-steps 0 \
     > gpurun_out/ncu_ls_${TAG}.log 2>&1
 echo "ncu ls rc=$?" >> gpurun_out/ncu_ls_${TAG}.log
-timeout 900 ncu --set full --clock-control none --import-source on -k 'regex:^k_grad(128|_hf)$' -s 2 -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on -k 'regex:^k_grad(128|_hf)?$' -s 2 -c 1 \
     -o gpurun_out/prof_grad_${TAG} -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --e2e-steps 0 \
     > gpurun_out/ncu_grad_${TAG}.log 2>&1
 echo "ncu grad rc=$?" >> gpurun_out/ncu_grad_${TAG}.log
