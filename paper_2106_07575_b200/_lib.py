@@ -11,7 +11,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libptyger.so")
+# PTYGER_LIB: an alternative build of the same library (A/B experiments); default: the in-tree build
+LIB_PATH = os.environ.get("PTYGER_LIB") or os.path.join(_HERE, "libptyger.so")
 
 PTYGER_OK = 0
 STATUS = {0: "OK", 2: "E_ARG", 3: "E_DATA", 4: "E_NUMERIC", 5: "E_CUDA", 6: "E_NCCL", 7: "E_OOM", 8: "E_STATE"}
