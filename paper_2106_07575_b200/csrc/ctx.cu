@@ -142,6 +142,8 @@ struct ptyger_ctx {
     float last_ms = 0.f;
     int grid_fr = 0, grid_el = 0;
     bool hf = false;     // N = 128 half-frame cluster kernels (kernels_hf128.cu)
+    bool c256 = false;   // N = 256 cluster-of-four LS kernel (kernels_c256.cu)
+    bool c256g = false;  // ... and the cluster-of-four GRAD kernel (opt-in: slower than the slot kernel)
     int parts_ls = 0;    // per-CTA partial rows written by the LS pass-0 frame kernel
     int m_host = 0;
     int64_t launches_per_iter = 0, last_launches = 0;
@@ -211,6 +213,8 @@ static int enqueue_iteration(ptyger_ctx* c, int p, std::string& err, int64_t& la
     // GRAD stage (Alg.1 648-649)
     if (c->hf) {
         LK(launch_grad_hf(g, c->u, c->v, c->d, c->probe_s, c->st, eps, s));
+    } else if (c->c256g) {
+        LK(launch_grad_c256(g, c->u, c->v, c->d, c->probe_s, c->st, eps, s));
     } else {
         LK(launch_grad(g, c->u, c->v, c->d, c->probe, c->probe_s, c->st, eps, c->grid_fr, s));
     }
@@ -257,6 +261,8 @@ static int enqueue_iteration(ptyger_ctx* c, int p, std::string& err, int64_t& la
         LK(launch_fwd(g, c->eta, c->probe, c->pos, c->order, nullptr, c->v, c->part_fr, c->grid_fr, (float)sc.eps, s));
     } else if (c->hf) {
         LK(launch_ls_hf(g, c->eta, c->probe_s, c->pos, c->order, c->u, c->v, c->d, sc, c->part_fr, c->st, s));
+    } else if (c->c256) {
+        LK(launch_ls_c256(g, c->eta, c->probe_s, c->pos, c->order, c->u, c->v, c->d, sc, c->part_fr, c->st, s));
     } else {
         LK(launch_ls(g, c->eta, c->probe, c->probe_s, c->pos, c->order, c->u, c->v, c->d, sc, c->part_fr, c->grid_fr, c->st, s));
     }
@@ -533,7 +539,12 @@ static ptyger_status init_impl(ptyger_ctx* c, const float* object, const float* 
     c->band_grid = c->sms * 2;
     AL(c->part_adj, double, ((int64_t)c->ntx * c->nty + 2 * c->band_grid) * NDY);
     c->hf = N == 128 && !c->subpx && getenv("PTYGER_HF") && atoi(getenv("PTYGER_HF")) == 1;   // opt-in (r1_history)
-    c->parts_ls = c->hf ? hf_ls_parts(nl) : c->grid_fr;
+    // N = 256: the LS pass runs on clusters of four CTAs (large config: 96.7 -> 71.6 ms) unless
+    // PTYGER_N256_SLOT=1; the GRAD pass keeps the v-slot transpose kernel (51 ms; its cluster version
+    // measured 63.7 ms), the cluster one is selectable with PTYGER_N256_GRAD_C=1
+    c->c256 = N == 256 && !(getenv("PTYGER_N256_SLOT") && atoi(getenv("PTYGER_N256_SLOT")) == 1);
+    c->c256g = c->c256 && getenv("PTYGER_N256_GRAD_C") && atoi(getenv("PTYGER_N256_GRAD_C")) == 1;
+    c->parts_ls = c->hf ? hf_ls_parts(nl) : c->c256 ? c256_ls_parts(nl) : c->grid_fr;
     if (c->parts_ls <= 0) {
         err = "half-frame kernel setup failed";
         return PTYGER_E_CUDA;

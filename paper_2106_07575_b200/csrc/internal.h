@@ -121,6 +121,13 @@ int launch_ls_hf(const Geometry& g, const float2* eta, const float2* probe_s, co
                  cudaStream_t s);
 int launch_grad_hf(const Geometry& g, float2* u, float2* v, const float* d, const float2* probe_s,
                    const DevState* st, float eps, cudaStream_t s);
+// cluster-of-four frame kernels for N = 256 (kernels_c256.cu); probe_s = probe / N
+int c256_ls_parts(int64_t nfr);
+int launch_ls_c256(const Geometry& g, const float2* eta, const float2* probe_s, const int2* pos, const int* order,
+                   const float2* u, float2* v, const float* d, const SolverCfg& c, double* part, const DevState* st,
+                   cudaStream_t s);
+int launch_grad_c256(const Geometry& g, float2* u, float2* v, const float* d, const float2* probe_s,
+                     const DevState* st, float eps, cudaStream_t s);
 int launch_scale_c(const float2* in, float2* out, int64_t n, float s, cudaStream_t st);
 int launch_band_add(float2* gcur, const float2* recv, int64_t row_lo, int64_t rows, int64_t W,
                     const float2* gprev, const float2* eta, int64_t own_lo, int64_t own_hi,

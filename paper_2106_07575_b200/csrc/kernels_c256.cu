@@ -1,0 +1,369 @@
+// Frame kernels for N = 256 on a CLUSTER OF FOUR CTAs per frame (distributed shared memory).
+//
+// A 256 x 256 complex64 frame is 512 KB, more than one SM's shared memory.  The slot kernels
+// (kernels_n256.cu) transpose through the frame's own v slot in HBM, which at the large config
+// costs +34 % DRAM traffic in k_grad (the 76 MB of in-flight intermediates overflow L2) and leaves
+// both passes latency-bound.  Here the four CTAs of a cluster (4 SMs, 4 x 218 KB of shared memory)
+// hold the frame between the two passes:
+//   * CTA r transforms rows [64 r, 64 r + 64) (row pass, inputs straight from global memory);
+//   * output column k of a row belongs to CTA k / 64: each row's 256 outputs are stored straight
+//     into the owning CTA's 256 x 64 column block (st.shared::cluster, 3/4 of them remote), so the
+//     2-D transpose is the DSMEM exchange (96 KB out of every CTA per frame);
+//   * CTA r runs the column pass and the fused epilogue on its 64 columns locally.
+// The arithmetic is that of the other FFT paths (fft.cuh: radix-16 in registers x radix-16
+// across 16 threads per dimension, fp64-built twiddles, paired-FP32 complex arithmetic); the
+// unitary 1/N rides on the prescaled probe (probe_s = p / N).
+//
+//   k_grad_c256  GRAD stage frame part (Alg.1 648-649): u <- u + gamma v, r = u - d/u^*,
+//                y = conj(p) F^H r into v's slot
+//   k_ls_c256    LS pass 0 (Alg.1 659-668, Eq.7 on the Eq.2 objective): v = F(p eta[window]) and
+//                the screening partials of the pass-0 trials against (u, d)
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "dev.cuh"
+
+namespace pty {
+
+namespace c256 {
+constexpr int N = 256, R = 16, T = 16, NT = 512, NW = NT / 32, CL = 4;
+constexpr int QC = N / CL;                  // 64 columns owned per CTA
+constexpr int QR = N / CL;                  // 64 rows transformed per CTA
+constexpr int SROWS = NT / T;               // 32 rows per row-pass round
+constexpr int SLD = N + 8;                  // row-scratch stride (complex)
+constexpr size_t BLK_BYTES = (size_t)N * QC * 8;           // 131072
+constexpr size_t SCR_OFF = BLK_BYTES;
+constexpr size_t TW_OFF = SCR_OFF + (size_t)SROWS * SLD * 8; // + 67584
+constexpr size_t DYN_BYTES = TW_OFF + (size_t)N * 8;         // 200704
+}  // namespace c256
+
+__device__ __forceinline__ uint32_t c4_mapa(uint32_t saddr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void c4_st2(uint32_t caddr, float2 v) {
+    asm volatile("st.shared::cluster.v2.f32 [%0], {%1, %2};" ::"r"(caddr), "f"(v.x), "f"(v.y) : "memory");
+}
+__device__ __forceinline__ uint32_t c4_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t c4_id() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t c4_count() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void c4_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
+__device__ __forceinline__ void c4_arrive_relaxed() {
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void c4_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+
+// Row pass of one row (16 sub-threads t of one row, consecutive lanes): x[n1] = input at column
+// 16 n1 + t.  After the transform x[k2] is output column t + 16 k2, owned by CTA k2 / 4 at local
+// column t + 16 (k2 % 4).  `first` (round 0): wait until every peer has released its block.
+template <bool INV>
+__device__ __forceinline__ void c4_row(float2 (&x)[16], float2* srow, int t, const float2* tw, int row,
+                                       const uint32_t (&cb)[4], bool first) {
+    using namespace c256;
+    row_fft_regs<N, INV>(x, srow, t, tw);
+    if (first) c4_wait();
+#pragma unroll
+    for (int k2 = 0; k2 < T; ++k2)
+        c4_st2(cb[k2 >> 2] + (uint32_t)(row * QC + t + R * (k2 & 3)) * 8u, x[k2]);
+}
+
+// Column pass on the local 256 x 64 block: phase 1 for local column cl, sub-thread t (= warp).
+template <bool INV>
+__device__ __forceinline__ void c4_col1(float2* blk, int cl, int t, const float2* tw) {
+    using namespace c256;
+    float2 x[R];
+#pragma unroll
+    for (int n1 = 0; n1 < R; ++n1) x[n1] = blk[(T * n1 + t) * QC + cl];
+    DFT<R, INV>::run(x);
+#pragma unroll
+    for (int k1 = 1; k1 < R; ++k1) x[k1] = twmul<INV>(x[k1], tw[t * k1]);
+#pragma unroll
+    for (int k1 = 0; k1 < R; ++k1) blk[(T * k1 + t) * QC + cl] = x[k1];
+}
+
+// phase 2: X[k2] = output row t + 16 k2 of local column cl (k1 = t, inputs rows 16 t + n2)
+template <bool INV>
+__device__ __forceinline__ void c4_col2(const float2* blk, int cl, int t, float2 (&X)[16]) {
+    using namespace c256;
+#pragma unroll
+    for (int n2 = 0; n2 < T; ++n2) X[n2] = blk[(T * t + n2) * QC + cl];
+    DFT<T, INV>::run(X);
+}
+
+// ----------------------------------------------------------------------------------------
+// k_grad_c256
+// ----------------------------------------------------------------------------------------
+__global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(512, 1)
+    k_grad_c256(Geometry g, float2* __restrict__ u, float2* __restrict__ v, const float* __restrict__ d,
+                const float2* __restrict__ probe_s, const DevState* __restrict__ st, float eps) {
+    using namespace c256;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    float2* blk = reinterpret_cast<float2*>(smraw);
+    float2* scr = reinterpret_cast<float2*>(smraw + SCR_OFF);
+    float2* tw = reinterpret_cast<float2*>(smraw + TW_OFF);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t rank = c4_rank();
+    const int64_t cid = c4_id(), ncl = c4_count();
+    const bool err = st->numeric_error != 0;
+    ktime_start(st, 0);
+    const float gam = (float)st->gamma;
+    const bool upd = gam != 0.0f;
+    build_twiddles<N>(tw);
+    uint32_t cb[4];
+    {
+        const uint32_t sb = static_cast<uint32_t>(__cvta_generic_to_shared(blk));
+#pragma unroll
+        for (int q = 0; q < 4; ++q) cb[q] = c4_mapa(sb, q);
+    }
+    __syncthreads();
+    c4_arrive_relaxed();   // "my block is free" for the first frame
+    const int64_t nfr = err ? 0 : g.n_local;
+    const float eps2 = eps * eps;
+    const int rt = tid & 15, rrow = tid >> 4;
+    for (int64_t j = cid; j < nfr; j += ncl) {
+#pragma unroll 1
+        for (int rd = 0; rd < QR / SROWS; ++rd) {
+            const int row = (int)rank * QR + rd * SROWS + rrow;
+            const int64_t b0 = j * (N * N) + (int64_t)row * N + rt;
+            float2 uu[R];
+            float dd[R];
+#pragma unroll
+            for (int n1 = 0; n1 < R; ++n1) {
+                uu[n1] = u[b0 + T * n1];
+                dd[n1] = __ldg(d + b0 + T * n1);
+            }
+            if (upd) {
+                float2 vv[R];
+#pragma unroll
+                for (int n1 = 0; n1 < R; ++n1) vv[n1] = v[b0 + T * n1];
+#pragma unroll
+                for (int n1 = 0; n1 < R; ++n1) {
+                    uu[n1] = make_float2(fmaf(gam, vv[n1].x, uu[n1].x), fmaf(gam, vv[n1].y, uu[n1].y));
+                    u[b0 + T * n1] = uu[n1];
+                }
+            }
+            float2 x[R];
+#pragma unroll
+            for (int n1 = 0; n1 < R; ++n1) x[n1] = residual(uu[n1], dd[n1], eps2, g.est);
+            c4_row<true>(x, scr + rrow * SLD, rt, tw, row, cb, rd == 0);
+        }
+        c4_arrive();
+        c4_wait();   // all four quarters of every row have landed
+#pragma unroll 1
+        for (int rd = 0; rd < QC / 32; ++rd) c4_col1<true>(blk, rd * 32 + lane, warp, tw);
+        __syncthreads();
+#pragma unroll 1
+        for (int rd = 0; rd < QC / 32; ++rd) {
+            const int cl = rd * 32 + lane;
+            const int c = (int)rank * QC + cl;
+            float2 X[R];
+            c4_col2<true>(blk, cl, warp, X);
+#pragma unroll
+            for (int k2 = 0; k2 < T; ++k2) {
+                const int k = warp + R * k2;
+                v[j * (N * N) + (int64_t)k * N + c] = cconjmul(ldg2(probe_s + k * N + c), X[k2]);
+            }
+        }
+        __syncthreads();
+        c4_arrive_relaxed();
+    }
+    c4_wait();
+    ktime_end(st, 0);
+}
+
+// ----------------------------------------------------------------------------------------
+// k_ls_c256 (screening contract: k_ls<N> in kernels_frame.cu)
+// ----------------------------------------------------------------------------------------
+__global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(512, 1)
+    k_ls_c256(Geometry g, const float2* __restrict__ eta, const float2* __restrict__ probe_s,
+              const int2* __restrict__ pos, const int* __restrict__ order, const float2* __restrict__ u,
+              float2* __restrict__ v, const float* __restrict__ d, SolverCfg cfg, double* __restrict__ part,
+              const DevState* __restrict__ st) {
+    using namespace c256;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    float2* blk = reinterpret_cast<float2*>(smraw);
+    float2* scr = reinterpret_cast<float2*>(smraw + SCR_OFF);
+    float2* tw = reinterpret_cast<float2*>(smraw + TW_OFF);
+    __shared__ double sred[NW][KC];
+    __shared__ double smom[NW][4];
+    __shared__ float sgam[KC];
+    __shared__ LsWarpQ wq[NW];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t rank = c4_rank();
+    const int64_t cid = c4_id(), ncl = c4_count();
+    const bool err = st->numeric_error != 0;
+    int base, cnt;
+    ls_pass_range(0, st->keff, cfg, base, cnt);
+    ktime_start(st, 1);
+    build_twiddles<N>(tw);
+    if (tid < KC) sgam[tid] = (float)trial_gamma(cfg.gamma0, cfg.tau, base + tid);
+    uint32_t cb[4];
+    {
+        const uint32_t sb = static_cast<uint32_t>(__cvta_generic_to_shared(blk));
+#pragma unroll
+        for (int q = 0; q < 4; ++q) cb[q] = c4_mapa(sb, q);
+    }
+    __syncthreads();
+    c4_arrive_relaxed();
+    const int64_t nfr = err ? 0 : g.n_local;
+    const float eps2 = (float)(cfg.eps * cfg.eps);
+    double tot = 0.0;
+    double mom[4] = {0.0, 0.0, 0.0, 0.0};
+    const int rt = tid & 15, rrow = tid >> 4;
+    for (int64_t i = cid; i < nfr; i += ncl) {
+        const int j = order[i];
+        const int2 s = pos[j];
+        // ---- row pass: rows 64 rank + 32 rd + rrow of (p / N) * eta[window]
+        {
+            float2 xa[R], xb[R];
+            const int row0 = (int)rank * QR + rrow, row1 = row0 + SROWS;
+            window_row<R, T>(eta, g, s, j, row0, rt, probe_s + row0 * N + rt, xa);
+            window_row<R, T>(eta, g, s, j, row1, rt, probe_s + row1 * N + rt, xb);
+            c4_row<false>(xa, scr + rrow * SLD, rt, tw, row0, cb, true);
+            c4_row<false>(xb, scr + rrow * SLD, rt, tw, row1, cb, false);
+        }
+        c4_arrive();
+        c4_wait();
+#pragma unroll 1
+        for (int rd = 0; rd < QC / 32; ++rd) c4_col1<false>(blk, rd * 32 + lane, warp, tw);
+        __syncthreads();
+#pragma unroll 1
+        for (int rd = 0; rd < QC / 32; ++rd) {
+            const int cl = rd * 32 + lane;
+            float2* mine = blk + (T * warp) * QC + cl;   // the thread's own phase-2 rows 16 t + k2
+            {
+                float2 X[R];
+                c4_col2<false>(blk, cl, warp, X);
+#pragma unroll
+                for (int k2 = 0; k2 < T; ++k2) mine[k2 * QC] = X[k2];
+            }
+            float S[KC];
+            LsMom m;
+#pragma unroll
+            for (int k = 0; k < KC; ++k) S[k] = 0.f;
+            // element k2 of column c sits at frame row t + 16 k2: offset (t + 16 k2) N + c
+            const int64_t fb = (int64_t)j * (N * N) + (int64_t)warp * N + (int64_t)rank * QC + cl;
+            const float2* __restrict__ ub = u + fb;
+            const float* __restrict__ db = d + fb;
+            float2* __restrict__ vb = v + fb;
+            if (cnt > 0) trial_dispatch(cnt, cfg.est, [&]<int KT, bool LSE>() {
+                float gk[KT];
+#pragma unroll
+                for (int k = 0; k < KT; ++k) gk[k] = sgam[k];
+                LsQState qs;
+                float2 un[4];
+                float dn[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    un[e] = ub[e * R * N];
+                    dn[e] = __ldg(db + e * R * N);
+                }
+#pragma unroll 1
+                for (int gi = 0; gi < T / 4; ++gi) {
+                    const int go = gi * 4 * R * N;
+                    float2 uc[4];
+                    float dc[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        uc[e] = un[e];
+                        dc[e] = dn[e];
+                    }
+                    if (gi + 1 < T / 4) {
+                        const int gn = go + 4 * R * N;
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            un[e] = ub[gn + e * R * N];
+                            dn[e] = __ldg(db + gn + e * R * N);
+                        }
+                    }
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const float2 vv = mine[(gi * 4 + e) * QC];
+                        vb[go + e * R * N] = vv;
+                        ls_push<KT, LSE>(wq[warp], qs, uc[e], vv, dc[e], gk, eps2, S, m, lane);
+                    }
+                }
+                ls_flush<KT, LSE>(wq[warp], qs, gk, eps2, S, m, lane);
+            });
+            double dv[KC];
+#pragma unroll
+            for (int k = 0; k < KC; ++k) dv[k] = (double)S[k];
+            tot += warp_reduce_scatter<KC>(dv, lane);
+            mom[0] += (double)m.A;
+            mom[1] += (double)m.D;
+            mom[2] += (double)m.sa;
+            mom[3] += (double)m.sb;
+        }
+        __syncthreads();
+        c4_arrive_relaxed();
+    }
+    c4_wait();
+    ktime_end(st, 1);
+    ls_block_out<KC, NW>(tot, mom, sred, smom, part);
+}
+
+// ----------------------------------------------------------------------------------------
+// launchers: grid = 4 x (resident clusters, capped by the frame count)
+// ----------------------------------------------------------------------------------------
+template <typename K>
+static int c256_grid(K* kern, int slot, int64_t nfr) {
+    static int cached[2] = {0, 0};
+    if (cached[slot] == 0) {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c256::DYN_BYTES) !=
+            cudaSuccess)
+            return -1;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(4 * 148, 1, 1);
+        cfg.blockDim = dim3(c256::NT, 1, 1);
+        cfg.dynamicSmemBytes = c256::DYN_BYTES;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 4;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int ncl = 0;
+        if (cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg) != cudaSuccess || ncl <= 0) {
+            cudaGetLastError();
+            ncl = 148 / 4;
+        }
+        cached[slot] = ncl;
+    }
+    const int64_t ncl = nfr < cached[slot] ? (nfr > 0 ? nfr : 1) : cached[slot];
+    return (int)(4 * ncl);
+}
+
+int c256_ls_parts(int64_t nfr) { return c256_grid(k_ls_c256, 0, nfr); }
+
+int launch_ls_c256(const Geometry& g, const float2* eta, const float2* probe_s, const int2* pos, const int* order,
+                   const float2* u, float2* v, const float* d, const SolverCfg& c, double* part, const DevState* st,
+                   cudaStream_t s) {
+    const int grid = c256_grid(k_ls_c256, 0, g.n_local);
+    if (grid < 0) return -1;
+    k_ls_c256<<<grid, c256::NT, c256::DYN_BYTES, s>>>(g, eta, probe_s, pos, order, u, v, d, c, part, st);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+int launch_grad_c256(const Geometry& g, float2* u, float2* v, const float* d, const float2* probe_s,
+                     const DevState* st, float eps, cudaStream_t s) {
+    const int grid = c256_grid(k_grad_c256, 1, g.n_local);
+    if (grid < 0) return -1;
+    k_grad_c256<<<grid, c256::NT, c256::DYN_BYTES, s>>>(g, u, v, d, probe_s, st, eps);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+}  // namespace pty
