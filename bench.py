@@ -43,7 +43,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="paper", choices=["tiny", "small", "paper", "mid", "large", "view3d"])
+    ap.add_argument("--config", default="paper", choices=["tiny", "small", "paper", "mid", "large", "view3d", "l256p"])
     ap.add_argument("--views", type=int, default=0, help="view3d: number of views (default: all 64)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ls-batch", type=int, default=16)

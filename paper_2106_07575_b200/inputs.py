@@ -48,6 +48,8 @@ WORKLOADS = {
     "large": Workload("large", 8192, 8192, 256, 316, 25, 2, 3),
     "view3d": Workload("view3d", 2048, 2048, 128, 64, 30, 2, 4, views=64),
     "mid": Workload("mid", 1024, 1024, 64, 121, 8, 0, 5),
+    # N = 256 profiling stand-in for "large" (same frame size, step and density; 1/19 of the frames)
+    "l256p": Workload("l256p", 2048, 2048, 256, 72, 25, 2, 3),
 }
 
 
