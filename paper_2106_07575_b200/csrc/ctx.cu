@@ -279,12 +279,12 @@ static int enqueue_iteration(ptyger_ctx* c, int p, std::string& err, int64_t& la
             ++launches;
         }
         LK(launch_reduce(fused ? c->part_fr : c->part_el, fused ? c->parts_ls : c->grid_el, wscreen,
-                         &c->st->ls_pass[0], s));
+                         &c->st->ls_pass[0], s, c->st, pass == 0 ? 0 : 1, pass));
         ++launches;
         if (multi) NK(c->nc->AllReduce(&c->st->ls_pass[0], &c->st->ls_pass[0], LSW, ncclFloat64, ncclSum, c->comm, s));
         LK(launch_pick(c->st, sc, pass, 0, 0, s)); ++launches;
         LK(launch_lsx(g, c->u, c->v, c->d, sc, pass, true, c->part_el, c->grid_el, c->st, s)); ++launches;
-        LK(launch_reduce(c->part_el, c->grid_el, LSP, &c->st->ls_pass[0], s)); ++launches;
+        LK(launch_reduce(c->part_el, c->grid_el, LSP, &c->st->ls_pass[0], s, c->st, 2, pass)); ++launches;
         if (multi) NK(c->nc->AllReduce(&c->st->ls_pass[0], &c->st->ls_pass[0], KC, ncclFloat64, ncclSum, c->comm, s));
         LK(launch_pick(c->st, sc, pass, 1, pass == npass - 1, s)); ++launches;
     }

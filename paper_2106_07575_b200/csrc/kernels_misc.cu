@@ -191,22 +191,40 @@ __global__ void __launch_bounds__(256) k_band_add(float2* __restrict__ gcur, con
 // ----------------------------------------------------------------------------------------
 // Deterministic reduction of per-block partials: dst[w] = sum_b part[b*width + w].
 // ----------------------------------------------------------------------------------------
+// Fixed-order fp64 reduction of per-CTA partials (width <= LSW columns): thread i sums rows
+// i, i + 1024, ... of every column in registers, then each column is reduced by a fixed warp
+// butterfly and a fixed-order sum over the 32 warps, so the result is bitwise reproducible.  One
+// pass over the partials, two barriers.  mode 1: only while no trial is accepted (screening of an
+// extra LS pass); mode 2: only when the screening left pass `pass` undecided (its exact
+// re-evaluation).  A skipped reduction leaves dst untouched and the matching k_pick ignores it.
 __global__ void __launch_bounds__(1024) k_reduce(const double* __restrict__ part, int nblocks, int width,
-                                                 double* __restrict__ dst) {
-    __shared__ double sred[32];
-    for (int w = 0; w < width; ++w) {
-        double s = 0.0;
-        for (int b = threadIdx.x; b < nblocks; b += blockDim.x) s += part[(int64_t)b * width + w];
-        s = warp_sum(s);
-        const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
-        if (lane == 0) sred[wp] = s;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            double t = 0.0;
-            for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += sred[i];
-            dst[w] = t;
+                                                 double* __restrict__ dst, const DevState* __restrict__ st,
+                                                 int mode, int pass) {
+    if (mode == 1 && (st->accepted || st->numeric_error)) return;
+    if (mode == 2 && st->need_exact != pass + 1) return;
+    __shared__ double sred[32][LSW];
+    const int wp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double acc[LSW];
+#pragma unroll
+    for (int w = 0; w < LSW; ++w) acc[w] = 0.0;
+    for (int b = threadIdx.x; b < nblocks; b += blockDim.x) {
+        const double* row = part + (int64_t)b * width;
+#pragma unroll
+        for (int w = 0; w < LSW; ++w)
+            if (w < width) acc[w] += row[w];
+    }
+#pragma unroll
+    for (int w = 0; w < LSW; ++w) {
+        if (w < width) {
+            const double t = warp_sum(acc[w]);
+            if (lane == 0) sred[wp][w] = t;
         }
-        __syncthreads();
+    }
+    __syncthreads();
+    if ((int)threadIdx.x < width) {
+        double t = 0.0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += sred[i][threadIdx.x];
+        dst[threadIdx.x] = t;
     }
 }
 
@@ -580,8 +598,9 @@ int launch_scale_c(const float2* in, float2* out, int64_t n, float s, cudaStream
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
-int launch_reduce(const double* part, int nblocks, int width, double* dst, cudaStream_t s) {
-    k_reduce<<<1, 1024, 0, s>>>(part, nblocks, width, dst);
+int launch_reduce(const double* part, int nblocks, int width, double* dst, cudaStream_t s, const DevState* st,
+                  int mode, int pass) {
+    k_reduce<<<1, 1024, 0, s>>>(part, nblocks, width, dst, st, st ? mode : 0, pass);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
