@@ -67,6 +67,32 @@ __device__ __forceinline__ double warp_reduce_scatter(double (&v)[K], int lane) 
 
 __device__ __forceinline__ float2 ldg2(const float2* p) { return __ldg(p); }
 
+// L2 cache-policy hints (createpolicy + .L2::cache_hint): keep short-lived intermediates (the N = 256
+// slot transpose) resident, stream data that is read or written once per pass.
+__device__ __forceinline__ uint64_t l2_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t l2_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void st2_hint(float2* a, float2 v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;" ::"l"(a), "f"(v.x), "f"(v.y), "l"(pol) : "memory");
+}
+__device__ __forceinline__ float2 ld2_hint(const float2* a, uint64_t pol) {
+    float2 v;
+    asm volatile("ld.global.L2::cache_hint.v2.f32 {%0, %1}, [%2], %3;" : "=f"(v.x), "=f"(v.y) : "l"(a), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ float ld1_hint(const float* a, uint64_t pol) {
+    float v;
+    asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(a), "l"(pol));
+    return v;
+}
+
 // Frame-kernel timers (DevState::tk_*): thread 0 of every CTA marks its start / end with the
 // global nanosecond timer, so one launch's duration is max(end) - min(start) over its CTAs.
 // The timer words are the only DevState fields these kernels write (hence the const_cast).

@@ -72,6 +72,8 @@ __global__ void __launch_bounds__(512, 1) k_grad256(Geometry g, float2* __restri
     const bool upd = gam != 0.0f;
     const float eps2 = eps * eps, scale = 1.0f / (float)N;
     const int tid = threadIdx.x;
+    // streamed once: u, v, d reads and the u / y writes; reused within microseconds: the slot rows
+    const uint64_t pol_s = l2_evict_first(), pol_k = l2_evict_last();
     for (int64_t j = blockIdx.x; j < g.n_local; j += gridDim.x) {
         float2* vj = v + j * N * N;
         // pass 1: rows
@@ -83,17 +85,17 @@ __global__ void __launch_bounds__(512, 1) k_grad256(Geometry g, float2* __restri
             float dd[R];
 #pragma unroll
             for (int n1 = 0; n1 < R; ++n1) {
-                uu[n1] = u[base + T * n1];
-                dd[n1] = __ldg(d + base + T * n1);
+                uu[n1] = ld2_hint(u + base + T * n1, pol_s);
+                dd[n1] = ld1_hint(d + base + T * n1, pol_s);
             }
             if (upd) {
                 float2 vv[R];
 #pragma unroll
-                for (int n1 = 0; n1 < R; ++n1) vv[n1] = v[base + T * n1];
+                for (int n1 = 0; n1 < R; ++n1) vv[n1] = ld2_hint(v + base + T * n1, pol_s);
 #pragma unroll
                 for (int n1 = 0; n1 < R; ++n1) {
                     uu[n1] = make_float2(fmaf(gam, vv[n1].x, uu[n1].x), fmaf(gam, vv[n1].y, uu[n1].y));
-                    u[base + T * n1] = uu[n1];
+                    st2_hint(u + base + T * n1, uu[n1], pol_s);
                 }
             }
             float2 x[R];
@@ -105,7 +107,7 @@ __global__ void __launch_bounds__(512, 1) k_grad256(Geometry g, float2* __restri
             // x[k2] is column t + 16 k2; v of this row was consumed above, so the slot row is free
             float2* dst = vj + (int64_t)row * N + t;
 #pragma unroll
-            for (int k2 = 0; k2 < T; ++k2) dst[R * k2] = x[k2];
+            for (int k2 = 0; k2 < T; ++k2) st2_hint(dst + R * k2, x[k2], pol_k);
         }
         __syncthreads();
         // pass 2: columns, epilogue y = conj(p) X / N
@@ -118,7 +120,7 @@ __global__ void __launch_bounds__(512, 1) k_grad256(Geometry g, float2* __restri
 #pragma unroll
             for (int k2 = 0; k2 < T; ++k2) {
                 const int k = t + R * k2;
-                vj[(int64_t)k * N + c] = cscale(cconjmul(ldg2(probe + k * N + c), X[k2]), scale);
+                st2_hint(vj + (int64_t)k * N + c, cscale(cconjmul(ldg2(probe + k * N + c), X[k2]), scale), pol_s);
             }
         }
         __syncthreads();
