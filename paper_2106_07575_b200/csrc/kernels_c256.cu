@@ -264,12 +264,13 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(512, 1)
 #pragma unroll
                 for (int k = 0; k < KT; ++k) gk[k] = sgam[k];
                 LsQState qs;
+                const uint64_t pol = l2_evict_first();   // u, d read once, v written once per pass
                 float2 un[4];
                 float dn[4];
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
-                    un[e] = ub[e * R * N];
-                    dn[e] = __ldg(db + e * R * N);
+                    un[e] = ld2_hint(ub + e * R * N, pol);
+                    dn[e] = ld1_hint(db + e * R * N, pol);
                 }
 #pragma unroll 1
                 for (int gi = 0; gi < T / 4; ++gi) {
@@ -285,14 +286,14 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(512, 1)
                         const int gn = go + 4 * R * N;
 #pragma unroll
                         for (int e = 0; e < 4; ++e) {
-                            un[e] = ub[gn + e * R * N];
-                            dn[e] = __ldg(db + gn + e * R * N);
+                            un[e] = ld2_hint(ub + gn + e * R * N, pol);
+                            dn[e] = ld1_hint(db + gn + e * R * N, pol);
                         }
                     }
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
                         const float2 vv = mine[(gi * 4 + e) * QC];
-                        vb[go + e * R * N] = vv;
+                        st2_hint(vb + go + e * R * N, vv, pol);
                         ls_push<KT, LSE>(wq[warp], qs, uc[e], vv, dc[e], gk, eps2, S, m, lane);
                     }
                 }
