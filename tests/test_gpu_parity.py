@@ -363,10 +363,11 @@ def test_view_batch_equals_independent_views(L):
 
 # ------------------------------------------------------------------ alternative N = 128 kernels
 
-@pytest.mark.parametrize("env", ["PTYGER_HF", "PTYGER_GRAD_TMA"])
+@pytest.mark.parametrize("env", ["PTYGER_HF", "PTYGER_GRAD_TMA", "PTYGER_LS_SPLIT"])
 def test_alternative_n128_kernels(L, env, monkeypatch):
-    """The opt-in N = 128 kernels (half-frame cluster pair with a DSMEM transpose, PTYGER_HF=1;
-    TMA-ring k_grad128, PTYGER_GRAD_TMA=1) meet the same teacher-forced tolerance as the default."""
+    """The opt-in N = 128 paths (half-frame cluster pair with a DSMEM transpose, PTYGER_HF=1;
+    TMA-ring k_grad128, PTYGER_GRAD_TMA=1; transform-only frame kernel + elementwise screening
+    pass, PTYGER_LS_SPLIT=1) meet the same teacher-forced tolerance as the default."""
     monkeypatch.setenv(env, "1")
     psi_true, p, scan, d = get_fixture("n128")
     d64 = d.astype(np.float64)
