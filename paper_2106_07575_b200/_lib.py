@@ -289,11 +289,12 @@ class ViewBatch:
         return sum(v.last_iterate_ms() for v in self.views)
 
     def kernel_times(self, reset: bool = True):
-        """{"k_grad": (total ms, launches), "k_ls": (total ms, launches)} since the last reset."""
-        ms = np.zeros(2, np.float64)
-        cnt = np.zeros(2, np.int32)
-        _check(lib.ptyger_kernel_times(self.ctx, ms.ctypes.data, cnt.ctypes.data, int(reset)), self.ctx)
-        return {"k_grad": (float(ms[0]), int(cnt[0])), "k_ls": (float(ms[1]), int(cnt[1]))}
+        """Summed over the views: {"k_grad": (total ms, launches), "k_ls": (total ms, launches)}."""
+        out = {"k_grad": (0.0, 0), "k_ls": (0.0, 0)}
+        for v in self.views:
+            for k, (ms, n) in v.kernel_times(reset).items():
+                out[k] = (out[k][0] + ms, out[k][1] + n)
+        return out
 
     def kernel_launches(self) -> int:
         return sum(v.kernel_launches() for v in self.views)

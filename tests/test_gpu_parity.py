@@ -408,3 +408,20 @@ def test_alternative_n256_kernels(L, env, monkeypatch):
         refs = [O.ls_delta(u_ref, v_ref, d64, 0.5 ** k) for k in range(tr["shrinks"] + 1)]
         assert refs[-1] <= 0 and all(r > 0 for r in refs[:-1])
     pt.close()
+
+
+def test_kernel_timers_cover_every_launch(L):
+    """ptyger_kernel_times: one GRAD and one LS pass-0 launch per iteration, positive durations that
+    fit inside the iteration time, and reset semantics."""
+    psi_true, p, scan, d = get_fixture("n128")
+    pt = L.Ptyger(np.ones_like(psi_true), p, scan, d)
+    pt.iterate(1)
+    pt.kernel_times(reset=True)
+    pt.iterate(4)
+    it_ms = pt.last_iterate_ms()
+    kt = pt.kernel_times(reset=True)
+    assert kt["k_grad"][1] == 4 and kt["k_ls"][1] == 4
+    assert 0 < kt["k_grad"][0] and 0 < kt["k_ls"][0]
+    assert kt["k_grad"][0] + kt["k_ls"][0] <= it_ms * 1.05
+    assert pt.kernel_times(reset=True) == {"k_grad": (0.0, 0), "k_ls": (0.0, 0)}
+    pt.close()
