@@ -308,6 +308,7 @@ def main():
         psi_h = torch.ones((w.H, w.W), dtype=torch.complex64).pin_memory()
         p_h = torch.from_numpy(p.astype(np.complex64)).pin_memory()
         del pt
+        obj_pin = torch.empty((w.H, w.W), dtype=torch.complex64).pin_memory().numpy()
         torch.cuda.synchronize()
         t_list = []
         for _ in range(args.e2e_steps):
@@ -315,7 +316,7 @@ def main():
             t0 = time.perf_counter()
             q = L.Ptyger(psi_h, p_h, scan, d_host, config=L.default_config(ls_batch=args.ls_batch, device=local))
             q.iterate(1, traces=False)
-            out = q.get_object()
+            out = q.get_object(obj_pin)
             t_list.append(time.perf_counter() - t0)
             q.close()
         tm = float(np.median(t_list))

@@ -216,8 +216,12 @@ class Ptyger:
     def _obj_buf(self):
         return np.empty((self.H, self.W), np.complex64)
 
-    def get_object(self):
-        out = self._obj_buf()
+    def get_object(self, out=None):
+        """psi_m as (H, W) complex64; `out` may be a caller buffer (e.g. a pinned-memory view, which
+        makes the device-to-host copy run at full link speed)."""
+        if out is None:
+            out = self._obj_buf()
+        assert out.dtype == np.complex64 and out.shape == (self.H, self.W) and out.flags["C_CONTIGUOUS"]
         _check(lib.ptyger_get_object(self.ctx, out.ctypes.data), self.ctx)
         return out
 

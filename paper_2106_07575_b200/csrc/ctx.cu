@@ -295,7 +295,21 @@ static int enqueue_iteration(ptyger_ctx* c, int p, std::string& err, int64_t& la
     return 0;
 }
 
+static int build_graphs_on(ptyger_ctx* c, std::string& err);
+
+// Captured on a private stream, so the context stream may still be busy with the uploads and
+// the d validation while the graphs are built (the graphs are launched on c->stream later).
 static int build_graphs(ptyger_ctx* c, std::string& err) {
+    cudaStream_t cap = nullptr, own = c->stream;
+    CK(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+    c->stream = cap;
+    const int rc = build_graphs_on(c, err);
+    c->stream = own;
+    cudaStreamDestroy(cap);
+    return rc;
+}
+
+static int build_graphs_on(ptyger_ctx* c, std::string& err) {
     for (int p = 0; p < 2; ++p) {
         if (c->graph[p]) {
             cudaGraphExecDestroy(c->graph[p]);
@@ -486,11 +500,8 @@ static ptyger_status init_impl(ptyger_ctx* c, const float* object, const float* 
         sub[2 * i] = scan[2 * j];
         sub[2 * i + 1] = scan[2 * j + 1];
     }
-    std::vector<int64_t> ord64;
-    canonical_order(sub.data(), nl, N, ord64);
-    std::vector<int32_t> ord(ord64.begin(), ord64.end());
-    std::vector<int32_t> tptr, ent;
-    build_tiles(lpos, ord, foot, c->SH, W, c->ntx, c->nty, tptr, ent);
+    // canonical order and tile lists are built on the host AFTER the big uploads are issued (below)
+    std::vector<int32_t> ord, tptr, ent;
 
     // ---- device ----
     int ndev = 0;
@@ -525,19 +536,23 @@ static ptyger_status init_impl(ptyger_ctx* c, const float* object, const float* 
     AL(c->g[0], float2, obj);
     AL(c->g[1], float2, obj);
     AL(c->eta, float2, obj);
-    AL(c->u, float2, nl * NN);
-    AL(c->v, float2, nl * NN);
-    AL(c->d, float, nl * NN);
+    // u is written by k_fwd, d by the upload, v by the first LS pass before any read: no zero fill
+#define ALN(ptr, T, cnt)                                       \
+    do {                                                       \
+        ptr = dalloc<T>((size_t)(cnt), err, false);            \
+        if (!ptr) return PTYGER_E_OOM;                         \
+    } while (0)
+    ALN(c->u, float2, nl * NN);
+    ALN(c->v, float2, nl * NN);
+    ALN(c->d, float, nl * NN);
+#undef ALN
     AL(c->probe, float2, NN);
     AL(c->pos, int2, nl);
     AL(c->order, int, nl);
     if (c->subpx) AL(c->frac, float2, nl);
-    AL(c->tile_ptr, int, tptr.size());
-    AL(c->entries, int, ent.size());
     c->grid_fr = (int)std::max<int64_t>(1, std::min<int64_t>(c->sms, nl));
     c->grid_el = c->sms * 8;
     c->band_grid = c->sms * 2;
-    AL(c->part_adj, double, ((int64_t)c->ntx * c->nty + 2 * c->band_grid) * NDY);
     c->hf = N == 128 && !c->subpx && getenv("PTYGER_HF") && atoi(getenv("PTYGER_HF")) == 1;   // opt-in (r1_history)
     // N = 256: the LS pass runs on clusters of four CTAs (large config: 96.7 -> 71.6 ms) unless
     // PTYGER_N256_SLOT=1; the GRAD pass keeps the v-slot transpose kernel (51 ms; its cluster version
@@ -559,44 +574,72 @@ static ptyger_status init_impl(ptyger_ctx* c, const float* object, const float* 
     if (cfg.world > 1) AL(c->full, float2, H * W);
 #undef AL
     CK(cudaStreamSynchronize(0));  // pool allocations and zero fills (legacy stream) are done
-    CK(cudaMemcpy(c->psi, object + 2 * c->st_lo * W, sizeof(float2) * obj, cudaMemcpyDefault));
-    CK(cudaMemcpy(c->probe, probe, sizeof(float2) * NN, cudaMemcpyDefault));
-    // probe / N (exact: N is a power of two) carries the unitary FFT scale of the HF kernels
-    LK(launch_scale_c(c->probe, c->probe_s, NN, 1.0f / (float)N, 0));
-    CK(cudaStreamSynchronize(0));
-    // d: contiguous runs of local frames
+    // Uploads are asynchronous on the context stream (from pinned host memory the DMA of d overlaps
+    // the graph capture below; pageable sources are staged before each call returns, so the host
+    // vectors below may go out of scope).  d first: contiguous runs of local frames.
     for (int64_t i = 0; i < nl;) {
         int64_t k = i;
         while (k + 1 < nl && c->local_global[k + 1] == c->local_global[k] + 1) ++k;
         const int64_t j0 = c->local_global[i];
-        CK(cudaMemcpy(c->d + i * NN, intensities + j0 * NN, sizeof(float) * NN * (k - i + 1), cudaMemcpyDefault));
+        CK(cudaMemcpyAsync(c->d + i * NN, intensities + j0 * NN, sizeof(float) * NN * (k - i + 1), cudaMemcpyDefault,
+                           c->stream));
         i = k + 1;
+    }
+    CK(cudaMemcpyAsync(c->psi, object + 2 * c->st_lo * W, sizeof(float2) * obj, cudaMemcpyDefault, c->stream));
+    CK(cudaMemcpyAsync(c->probe, probe, sizeof(float2) * NN, cudaMemcpyDefault, c->stream));
+    // probe / N (exact: N is a power of two) carries the unitary FFT scale of the frame kernels
+    LK(launch_scale_c(c->probe, c->probe_s, NN, 1.0f / (float)N, c->stream));
+    // host work while the DMA runs: canonical processing order and the tile -> frame lists
+    {
+        std::vector<int64_t> ord64;
+        canonical_order(sub.data(), nl, N, ord64);
+        ord.assign(ord64.begin(), ord64.end());
+        build_tiles(lpos, ord, foot, c->SH, W, c->ntx, c->nty, tptr, ent);
+        c->tile_ptr = dalloc<int>(tptr.size(), err, false);
+        c->entries = dalloc<int>(ent.size(), err, false);
+        if (!c->tile_ptr || !c->entries) return PTYGER_E_OOM;
+        c->part_adj = dalloc<double>(((int64_t)c->ntx * c->nty + 2 * c->band_grid) * NDY, err);
+        if (!c->part_adj) return PTYGER_E_OOM;
+        CK(cudaStreamSynchronize(0));   // the pool allocations above (legacy stream) are done
     }
     std::vector<int2> p2(nl);
     for (int64_t i = 0; i < nl; ++i) p2[i] = make_int2(lpos[2 * i], lpos[2 * i + 1]);
-    CK(cudaMemcpy(c->pos, p2.data(), sizeof(int2) * nl, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(c->order, ord.data(), sizeof(int) * nl, cudaMemcpyHostToDevice));
+    CK(cudaMemcpyAsync(c->pos, p2.data(), sizeof(int2) * nl, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->order, ord.data(), sizeof(int) * nl, cudaMemcpyHostToDevice, c->stream));
+    std::vector<float2> fl;
     if (c->subpx) {
-        std::vector<float2> fl(nl);
+        fl.resize(nl);
         for (int64_t i = 0; i < nl; ++i) {
             const int64_t j = c->local_global[i];
             fl[i] = make_float2(fr[2 * j], fr[2 * j + 1]);
         }
-        CK(cudaMemcpy(c->frac, fl.data(), sizeof(float2) * nl, cudaMemcpyHostToDevice));
+        CK(cudaMemcpyAsync(c->frac, fl.data(), sizeof(float2) * nl, cudaMemcpyHostToDevice, c->stream));
         c->geo.frac = c->frac;
     }
-    CK(cudaMemcpy(c->tile_ptr, tptr.data(), sizeof(int) * tptr.size(), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(c->entries, ent.data(), sizeof(int) * ent.size(), cudaMemcpyHostToDevice));
-    // validate d on the device
+    CK(cudaMemcpyAsync(c->tile_ptr, tptr.data(), sizeof(int) * tptr.size(), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->entries, ent.data(), sizeof(int) * ent.size(), cudaMemcpyHostToDevice, c->stream));
+    // validate d on the device (result read after the graph capture)
+    unsigned long long* bad = dalloc<unsigned long long>(1, err, false);
+    if (!bad) return PTYGER_E_OOM;
     {
-        unsigned long long* bad = dalloc<unsigned long long>(1, err, false);
-        if (!bad) return PTYGER_E_OOM;
         const unsigned long long init = ~0ull;
-        CK(cudaMemcpy(bad, &init, sizeof(init), cudaMemcpyHostToDevice));
+        CK(cudaMemcpyAsync(bad, &init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
         LK(launch_validate_d(c->d, nl * NN, NN, bad, c->stream));
+    }
+    DevState hs;
+    std::memset(&hs, 0, sizeof(hs));
+    hs.tk_start[0] = hs.tk_start[1] = ~0ull;   // disarmed frame-kernel timers
+    CK(cudaMemcpyAsync(c->st, &hs, sizeof(hs), cudaMemcpyHostToDevice, c->stream));
+    int rc2 = build_graphs(c, err);   // host-side capture + instantiation overlaps the uploads
+    if (rc2) {
+        cudaStreamSynchronize(c->stream);
+        cudaFreeAsync(bad, 0);
+        return (ptyger_status)rc2;
+    }
+    {
         unsigned long long hb = 0;
+        CK(cudaMemcpyAsync(&hb, bad, sizeof(hb), cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
-        CK(cudaMemcpy(&hb, bad, sizeof(hb), cudaMemcpyDeviceToHost));
         cudaFreeAsync(bad, 0);
         if (hb != ~0ull) {
             err = "intensities: frame " + std::to_string(c->local_global[(int64_t)hb]) +
@@ -605,13 +648,7 @@ static ptyger_status init_impl(ptyger_ctx* c, const float* object, const float* 
         }
     }
     // F(psi_0), u_0
-    DevState hs;
-    std::memset(&hs, 0, sizeof(hs));
-    hs.tk_start[0] = hs.tk_start[1] = ~0ull;   // disarmed frame-kernel timers
-    CK(cudaMemcpy(c->st, &hs, sizeof(hs), cudaMemcpyHostToDevice));
-    int rc2 = run_forward(c, err);
-    if (rc2) return (ptyger_status)rc2;
-    rc2 = build_graphs(c, err);
+    rc2 = run_forward(c, err);
     if (rc2) return (ptyger_status)rc2;
     return PTYGER_OK;
 }
