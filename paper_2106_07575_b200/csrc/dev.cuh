@@ -66,6 +66,17 @@ __device__ __forceinline__ double warp_reduce_scatter(double (&v)[K], int lane) 
 }
 
 __device__ __forceinline__ float2 ldg2(const float2* p) { return __ldg(p); }
+// streamed reads that should not displace the frame-invariant probe / window data from L1
+__device__ __forceinline__ float2 ldg2_na(const float2* p) {
+    float2 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f32 {%0, %1}, [%2];" : "=f"(r.x), "=f"(r.y) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ float ldg1_na(const float* p) {
+    float r;
+    asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(r) : "l"(p));
+    return r;
+}
 
 // L2 cache-policy hints (createpolicy + .L2::cache_hint): keep short-lived intermediates (the N = 256
 // slot transpose) resident, stream data that is read or written once per pass.

@@ -317,8 +317,8 @@ __global__ void __launch_bounds__(512, 1) k_ls(Geometry g, const float2* __restr
                     float dn[4];
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
-                        un[e] = valid ? ub[e * R * N] : make_float2(0.f, 0.f);
-                        dn[e] = valid ? __ldg(db + e * R * N) : 0.f;
+                        un[e] = valid ? ldg2_na(ub + e * R * N) : make_float2(0.f, 0.f);
+                        dn[e] = valid ? ldg1_na(db + e * R * N) : 0.f;
                     }
 #pragma unroll 1
                     for (int gi = 0; gi < R / 4; ++gi) {
@@ -337,8 +337,8 @@ __global__ void __launch_bounds__(512, 1) k_ls(Geometry g, const float2* __restr
                             const int gn = ((q1 / T) * T + R * (q1 % T)) * N;
 #pragma unroll
                             for (int e = 0; e < 4; ++e) {
-                                un[e] = ub[gn + e * R * N];
-                                dn[e] = __ldg(db + gn + e * R * N);
+                                un[e] = ldg2_na(ub + gn + e * R * N);
+                                dn[e] = ldg1_na(db + gn + e * R * N);
                             }
                         }
 #pragma unroll
