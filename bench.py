@@ -288,6 +288,7 @@ def main():
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         kt = {"k_grad": float(tt[0]), "k_ls": float(tt[1])}
     cand = {"k_grad": (kt["k_grad"], n_local_bytes_grad), "k_ls": (kt["k_ls"], n_local_bytes_ls)}
+    it_bytes = (64.0 * n * N * N + 80.0 * w.H * w.W) / world
     dom = max(cand, key=lambda k: cand[k][0])
     dur_ms, algo_bytes = cand[dom]
     achieved = algo_bytes / (dur_ms / 1e3) / 1e9
@@ -362,6 +363,10 @@ def main():
                      "algorithmic_bytes_per_launch": algo_bytes, "avg_launch_ms": dur_ms,
                      "timing": "device globaltimer per launch, timed region (%d launches)" % ktimes[dom][1],
                      "k_grad_avg_ms": kt["k_grad"], "k_ls_avg_ms": kt["k_ls"]},
+        # whole-iteration design-S roofline: 64 B per frame pixel (k_grad 36, k_ls 20,
+        # k_adj 8) + 80 B per object pixel (DY reads, eta, eta gather, update) per CG iteration
+        "iteration_roofline": {"algorithmic_bytes": it_bytes, "achieved_GBps": it_bytes / (ms / args.steps) / 1e6,
+                               "peak_GBps": pk, "frac": it_bytes / (ms / args.steps) / 1e6 / pk},
         "stage_ms": {"begin": stage[0], "k_grad": stage[1], "k_adj": stage[2], "dir_eta": stage[3],
                      "k_ls": stage[4], "ls_rest_upd": stage[5], "iteration_eager": stage[6]},
         "mean_shrinks": float(np.mean(shrinks)),
