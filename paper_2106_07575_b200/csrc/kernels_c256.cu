@@ -269,8 +269,8 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(512, 1)
                 float dn[4];
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
-                    un[e] = ld2_hint(ub + e * R * N, pol);
-                    dn[e] = ld1_hint(db + e * R * N, pol);
+                    un[e] = ld2_hint_na(ub + e * R * N, pol);
+                    dn[e] = ld1_hint_na(db + e * R * N, pol);
                 }
 #pragma unroll 1
                 for (int gi = 0; gi < T / 4; ++gi) {
@@ -286,8 +286,8 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(512, 1)
                         const int gn = go + 4 * R * N;
 #pragma unroll
                         for (int e = 0; e < 4; ++e) {
-                            un[e] = ld2_hint(ub + gn + e * R * N, pol);
-                            dn[e] = ld1_hint(db + gn + e * R * N, pol);
+                            un[e] = ld2_hint_na(ub + gn + e * R * N, pol);
+                            dn[e] = ld1_hint_na(db + gn + e * R * N, pol);
                         }
                     }
 #pragma unroll
