@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--views", type=int, default=0, help="view3d: number of views (default: all 64)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ls-batch", type=int, default=16)
+    ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
+                    help="world > 1: peer-memory windows (CUDA IPC) or NCCL for the per-iteration exchanges")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
@@ -218,10 +220,18 @@ def main():
     import torch.distributed as dist
     from paper_2106_07575_b200 import _lib as L
 
+    # one rank per GPU; more ranks than GPUs share them round-robin (functional runs only)
+    local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    # bench-level collectives (barrier, max over ranks, handle exchange) run on CPU tensors over gloo
+    # with the peer-memory transport (NCCL is not needed at all), on NCCL otherwise
+    coll_dev = dev if args.transport == "nccl" else torch.device("cpu")
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.transport == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
         try:
             import nvidia  # type: ignore
             for pth in nvidia.__path__:
@@ -231,12 +241,13 @@ def main():
         except Exception:
             pass
     if w.views > 1:
-        return run_views(args, w, world, rank, local, dev)
+        return run_views(args, w, world, rank, local, dev, coll_dev)
     psi_true, p, scan, d = synth_device(w, dev)
     n = len(scan)
-    cfg = L.default_config(ls_batch=args.ls_batch, device=local, rank=rank, world=world)
+    cfg = L.default_config(ls_batch=args.ls_batch, device=local, rank=rank, world=world,
+                           transport=L.TRANSPORT_P2P if args.transport == "p2p" else L.TRANSPORT_NCCL)
     idbuf = None
-    if world > 1:
+    if world > 1 and args.transport == "nccl":
         obj = [L.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         import ctypes
@@ -245,6 +256,10 @@ def main():
     psi0 = torch.ones((w.H, w.W), dtype=torch.complex64, device=dev)
     pdev = torch.from_numpy(p.astype(np.complex64)).to(dev)
     pt = L.Ptyger(psi0, pdev, scan, d, config=cfg)
+    if world > 1 and args.transport == "p2p":
+        handles = [None] * world
+        dist.all_gather_object(handles, pt.ipc_handle())
+        pt.ipc_connect(handles)
 
     def barrier():
         torch.cuda.synchronize()
@@ -268,7 +283,7 @@ def main():
     # the kernels themselves (global ns timer; graph launches on the library stream)
     ktimes = pt.kernel_times(reset=True)
     if world > 1:
-        tt = torch.tensor([ms], dtype=torch.float64, device=dev)
+        tt = torch.tensor([ms], dtype=torch.float64, device=coll_dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
     launches = pt.kernel_launches()
@@ -284,7 +299,7 @@ def main():
     pk, pk_kind = peaks()
     kt = {k: (v[0] / v[1] if v[1] else stage[1 if k == "k_grad" else 4]) for k, v in ktimes.items()}
     if world > 1:
-        tt = torch.tensor([kt["k_grad"], kt["k_ls"]], dtype=torch.float64, device=dev)
+        tt = torch.tensor([kt["k_grad"], kt["k_ls"]], dtype=torch.float64, device=coll_dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         kt = {"k_grad": float(tt[0]), "k_ls": float(tt[1])}
     cand = {"k_grad": (kt["k_grad"], n_local_bytes_grad), "k_ls": (kt["k_ls"], n_local_bytes_ls)}
@@ -357,6 +372,7 @@ def main():
                                f"({w.k}^2 raster, step {w.step}, jitter {w.jitter}), photons {w.photons:g}, Poisson",
                    "H": w.H, "W": w.W, "N": w.N, "frames": n, "ls_batch": args.ls_batch,
                    "parallelism": f"stripes{world}",
+                   "transport": args.transport if world > 1 else None,
                    "l2": "inputs larger than L2 (u, v, d resident in HBM: %.1f GB)" % (n * N * N * 20 / 1e9)},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": pk, "peak_kind": pk_kind,
                      "unit": "GB/s", "frac": achieved / pk, "traffic": traffic,
@@ -381,7 +397,7 @@ def main():
         dist.destroy_process_group()
 
 
-def run_views(args, w, world, rank, local, dev):
+def run_views(args, w, world, rank, local, dev, coll_dev=None):
     """3-D ptycho-tomography batch (BASELINE config 5): independent views, sharded
     round-robin over the ranks with no communication; each view is its own libptyger context.
     One step = one CG iteration of every view."""
@@ -413,7 +429,7 @@ def run_views(args, w, world, rank, local, dev):
     torch.cuda.synchronize()
     clocks = clk.stop()
     if world > 1:
-        tt = torch.tensor([ms], dtype=torch.float64, device=dev)
+        tt = torch.tensor([ms], dtype=torch.float64, device=coll_dev if coll_dev is not None else dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
     launches = sum(q.kernel_launches() for q in views)

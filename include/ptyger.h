@@ -80,8 +80,19 @@ typedef struct {
     int32_t device;       /* CUDA device ordinal                                          */
     int32_t rank;         /* this process's rank, 0..world-1                              */
     int32_t world;        /* number of ranks (one GPU each)                               */
-    const void* nccl_id;  /* 128-byte ncclUniqueId from ptyger_nccl_unique_id (world > 1) */
+    const void* nccl_id;  /* 128-byte ncclUniqueId from ptyger_nccl_unique_id (world > 1, NCCL transport) */
+    int32_t transport;    /* world > 1: PTYGER_TRANSPORT_NCCL (default) or PTYGER_TRANSPORT_P2P        */
 } ptyger_config;
+
+/* Transports of the per-iteration exchanges when world > 1 (band partial gradients, fp64 scalar
+ * allreduces, object gather).  NCCL: ncclSend/Recv/AllReduce captured in the iteration graph.
+ * P2P: the producing kernels store straight into the other ranks' CUDA-IPC-mapped exchange windows
+ * and signal with system-scope release/acquire epoch flags (kernels_p2p.cu); the scalar sums are
+ * taken in rank order, so every rank gets bitwise identical values.  P2P contexts are created in two
+ * steps: ptyger_init (everything local), then ptyger_ipc_handle on every rank, an out-of-band exchange
+ * of the 64-byte handles (e.g. torch.distributed), and ptyger_ipc_connect with all of them.  Ranks may
+ * share one GPU (CUDA IPC within a device) or use peer GPUs (NVLink). */
+enum { PTYGER_TRANSPORT_NCCL = 0, PTYGER_TRANSPORT_P2P = 1 };
 
 /* Per-iteration trace (SPEC trace fields S:226-229; step_norm = ||psi_{m+1}-psi_m||_2). */
 typedef struct {

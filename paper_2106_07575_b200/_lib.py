@@ -18,6 +18,7 @@ PTYGER_OK = 0
 STATUS = {0: "OK", 2: "E_ARG", 3: "E_DATA", 4: "E_NUMERIC", 5: "E_CUDA", 6: "E_NCCL", 7: "E_OOM", 8: "E_STATE"}
 DIR_DY, DIR_DY_REAL, DIR_FR, DIR_PR, DIR_GD = 0, 1, 2, 3, 4
 EST_ML, EST_LS = 0, 1
+TRANSPORT_NCCL, TRANSPORT_P2P = 0, 1
 
 
 class PtygerError(RuntimeError):
@@ -30,7 +31,8 @@ class Config(C.Structure):
     _fields_ = [("gamma0", C.c_double), ("tau", C.c_double), ("t", C.c_double), ("eps", C.c_double),
                 ("max_shrinks", C.c_int32), ("direction", C.c_int32), ("ls_batch", C.c_int32),
                 ("estimator", C.c_int32),
-                ("device", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32), ("nccl_id", C.c_void_p)]
+                ("device", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32), ("nccl_id", C.c_void_p),
+                ("transport", C.c_int32)]
 
 
 class Trace(C.Structure):
@@ -52,6 +54,8 @@ def _load():
         "ptyger_init": (I32, [C.POINTER(P), C.POINTER(Config), P, I64, I64, P, I32, P, I64, P]),
         "ptyger_init_subpixel": (I32, [C.POINTER(P), C.POINTER(Config), P, I64, I64, P, I32, P, I64, P]),
         "ptyger_partition_subpixel": (I32, [P, I64, I64, I32, I32, P, P]),
+        "ptyger_ipc_handle": (I32, [P, P]),
+        "ptyger_ipc_connect": (I32, [P, P]),
         "ptyger_cg_iterate": (I32, [P, I32, P]),
         "ptyger_get_object": (I32, [P, P]),
         "ptyger_get_gradient": (I32, [P, P]),
@@ -196,6 +200,19 @@ class Ptyger:
         st = init(C.byref(self.ctx), C.byref(self.cfg), po, self.H, self.W, pp, self.N, sc.ctypes.data, self.n, pd)
         _check(st, None)
         self.K = self.cfg.ls_batch
+
+    def ipc_handle(self) -> bytes:
+        """P2P transport: this rank's 64-byte exchange-window handle (exchange it out of band)."""
+        buf = (C.c_char * 64)()
+        _check(lib.ptyger_ipc_handle(self.ctx, buf), self.ctx)
+        return bytes(buf)
+
+    def ipc_connect(self, handles):
+        """P2P transport: all ranks' handles in rank order (list of 64-byte strings)."""
+        blob = b"".join(handles)
+        assert len(blob) == 64 * self.cfg.world
+        buf = (C.c_char * len(blob)).from_buffer_copy(blob)
+        _check(lib.ptyger_ipc_connect(self.ctx, buf), self.ctx)
 
     def close(self):
         if getattr(self, "ctx", None) and self.ctx.value:

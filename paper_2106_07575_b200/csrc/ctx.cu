@@ -15,6 +15,7 @@
 
 #include "host.h"
 #include "internal.h"
+#include "p2p.h"
 
 using namespace pty;
 
@@ -150,6 +151,11 @@ struct ptyger_ctx {
     bool failed_numeric = false;
     // bands: [0] with rank-1, [1] with rank+1 (storage-local rows)
     int64_t band_lo[2] = {0, 0}, band_rows[2] = {0, 0};
+    // peer-memory transport (cfg.transport == PTYGER_TRANSPORT_P2P, world > 1)
+    bool p2p = false, connected = true;
+    unsigned char* win = nullptr;        // own exchange window (cudaMalloc: IPC-exportable)
+    P2PView pv{};
+    uint64_t gather_epoch = 1;           // host mirror of the gather channel's epoch (buffer parity)
     // nccl
     NcclApi* nc = nullptr;
     ncclComm_t comm = nullptr;
@@ -191,6 +197,12 @@ static ptyger_status set_err(ptyger_ctx* c, ptyger_status s, const std::string& 
     return s;
 }
 
+// fp64 sum over ranks, in place on the device (NCCL or the peer-memory mailbox)
+static int allreduce(ptyger_ctx* c, double* buf, int count, cudaStream_t s) {
+    if (c->p2p) return launch_p2p_allreduce(buf, count, c->pv, c->st, s);
+    return c->nc->AllReduce(buf, buf, count, ncclFloat64, ncclSum, c->comm, s) == ncclSuccess ? 0 : -1;
+}
+
 // ------------------------------------------------------------------------------------------
 // One iteration as a sequence of launches on c->stream (captured into a graph).
 // parity p: gcur = g[p], gprev = g[1-p].
@@ -224,7 +236,19 @@ static int enqueue_iteration(ptyger_ctx* c, int p, std::string& err, int64_t& la
     ++launches;
     EV(3);
     int nparts = c->ntx * c->nty;
-    if (multi) {
+    if (multi && c->p2p) {
+        // band exchange through the neighbours' exchange windows (kernels_p2p.cu)
+        LK(launch_p2p_band(gcur, c->band_lo[0], c->band_rows[0], c->band_lo[1], c->band_rows[1], c->W, c->pv, c->st,
+                           c->band_grid, s));
+        launches += 2;
+        for (int b = 0; b < 2; ++b) {
+            if (c->band_rows[b] <= 0) continue;
+            LK(launch_band_add(gcur, c->recv[b], c->band_lo[b], c->band_rows[b], c->W, gprev, c->eta, g.own_lo, g.own_hi,
+                               c->part_adj + (int64_t)nparts * NDY, c->band_grid, s));
+            ++launches;
+            nparts += c->band_grid;
+        }
+    } else if (multi) {
         // band exchange of partial gradients with the two neighbours (replaces the paper's
         // pattern duplication + border exchange, R#15)
         NK(c->nc->GroupStart());
@@ -245,7 +269,7 @@ static int enqueue_iteration(ptyger_ctx* c, int p, std::string& err, int64_t& la
         }
     }
     LK(launch_reduce(c->part_adj, nparts, NDY, &c->st->dy[0], s)); ++launches;
-    if (multi) NK(c->nc->AllReduce(&c->st->dy[0], &c->st->dy[0], NDY, ncclFloat64, ncclSum, c->comm, s));
+    if (multi) LK(allreduce(c, &c->st->dy[0], NDY, s));
     // DIR stage (Alg.1 651-656)
     LK(launch_dir(c->st, sc, s)); ++launches;
     LK(launch_eta(g, gcur, c->eta, c->st, c->part_el, c->grid_el, s)); ++launches;
@@ -281,11 +305,11 @@ static int enqueue_iteration(ptyger_ctx* c, int p, std::string& err, int64_t& la
         LK(launch_reduce(fused ? c->part_fr : c->part_el, fused ? c->parts_ls : c->grid_el, wscreen,
                          &c->st->ls_pass[0], s, c->st, pass == 0 ? 0 : 1, pass));
         ++launches;
-        if (multi) NK(c->nc->AllReduce(&c->st->ls_pass[0], &c->st->ls_pass[0], LSW, ncclFloat64, ncclSum, c->comm, s));
+        if (multi) LK(allreduce(c, &c->st->ls_pass[0], LSW, s));
         LK(launch_pick(c->st, sc, pass, 0, 0, s)); ++launches;
         LK(launch_lsx(g, c->u, c->v, c->d, sc, pass, true, c->part_el, c->grid_el, c->st, s)); ++launches;
         LK(launch_reduce(c->part_el, c->grid_el, LSP, &c->st->ls_pass[0], s, c->st, 2, pass)); ++launches;
-        if (multi) NK(c->nc->AllReduce(&c->st->ls_pass[0], &c->st->ls_pass[0], KC, ncclFloat64, ncclSum, c->comm, s));
+        if (multi) LK(allreduce(c, &c->st->ls_pass[0], KC, s));
         LK(launch_pick(c->st, sc, pass, 1, pass == npass - 1, s)); ++launches;
     }
     // Update stage (Alg.1 672)
@@ -342,12 +366,9 @@ static int run_forward(ptyger_ctx* c, std::string& err) {
     const Geometry& g = c->geo;
     LK(launch_fwd(g, c->psi, c->probe, c->pos, c->order, c->d, c->u, c->part_fr, c->grid_fr, (float)c->sc.eps, c->stream));
     LK(launch_reduce(c->part_fr, c->grid_fr, 1, c->scratch, c->stream));
-    if (c->cfg.world > 1) {
-        ncclResult_t r = c->nc->AllReduce(c->scratch, c->scratch, 1, ncclFloat64, ncclSum, c->comm, c->stream);
-        if (r != ncclSuccess) {
-            err = std::string("ncclAllReduce(F0): ") + c->nc->GetErrorString(r);
-            return PTYGER_E_NCCL;
-        }
+    if (c->cfg.world > 1 && allreduce(c, c->scratch, 1, c->stream) != 0) {
+        err = "allreduce(F0) failed";
+        return c->p2p ? PTYGER_E_CUDA : PTYGER_E_NCCL;
     }
     LK(launch_set_F(c->st, c->scratch, c->sc.K, c->stream));
     CK(cudaStreamSynchronize(c->stream));
@@ -358,6 +379,7 @@ static void free_ctx(ptyger_ctx* c) {
     if (!c) return;
     for (int p = 0; p < 2; ++p)
         if (c->graph[p]) cudaGraphExecDestroy(c->graph[p]);
+    if (c->p2p) c->full = c->recv[0] = c->recv[1] = nullptr;   // inside the exchange window
     void* ptrs[] = {c->psi, c->g[0], c->g[1], c->eta, c->u, c->v, c->probe, c->probe_s, c->full, c->recv[0], c->recv[1], c->d,
                     c->pos, c->order, c->frac, c->tile_ptr, c->entries, c->part_adj, c->part_fr, c->part_el, c->scratch, c->st,
                     c->d_tr};
@@ -368,6 +390,11 @@ static void free_ctx(ptyger_ctx* c) {
     for (int i = 0; i < 2; ++i)
         if (c->ev_it[i]) cudaEventDestroy(c->ev_it[i]);
     if (c->comm && c->nc) c->nc->CommDestroy(c->comm);
+    if (c->p2p) {
+        for (int r = 0; r < c->pv.world; ++r)
+            if (r != c->cfg.rank && c->pv.win[r]) cudaIpcCloseMemHandle(c->pv.win[r]);
+        if (c->win) cudaFree(c->win);
+    }
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -387,6 +414,7 @@ void ptyger_config_default(ptyger_config* cfg) {
     cfg->device = 0;
     cfg->rank = 0;
     cfg->world = 1;
+    cfg->transport = PTYGER_TRANSPORT_NCCL;
     cfg->nccl_id = nullptr;
 }
 
@@ -518,7 +546,8 @@ static ptyger_status init_impl(ptyger_ctx* c, const float* object, const float* 
     pool_setup(cfg.device);
     CK(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, cfg.device));
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-    if (cfg.world > 1) {
+    c->p2p = cfg.world > 1 && cfg.transport == PTYGER_TRANSPORT_P2P;
+    if (cfg.world > 1 && !c->p2p) {
         c->nc = nccl_api(err);
         if (!c->nc) return PTYGER_E_NCCL;
         ncclUniqueId id;
@@ -569,9 +598,43 @@ static ptyger_status init_impl(ptyger_ctx* c, const float* object, const float* 
     AL(c->part_el, double, (int64_t)c->grid_el * LSW);
     AL(c->scratch, double, 64);
     AL(c->st, DevState, 1);
-    for (int b = 0; b < 2; ++b)
-        if (c->band_rows[b] > 0) AL(c->recv[b], float2, c->band_rows[b] * W);
-    if (cfg.world > 1) AL(c->full, float2, H * W);
+    if (c->p2p) {
+        // exchange window layout, identical arithmetic on every rank (p2p.h)
+        P2PView& v = c->pv;
+        v.world = cfg.world;
+        v.rank = cfg.rank;
+        v.off_flags = 0;
+        v.off_mail = 4096;
+        v.off_full = v.off_mail + (int64_t)2 * P2P_MAX_RANKS * P2P_MBW * 8;
+        v.full_elems = H * W;
+        auto up = [](int64_t x) { return (x + 255) / 256 * 256; };
+        int64_t my_bytes = 0;
+        for (int r = 0; r < cfg.world; ++r) {
+            const int64_t* Rr = &c->rows[6 * r];
+            int64_t b0 = 0, b1 = 0;
+            if (r > 0) b0 = std::max<int64_t>(0, c->rows[6 * (r - 1) + 3] - Rr[2]);
+            if (r + 1 < cfg.world) b1 = std::max<int64_t>(0, Rr[3] - c->rows[6 * (r + 1) + 2]);
+            v.off_recv0[r] = up(v.off_full + 2 * H * W * 8);
+            v.off_recv1[r] = up(v.off_recv0[r] + b0 * W * 8);
+            if (r == cfg.rank) my_bytes = up(v.off_recv1[r] + b1 * W * 8);
+        }
+        void* wp = nullptr;
+        if (cudaMalloc(&wp, (size_t)my_bytes) != cudaSuccess) {
+            cudaGetLastError();
+            err = "cudaMalloc of the " + std::to_string(my_bytes) + "-byte exchange window failed";
+            return PTYGER_E_OOM;
+        }
+        CK(cudaMemset(wp, 0, (size_t)my_bytes));
+        c->win = static_cast<unsigned char*>(wp);
+        v.win[cfg.rank] = c->win;
+        c->full = reinterpret_cast<float2*>(c->win + v.off_full);
+        c->recv[0] = c->band_rows[0] > 0 ? reinterpret_cast<float2*>(c->win + v.off_recv0[cfg.rank]) : nullptr;
+        c->recv[1] = c->band_rows[1] > 0 ? reinterpret_cast<float2*>(c->win + v.off_recv1[cfg.rank]) : nullptr;
+    } else {
+        for (int b = 0; b < 2; ++b)
+            if (c->band_rows[b] > 0) AL(c->recv[b], float2, c->band_rows[b] * W);
+        if (cfg.world > 1) AL(c->full, float2, H * W);
+    }
 #undef AL
     CK(cudaStreamSynchronize(0));  // pool allocations and zero fills (legacy stream) are done
     // Uploads are asynchronous on the context stream (from pinned host memory the DMA of d overlaps
@@ -629,7 +692,21 @@ static ptyger_status init_impl(ptyger_ctx* c, const float* object, const float* 
     DevState hs;
     std::memset(&hs, 0, sizeof(hs));
     hs.tk_start[0] = hs.tk_start[1] = ~0ull;   // disarmed frame-kernel timers
+    for (int ch = 0; ch < 4; ++ch) hs.p2p_epoch[ch] = 1;   // peer flags start at 0
     CK(cudaMemcpyAsync(c->st, &hs, sizeof(hs), cudaMemcpyHostToDevice, c->stream));
+    if (c->p2p) {   // the forward pass and the graphs need the peers: ptyger_ipc_connect
+        unsigned long long hb = 0;
+        CK(cudaMemcpyAsync(&hb, bad, sizeof(hb), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        cudaFreeAsync(bad, 0);
+        if (hb != ~0ull) {
+            err = "intensities: frame " + std::to_string(c->local_global[(int64_t)hb]) +
+                  " has a negative or non-finite value";
+            return PTYGER_E_DATA;
+        }
+        c->connected = false;
+        return PTYGER_OK;
+    }
     int rc2 = build_graphs(c, err);   // host-side capture + instantiation overlaps the uploads
     if (rc2) {
         cudaStreamSynchronize(c->stream);
@@ -668,7 +745,9 @@ static ptyger_status create_ctx(ptyger_ctx** out, const ptyger_config* cfg_in, c
         cfg.max_shrinks > SMAX || cfg.ls_batch < KMIN || cfg.ls_batch > KC || cfg.direction < 0 ||
         cfg.direction > PTYGER_DIR_GD || cfg.estimator < 0 || cfg.estimator > PTYGER_EST_LS || cfg.world < 1 ||
         cfg.rank < 0 || cfg.rank >= cfg.world ||
-        (cfg.world > 1 && !cfg.nccl_id) || !std::isfinite(cfg.t))
+        (cfg.world > 1 && cfg.transport == PTYGER_TRANSPORT_NCCL && !cfg.nccl_id) ||
+        (cfg.transport == PTYGER_TRANSPORT_P2P && cfg.world > P2P_MAX_RANKS) ||
+        (cfg.transport != PTYGER_TRANSPORT_NCCL && cfg.transport != PTYGER_TRANSPORT_P2P) || !std::isfinite(cfg.t))
         return set_err(nullptr, PTYGER_E_ARG,
                        "init: bad config (need gamma0>0, 0<tau<1, eps>0, 1<=max_shrinks<=64, 4<=ls_batch<=16, "
                        "direction in {0,1,2}, 0<=rank<world, nccl_id when world>1)");
@@ -786,6 +865,7 @@ ptyger_status ptyger_cg_iterate(ptyger_ctx* c, int32_t n_iter, ptyger_trace* tra
     std::string& err = c->err;
     if (n_iter < 0) return set_err(c, PTYGER_E_ARG, "cg_iterate: n_iter < 0");
     if (c->failed_numeric) return set_err(c, PTYGER_E_NUMERIC, "context is in a numeric-failure state; call set_state");
+    if (!c->connected) return set_err(c, PTYGER_E_STATE, "P2P context not connected (ptyger_ipc_connect)");
     if (n_iter == 0) return PTYGER_OK;
     CK(cudaSetDevice(c->cfg.device));
     if (c->tr_cap < n_iter) {
@@ -826,6 +906,15 @@ static ptyger_status gather_rows(ptyger_ctx* c, const float2* src, float* out) {
         return PTYGER_OK;
     }
     const int64_t* R = &c->rows[6 * c->cfg.rank];
+    if (c->p2p) {
+        if (!c->connected) return set_err(c, PTYGER_E_STATE, "P2P context not connected (ptyger_ipc_connect)");
+        const int64_t par = (int64_t)(c->gather_epoch & 1);
+        LK(launch_p2p_gather(src, c->st_lo, R[0], R[1], c->W, c->pv, c->st, c->band_grid, c->stream));
+        c->gather_epoch += 1;
+        CK(cudaStreamSynchronize(c->stream));
+        CK(cudaMemcpy(out, c->full + par * c->H * c->W, sizeof(float2) * c->H * c->W, cudaMemcpyDeviceToHost));
+        return PTYGER_OK;
+    }
     CK(cudaMemcpyAsync(c->full + R[0] * c->W, src + (R[0] - c->st_lo) * c->W, sizeof(float2) * (R[1] - R[0]) * c->W,
                        cudaMemcpyDeviceToDevice, c->stream));
     NK(c->nc->GroupStart());
@@ -902,6 +991,7 @@ ptyger_status ptyger_set_state(ptyger_ctx* c, const float* psi, const float* g_p
     std::memset(&hs, 0, sizeof(hs));
     hs.m = m;
     hs.tk_start[0] = hs.tk_start[1] = ~0ull;
+    for (int ch = 0; ch < 4; ++ch) hs.p2p_epoch[ch] = 1;
     CK(cudaMemcpy(c->st, &hs, sizeof(hs), cudaMemcpyHostToDevice));
     c->m_host = m;
     c->failed_numeric = false;
@@ -927,6 +1017,7 @@ float ptyger_last_iterate_ms(const ptyger_ctx* c) { return c ? c->last_ms : 0.f;
 
 ptyger_status ptyger_stage_times(ptyger_ctx* c, int32_t n_iter, double* ms) {
     if (!c || !ms || n_iter < 1) return set_err(c, PTYGER_E_ARG, "stage_times: bad arguments");
+    if (!c->connected) return set_err(c, PTYGER_E_STATE, "P2P context not connected (ptyger_ipc_connect)");
     if (c->failed_numeric) return set_err(c, PTYGER_E_NUMERIC, "context is in a numeric-failure state");
     std::string& err = c->err;
     CK(cudaSetDevice(c->cfg.device));
@@ -965,6 +1056,44 @@ ptyger_status ptyger_kernel_times(ptyger_ctx* c, double* ms, int32_t* count, int
     ms[1] = h[1];
     count[0] = (int32_t)h[2];
     count[1] = (int32_t)h[3];
+    return PTYGER_OK;
+}
+
+ptyger_status ptyger_ipc_handle(ptyger_ctx* c, void* out64) {
+    if (!c || !out64) return set_err(c, PTYGER_E_ARG, "ipc_handle: null pointer");
+    if (!c->p2p) return set_err(c, PTYGER_E_STATE, "ipc_handle: not a P2P-transport context");
+    std::string& err = c->err;
+    CK(cudaSetDevice(c->cfg.device));
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, c->win));
+    static_assert(sizeof(h) == 64, "CUDA IPC handles are 64 bytes");
+    std::memcpy(out64, &h, sizeof(h));
+    return PTYGER_OK;
+}
+
+ptyger_status ptyger_ipc_connect(ptyger_ctx* c, const void* handles) {
+    if (!c || !handles) return set_err(c, PTYGER_E_ARG, "ipc_connect: null pointer");
+    if (!c->p2p || c->connected) return set_err(c, PTYGER_E_STATE, "ipc_connect: not a pending P2P context");
+    std::string& err = c->err;
+    CK(cudaSetDevice(c->cfg.device));
+    for (int r = 0; r < c->cfg.world; ++r) {
+        if (r == c->cfg.rank) continue;
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, static_cast<const unsigned char*>(handles) + 64 * r, 64);
+        void* p = nullptr;
+        const cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            err = "cudaIpcOpenMemHandle(rank " + std::to_string(r) + "): " + cudaGetErrorString(e);
+            return PTYGER_E_CUDA;
+        }
+        c->pv.win[r] = static_cast<unsigned char*>(p);
+    }
+    c->connected = true;
+    int rc = run_forward(c, err);
+    if (rc) return (ptyger_status)rc;
+    rc = build_graphs(c, err);
+    if (rc) return (ptyger_status)rc;
     return PTYGER_OK;
 }
 

@@ -41,6 +41,10 @@ struct DevState {
     // device-side kernel timers (globaltimer ns) of the two frame kernels, [0] GRAD, [1] LS pass 0:
     // first CTA start / last CTA end of the current launch, folded into sums by k_begin_iter
     unsigned long long tk_start[2], tk_end[2];
+    // peer-memory transport (world > 1, PTYGER_TRANSPORT_P2P): per-channel epochs (start at 1, the
+    // windows' flags at 0) and grid-completion counters of the put kernels
+    unsigned long long p2p_epoch[4];
+    unsigned int p2p_done[4];
     double tk_sum_ms[2];
     int tk_cnt[2];
     int trace_idx;           // slot of the current iteration in the trace buffer

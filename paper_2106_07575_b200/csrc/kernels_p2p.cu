@@ -1,0 +1,152 @@
+// Peer-memory transport for world > 1 (PTYGER_TRANSPORT_P2P): the iteration's exchanges are done by
+// kernels that store straight into the other ranks' CUDA-IPC-mapped exchange windows and signal with
+// epoch flags (system-scope release / acquire), instead of NCCL calls:
+//   * band exchange (R#15): each rank stores the partial gradient of the rows it shares with a
+//     neighbour into that neighbour's receive buffer (k_p2p_band_put), then waits for the
+//     neighbours' flags (k_p2p_wait) before the existing k_band_add;
+//   * scalar allreduce (DY sums, LS partials, F0): every rank writes its vector into slot [rank] of
+//     every window's mailbox, waits for all flags and sums the slots in rank order, so all ranks get
+//     bitwise identical results (k_p2p_allreduce);
+//   * object gather (get_object / get_gradient): owned rows into every window's full-object buffer.
+// Mailboxes are double-buffered by epoch parity: a rank can only start epoch e + 2 after it has seen
+// every peer's epoch e + 1, i.e. after every peer finished reading epoch e.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "dev.cuh"
+#include "p2p.h"
+
+namespace pty {
+
+__device__ __forceinline__ void flag_release(unsigned long long* f, unsigned long long e) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(e) : "memory");
+}
+__device__ __forceinline__ unsigned long long flag_acquire(const unsigned long long* f) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
+    return v;
+}
+// bounded spin: a lost peer becomes a launch failure (trap) after ~tens of seconds, not a hang
+__device__ __forceinline__ void flag_wait(const unsigned long long* f, unsigned long long e) {
+    unsigned long long spins = 0;
+    while (flag_acquire(f) < e) {
+        if (++spins == (1ull << 36)) __trap();
+    }
+}
+
+__device__ __forceinline__ unsigned long long* win_flag(const P2PView& v, int owner, int src, int ch) {
+    return reinterpret_cast<unsigned long long*>(v.win[owner] + v.off_flags) + src * P2P_CHANNELS + ch;
+}
+__device__ __forceinline__ double* win_mail(const P2PView& v, int owner, int par, int src) {
+    return reinterpret_cast<double*>(v.win[owner] + v.off_mail) + ((int64_t)par * v.world + src) * P2P_MBW;
+}
+
+// Grid-wide "all blocks stored" -> the last block raises the flags of channel ch in the windows of
+// the given ranks.  st->p2p_done[ch] counts blocks.
+__device__ __forceinline__ void grid_signal(DevState* st, int ch, const P2PView& v, const int* to, int nto,
+                                            unsigned long long e) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        const unsigned int prev = atomicAdd(&st->p2p_done[ch], 1u);
+        if (prev == gridDim.x - 1) {
+            st->p2p_done[ch] = 0;
+            __threadfence_system();
+            for (int i = 0; i < nto; ++i) flag_release(win_flag(v, to[i], v.rank, ch), e);
+        }
+    }
+}
+
+// ---- band exchange -------------------------------------------------------------------------
+__global__ void k_p2p_band_put(const float2* __restrict__ gcur, int64_t lo0, int64_t rows0, int64_t lo1,
+                               int64_t rows1, int64_t W, P2PView v, DevState* st) {
+    const unsigned long long e = st->p2p_epoch[P2P_CH_BAND];
+    // my left band -> left neighbour's recv[1]; my right band -> right neighbour's recv[0]
+    const int64_t n0 = rows0 * W, n1 = rows1 * W;
+    float2* d0 = rows0 > 0 ? reinterpret_cast<float2*>(v.win[v.rank - 1] + v.off_recv1[v.rank - 1]) : nullptr;
+    float2* d1 = rows1 > 0 ? reinterpret_cast<float2*>(v.win[v.rank + 1] + v.off_recv0[v.rank + 1]) : nullptr;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n0 + n1; i += (int64_t)gridDim.x * blockDim.x) {
+        if (i < n0) d0[i] = gcur[lo0 * W + i];
+        else d1[i - n0] = gcur[lo1 * W + (i - n0)];
+    }
+    int to[2], nto = 0;
+    if (rows0 > 0) to[nto++] = v.rank - 1;
+    if (rows1 > 0) to[nto++] = v.rank + 1;
+    grid_signal(st, P2P_CH_BAND, v, to, nto, e);
+}
+
+// wait for the neighbours' band data (channel ch, from ranks with a band), then advance the epoch
+__global__ void k_p2p_wait(P2PView v, DevState* st, int ch, int from_left, int from_right) {
+    const unsigned long long e = st->p2p_epoch[ch];
+    if (from_left) flag_wait(win_flag(v, v.rank, v.rank - 1, ch), e);
+    if (from_right) flag_wait(win_flag(v, v.rank, v.rank + 1, ch), e);
+    st->p2p_epoch[ch] = e + 1;
+}
+
+// ---- scalar allreduce (fixed rank order) ----------------------------------------------------
+__global__ void k_p2p_allreduce(double* buf, int count, P2PView v, DevState* st) {
+    const unsigned long long e = st->p2p_epoch[P2P_CH_SCALAR];
+    const int par = (int)(e & 1);
+    for (int r = 0; r < v.world; ++r) {
+        double* m = win_mail(v, r, par, v.rank);
+        for (int i = threadIdx.x; i < count; i += blockDim.x) m[i] = buf[i];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        for (int r = 0; r < v.world; ++r) flag_release(win_flag(v, r, v.rank, P2P_CH_SCALAR), e);
+        for (int r = 0; r < v.world; ++r) flag_wait(win_flag(v, v.rank, r, P2P_CH_SCALAR), e);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < count; i += blockDim.x) {
+        double s = 0.0;
+        for (int r = 0; r < v.world; ++r) s += win_mail(v, v.rank, par, r)[i];
+        buf[i] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) st->p2p_epoch[P2P_CH_SCALAR] = e + 1;
+}
+
+// ---- object gather: owned rows [lo, hi) of src (storage-local row 0 = global row st_lo) ----------
+__global__ void k_p2p_gather_put(const float2* __restrict__ src, int64_t st_lo, int64_t lo, int64_t hi, int64_t W,
+                                 P2PView v, DevState* st) {
+    const unsigned long long e = st->p2p_epoch[P2P_CH_GATHER];
+    const int64_t n = (hi - lo) * W;
+    const int64_t par = (int64_t)(e & 1);   // double-buffered: see the file header
+    for (int r = 0; r < v.world; ++r) {
+        float2* dst = reinterpret_cast<float2*>(v.win[r] + v.off_full) + par * v.full_elems + lo * W;
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+            dst[i] = src[(lo - st_lo) * W + i];
+    }
+    int to[P2P_MAX_RANKS];
+    for (int r = 0; r < v.world; ++r) to[r] = r;
+    grid_signal(st, P2P_CH_GATHER, v, to, v.world, e);
+}
+
+__global__ void k_p2p_wait_all(P2PView v, DevState* st, int ch) {
+    const unsigned long long e = st->p2p_epoch[ch];
+    for (int r = 0; r < v.world; ++r) flag_wait(win_flag(v, v.rank, r, ch), e);
+    st->p2p_epoch[ch] = e + 1;
+}
+
+// ---- launchers -------------------------------------------------------------------------------
+int launch_p2p_band(const float2* gcur, int64_t lo0, int64_t rows0, int64_t lo1, int64_t rows1, int64_t W,
+                    const P2PView& v, DevState* st, int grid, cudaStream_t s) {
+    k_p2p_band_put<<<grid, 256, 0, s>>>(gcur, lo0, rows0, lo1, rows1, W, v, st);
+    k_p2p_wait<<<1, 1, 0, s>>>(v, st, P2P_CH_BAND, rows0 > 0, rows1 > 0);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+int launch_p2p_allreduce(double* buf, int count, const P2PView& v, DevState* st, cudaStream_t s) {
+    k_p2p_allreduce<<<1, 32, 0, s>>>(buf, count, v, st);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+int launch_p2p_gather(const float2* src, int64_t st_lo, int64_t lo, int64_t hi, int64_t W, const P2PView& v,
+                      DevState* st, int grid, cudaStream_t s) {
+    k_p2p_gather_put<<<grid, 256, 0, s>>>(src, st_lo, lo, hi, W, v, st);
+    k_p2p_wait_all<<<1, 1, 0, s>>>(v, st, P2P_CH_GATHER);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+}  // namespace pty
