@@ -232,15 +232,16 @@ static int enqueue_iteration(ptyger_ctx* c, int p, std::string& err, int64_t& la
     }
     ++launches;
     EV(2);
-    LK(launch_adj(g, c->v, c->tile_ptr, c->entries, c->ntx, c->nty, gcur, gprev, c->eta, c->part_adj, c->st, s));
+    LK(launch_adj(g, c->v, c->tile_ptr, c->entries, c->ntx, c->nty, gcur, gprev, c->eta, c->part_adj, c->st, s,
+                  (multi && c->p2p) ? &c->pv : nullptr));
     ++launches;
     EV(3);
     int nparts = c->ntx * c->nty;
     if (multi && c->p2p) {
-        // band exchange through the neighbours' exchange windows (kernels_p2p.cu)
-        LK(launch_p2p_band(gcur, c->band_lo[0], c->band_rows[0], c->band_lo[1], c->band_rows[1], c->W, c->pv, c->st,
-                           c->band_grid, s));
-        launches += 2;
+        // band exchange fused into k_adj (its band tiles stored into the neighbours' windows and its
+        // last tile raised the flags); wait for the neighbours' bands, then add them
+        LK(launch_p2p_wait_band(c->pv, c->st, c->band_rows[0] > 0, c->band_rows[1] > 0, s));
+        launches += 1;
         for (int b = 0; b < 2; ++b) {
             if (c->band_rows[b] <= 0) continue;
             LK(launch_band_add(gcur, c->recv[b], c->band_lo[b], c->band_rows[b], c->W, gprev, c->eta, g.own_lo, g.own_hi,

@@ -96,9 +96,12 @@ int launch_ls256(const Geometry& g, const float2* eta, const float2* probe, cons
 int launch_fwd256(const Geometry& g, const float2* psi, const float2* probe, const int2* pos, const int* order,
                   const float* d, float2* u, double* part, int grid, float eps, cudaStream_t s);
 int launch_fft2_256(const float2* in, float2* out, int64_t batch, bool inv, cudaStream_t s);
+struct P2PView;
+// pv (peer-memory transport): band rows are also stored into the neighbours' windows and the band
+// flags raised by the kernel's last tile (fused compute + exchange); nullptr otherwise
 int launch_adj(const Geometry& g, const float2* y, const int* tile_ptr, const int* tile_frames,
                int ntx, int nty, float2* gcur, const float2* gprev, const float2* eta, double* part,
-               const DevState* st, cudaStream_t s);
+               const DevState* st, cudaStream_t s, const P2PView* pv = nullptr);
 int launch_ls(const Geometry& g, const float2* eta, const float2* probe, const float2* probe_s, const int2* pos,
               const int* order, const float2* u, float2* v, const float* d, const SolverCfg& c,
               double* part, int grid, const DevState* st, cudaStream_t s);

@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include "dev.cuh"
+#include "p2p.h"
 
 namespace pty {
 
@@ -17,7 +18,8 @@ __global__ void __launch_bounds__(256) k_adj(Geometry g, const float2* __restric
                                              const int4* __restrict__ ent, const int* __restrict__ tile_ptr,
                                              int ntx, float2* __restrict__ gcur,
                                              const float2* __restrict__ gprev, const float2* __restrict__ eta,
-                                             double* __restrict__ part, const DevState* __restrict__ st) {
+                                             double* __restrict__ part, const DevState* __restrict__ st,
+                                             P2PView pv, int p2p) {
     __shared__ double sred[NDY][8];
     if (st->numeric_error) return;
     const int tile = blockIdx.x;
@@ -115,6 +117,16 @@ __global__ void __launch_bounds__(256) k_adj(Geometry g, const float2* __restric
             if (r < g.SH) {
                 const int64_t o = r * g.W + col;
                 gcur[o] = acc[i];
+                if (p2p) {
+                    // peer-memory transport: band rows go straight into the neighbour's receive
+                    // buffer (its recv[1] for my left band, recv[0] for my right band)
+                    if (r >= g.band_lo0 && r < g.band_hi0)
+                        reinterpret_cast<float2*>(pv.win[pv.rank - 1] + pv.off_recv1[pv.rank - 1])
+                            [(r - g.band_lo0) * g.W + col] = acc[i];
+                    if (r >= g.band_lo1 && r < g.band_hi1)
+                        reinterpret_cast<float2*>(pv.win[pv.rank + 1] + pv.off_recv0[pv.rank + 1])
+                            [(r - g.band_lo1) * g.W + col] = acc[i];
+                }
                 const bool own = r >= g.own_lo && r < g.own_hi && !(r >= g.band_lo0 && r < g.band_hi0) &&
                                  !(r >= g.band_lo1 && r < g.band_hi1);
                 if (own) {
@@ -143,6 +155,12 @@ __global__ void __launch_bounds__(256) k_adj(Geometry g, const float2* __restric
         double t = 0.0;
         for (int k = 0; k < 8; ++k) t += sred[threadIdx.x][k];
         part[(int64_t)tile * NDY + threadIdx.x] = t;
+    }
+    if (p2p) {   // the last tile raises the band flags of this epoch in the neighbours' windows
+        int to[2], nto = 0;
+        if (g.band_hi0 > g.band_lo0) to[nto++] = pv.rank - 1;
+        if (g.band_hi1 > g.band_lo1) to[nto++] = pv.rank + 1;
+        grid_signal(const_cast<DevState*>(st), P2P_CH_BAND, pv, to, nto, st->p2p_epoch[P2P_CH_BAND]);
     }
 }
 
@@ -570,10 +588,12 @@ __global__ void k_validate_d(const float* __restrict__ d, int64_t count, int64_t
 
 int launch_adj(const Geometry& g, const float2* y, const int* tile_ptr, const int* tile_frames,
                int ntx, int nty, float2* gcur, const float2* gprev, const float2* eta, double* part,
-               const DevState* st, cudaStream_t s) {
+               const DevState* st, cudaStream_t s, const P2PView* pv) {
     // tile_frames holds int4 entries {frame, row, col, 0}
+    P2PView v{};
+    if (pv) v = *pv;
     k_adj<<<ntx * nty, 256, 0, s>>>(g, y, reinterpret_cast<const int4*>(tile_frames), tile_ptr, ntx, gcur,
-                                    gprev, eta, part, st);
+                                    gprev, eta, part, st, v, pv ? 1 : 0);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 

@@ -1,9 +1,9 @@
 // Peer-memory transport for world > 1 (PTYGER_TRANSPORT_P2P): the iteration's exchanges are done by
 // kernels that store straight into the other ranks' CUDA-IPC-mapped exchange windows and signal with
 // epoch flags (system-scope release / acquire), instead of NCCL calls:
-//   * band exchange (R#15): each rank stores the partial gradient of the rows it shares with a
-//     neighbour into that neighbour's receive buffer (k_p2p_band_put), then waits for the
-//     neighbours' flags (k_p2p_wait) before the existing k_band_add;
+//   * band exchange (R#15): k_adj itself stores the partial gradient of the rows a rank shares with
+//     a neighbour into that neighbour's receive buffer and its last tile raises the flag (compute and
+//     exchange in one kernel); k_p2p_wait then waits for the neighbours' flags before k_band_add;
 //   * scalar allreduce (DY sums, LS partials, F0): every rank writes its vector into slot [rank] of
 //     every window's mailbox, waits for all flags and sums the slots in rank order, so all ranks get
 //     bitwise identical results (k_p2p_allreduce);
@@ -18,9 +18,6 @@
 
 namespace pty {
 
-__device__ __forceinline__ void flag_release(unsigned long long* f, unsigned long long e) {
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(e) : "memory");
-}
 __device__ __forceinline__ unsigned long long flag_acquire(const unsigned long long* f) {
     unsigned long long v;
     asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
@@ -34,49 +31,14 @@ __device__ __forceinline__ void flag_wait(const unsigned long long* f, unsigned 
     }
 }
 
-__device__ __forceinline__ unsigned long long* win_flag(const P2PView& v, int owner, int src, int ch) {
-    return reinterpret_cast<unsigned long long*>(v.win[owner] + v.off_flags) + src * P2P_CHANNELS + ch;
-}
 __device__ __forceinline__ double* win_mail(const P2PView& v, int owner, int par, int src) {
     return reinterpret_cast<double*>(v.win[owner] + v.off_mail) + ((int64_t)par * v.world + src) * P2P_MBW;
 }
 
-// Grid-wide "all blocks stored" -> the last block raises the flags of channel ch in the windows of
-// the given ranks.  st->p2p_done[ch] counts blocks.
-__device__ __forceinline__ void grid_signal(DevState* st, int ch, const P2PView& v, const int* to, int nto,
-                                            unsigned long long e) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence_system();
-        const unsigned int prev = atomicAdd(&st->p2p_done[ch], 1u);
-        if (prev == gridDim.x - 1) {
-            st->p2p_done[ch] = 0;
-            __threadfence_system();
-            for (int i = 0; i < nto; ++i) flag_release(win_flag(v, to[i], v.rank, ch), e);
-        }
-    }
-}
-
-// ---- band exchange -------------------------------------------------------------------------
-__global__ void k_p2p_band_put(const float2* __restrict__ gcur, int64_t lo0, int64_t rows0, int64_t lo1,
-                               int64_t rows1, int64_t W, P2PView v, DevState* st) {
-    const unsigned long long e = st->p2p_epoch[P2P_CH_BAND];
-    // my left band -> left neighbour's recv[1]; my right band -> right neighbour's recv[0]
-    const int64_t n0 = rows0 * W, n1 = rows1 * W;
-    float2* d0 = rows0 > 0 ? reinterpret_cast<float2*>(v.win[v.rank - 1] + v.off_recv1[v.rank - 1]) : nullptr;
-    float2* d1 = rows1 > 0 ? reinterpret_cast<float2*>(v.win[v.rank + 1] + v.off_recv0[v.rank + 1]) : nullptr;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n0 + n1; i += (int64_t)gridDim.x * blockDim.x) {
-        if (i < n0) d0[i] = gcur[lo0 * W + i];
-        else d1[i - n0] = gcur[lo1 * W + (i - n0)];
-    }
-    int to[2], nto = 0;
-    if (rows0 > 0) to[nto++] = v.rank - 1;
-    if (rows1 > 0) to[nto++] = v.rank + 1;
-    grid_signal(st, P2P_CH_BAND, v, to, nto, e);
-}
-
+// ---- band exchange: the stores are fused into k_adj (kernels_misc.cu) -----------------------
 // wait for the neighbours' band data (channel ch, from ranks with a band), then advance the epoch
 __global__ void k_p2p_wait(P2PView v, DevState* st, int ch, int from_left, int from_right) {
+    if (st->numeric_error) return;   // the producing k_adj skipped too (the flag is rank-consistent)
     const unsigned long long e = st->p2p_epoch[ch];
     if (from_left) flag_wait(win_flag(v, v.rank, v.rank - 1, ch), e);
     if (from_right) flag_wait(win_flag(v, v.rank, v.rank + 1, ch), e);
@@ -130,10 +92,8 @@ __global__ void k_p2p_wait_all(P2PView v, DevState* st, int ch) {
 }
 
 // ---- launchers -------------------------------------------------------------------------------
-int launch_p2p_band(const float2* gcur, int64_t lo0, int64_t rows0, int64_t lo1, int64_t rows1, int64_t W,
-                    const P2PView& v, DevState* st, int grid, cudaStream_t s) {
-    k_p2p_band_put<<<grid, 256, 0, s>>>(gcur, lo0, rows0, lo1, rows1, W, v, st);
-    k_p2p_wait<<<1, 1, 0, s>>>(v, st, P2P_CH_BAND, rows0 > 0, rows1 > 0);
+int launch_p2p_wait_band(const P2PView& v, DevState* st, int from_left, int from_right, cudaStream_t s) {
+    k_p2p_wait<<<1, 1, 0, s>>>(v, st, P2P_CH_BAND, from_left, from_right);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 

@@ -23,8 +23,32 @@ struct P2PView {
     int64_t off_recv0[P2P_MAX_RANKS], off_recv1[P2P_MAX_RANKS];
 };
 
-int launch_p2p_band(const float2* gcur, int64_t lo0, int64_t rows0, int64_t lo1, int64_t rows1, int64_t W,
-                    const P2PView& v, DevState* st, int grid, cudaStream_t s);
+#ifdef __CUDACC__
+__device__ __forceinline__ void flag_release(unsigned long long* f, unsigned long long e) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(e) : "memory");
+}
+__device__ __forceinline__ unsigned long long* win_flag(const P2PView& v, int owner, int src, int ch) {
+    return reinterpret_cast<unsigned long long*>(v.win[owner] + v.off_flags) + src * P2P_CHANNELS + ch;
+}
+// Grid-wide "all blocks stored" -> the last block raises the flags of channel ch (epoch e) in the
+// windows of the ranks to[0..nto).  st->p2p_done[ch] counts the blocks.
+__device__ __forceinline__ void grid_signal(DevState* st, int ch, const P2PView& v, const int* to, int nto,
+                                            unsigned long long e) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        const unsigned int prev = atomicAdd(&st->p2p_done[ch], 1u);
+        if (prev == gridDim.x - 1) {
+            st->p2p_done[ch] = 0;
+            __threadfence_system();
+            for (int i = 0; i < nto; ++i) flag_release(win_flag(v, to[i], v.rank, ch), e);
+        }
+    }
+}
+#endif
+
+// band receive: wait for the neighbours' flags of the current band epoch, then advance it
+int launch_p2p_wait_band(const P2PView& v, DevState* st, int from_left, int from_right, cudaStream_t s);
 int launch_p2p_allreduce(double* buf, int count, const P2PView& v, DevState* st, cudaStream_t s);
 // gathers owned rows [lo, hi) (global) of src into every window's full buffer of the current epoch
 // parity; returns that parity through *par_out (host-known: the gather epoch counter is mirrored)
