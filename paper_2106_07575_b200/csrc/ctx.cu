@@ -269,12 +269,14 @@ static int enqueue_iteration(ptyger_ctx* c, int p, std::string& err, int64_t& la
             nparts += c->band_grid;
         }
     }
-    LK(launch_reduce(c->part_adj, nparts, NDY, &c->st->dy[0], s)); ++launches;
-    if (multi) LK(allreduce(c, &c->st->dy[0], NDY, s));
+    const P2PView* fuse = (multi && c->p2p) ? &c->pv : nullptr;   // reduce + allreduce in one kernel
+    LK(launch_reduce(c->part_adj, nparts, NDY, &c->st->dy[0], s, c->st, 0, 0, fuse)); ++launches;
+    if (multi && !c->p2p) LK(allreduce(c, &c->st->dy[0], NDY, s));
     // DIR stage (Alg.1 651-656)
     LK(launch_dir(c->st, sc, s)); ++launches;
     LK(launch_eta(g, gcur, c->eta, c->st, c->part_el, c->grid_el, s)); ++launches;
-    LK(launch_reduce(c->part_el, c->grid_el, 1, &c->st->ls_pass[LS_ETA], s)); ++launches;
+    // ||eta||^2: summed over ranks here with the peer-memory transport (NCCL: with the pass-0 LS vector)
+    LK(launch_reduce(c->part_el, c->grid_el, 1, &c->st->ls_pass[LS_ETA], s, c->st, 0, 0, fuse)); ++launches;
     EV(4);
     // LS stage (Alg.1 659-668).  Pass 0 computes v = G eta and screens trials 0..K-1; every pass
     // is followed by an exact re-evaluation that runs only when the screening left it undecided;
@@ -304,13 +306,13 @@ static int enqueue_iteration(ptyger_ctx* c, int p, std::string& err, int64_t& la
             ++launches;
         }
         LK(launch_reduce(fused ? c->part_fr : c->part_el, fused ? c->parts_ls : c->grid_el, wscreen,
-                         &c->st->ls_pass[0], s, c->st, pass == 0 ? 0 : 1, pass));
+                         &c->st->ls_pass[0], s, c->st, pass == 0 ? 0 : 1, pass, fuse));
         ++launches;
-        if (multi) LK(allreduce(c, &c->st->ls_pass[0], LSW, s));
+        if (multi && !c->p2p) LK(allreduce(c, &c->st->ls_pass[0], LSW, s));
         LK(launch_pick(c->st, sc, pass, 0, 0, s)); ++launches;
         LK(launch_lsx(g, c->u, c->v, c->d, sc, pass, true, c->part_el, c->grid_el, c->st, s)); ++launches;
-        LK(launch_reduce(c->part_el, c->grid_el, LSP, &c->st->ls_pass[0], s, c->st, 2, pass)); ++launches;
-        if (multi) LK(allreduce(c, &c->st->ls_pass[0], KC, s));
+        LK(launch_reduce(c->part_el, c->grid_el, LSP, &c->st->ls_pass[0], s, c->st, 2, pass, fuse)); ++launches;
+        if (multi && !c->p2p) LK(allreduce(c, &c->st->ls_pass[0], KC, s));
         LK(launch_pick(c->st, sc, pass, 1, pass == npass - 1, s)); ++launches;
     }
     // Update stage (Alg.1 672)

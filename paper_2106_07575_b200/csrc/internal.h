@@ -108,9 +108,11 @@ int launch_ls(const Geometry& g, const float2* eta, const float2* probe, const f
 int launch_lsx(const Geometry& g, const float2* u, const float2* v, const float* d,
                const SolverCfg& c, int pass, bool exact, double* part, int grid, const DevState* st,
                cudaStream_t s);
-// mode 0: always; 1: only while no LS trial is accepted; 2: only when pass `pass` needs its exact pass
+struct P2PView;
+// mode 0: always; 1: only while no LS trial is accepted; 2: only when pass `pass` needs its exact pass.
+// pv (peer-memory transport, st required): the rank-ordered sum over ranks follows in the same kernel.
 int launch_reduce(const double* part, int nblocks, int width, double* dst, cudaStream_t s,
-                  const DevState* st = nullptr, int mode = 0, int pass = 0);
+                  const DevState* st = nullptr, int mode = 0, int pass = 0, const P2PView* pv = nullptr);
 int launch_dir(DevState* st, const SolverCfg& c, cudaStream_t s);
 int launch_eta(const Geometry& g, const float2* gcur, float2* eta, const DevState* st,
                double* part, int grid, cudaStream_t s);

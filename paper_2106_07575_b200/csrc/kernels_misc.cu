@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(256) k_band_add(float2* __restrict__ gcur, con
 // re-evaluation).  A skipped reduction leaves dst untouched and the matching k_pick ignores it.
 __global__ void __launch_bounds__(1024) k_reduce(const double* __restrict__ part, int nblocks, int width,
                                                  double* __restrict__ dst, const DevState* __restrict__ st,
-                                                 int mode, int pass) {
+                                                 int mode, int pass, P2PView pv, int p2p) {
     if (mode == 1 && (st->accepted || st->numeric_error)) return;
     if (mode == 2 && st->need_exact != pass + 1) return;
     __shared__ double sred[32][LSW];
@@ -244,6 +244,8 @@ __global__ void __launch_bounds__(1024) k_reduce(const double* __restrict__ part
         for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += sred[i][threadIdx.x];
         dst[threadIdx.x] = t;
     }
+    // peer-memory transport: the sum over ranks follows in the same kernel (reduce + allreduce)
+    if (p2p) p2p_allreduce_block(dst, width, pv, const_cast<DevState*>(st));
 }
 
 __global__ void k_set_F(DevState* st, const double* src, int keff0) {
@@ -619,8 +621,10 @@ int launch_scale_c(const float2* in, float2* out, int64_t n, float s, cudaStream
 }
 
 int launch_reduce(const double* part, int nblocks, int width, double* dst, cudaStream_t s, const DevState* st,
-                  int mode, int pass) {
-    k_reduce<<<1, 1024, 0, s>>>(part, nblocks, width, dst, st, st ? mode : 0, pass);
+                  int mode, int pass, const P2PView* pv) {
+    P2PView v{};
+    if (pv) v = *pv;
+    k_reduce<<<1, 1024, 0, s>>>(part, nblocks, width, dst, st, st ? mode : 0, pass, v, pv ? 1 : 0);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 

@@ -18,23 +18,6 @@
 
 namespace pty {
 
-__device__ __forceinline__ unsigned long long flag_acquire(const unsigned long long* f) {
-    unsigned long long v;
-    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
-    return v;
-}
-// bounded spin: a lost peer becomes a launch failure (trap) after ~tens of seconds, not a hang
-__device__ __forceinline__ void flag_wait(const unsigned long long* f, unsigned long long e) {
-    unsigned long long spins = 0;
-    while (flag_acquire(f) < e) {
-        if (++spins == (1ull << 36)) __trap();
-    }
-}
-
-__device__ __forceinline__ double* win_mail(const P2PView& v, int owner, int par, int src) {
-    return reinterpret_cast<double*>(v.win[owner] + v.off_mail) + ((int64_t)par * v.world + src) * P2P_MBW;
-}
-
 // ---- band exchange: the stores are fused into k_adj (kernels_misc.cu) -----------------------
 // wait for the neighbours' band data (channel ch, from ranks with a band), then advance the epoch
 __global__ void k_p2p_wait(P2PView v, DevState* st, int ch, int from_left, int from_right) {
@@ -47,26 +30,7 @@ __global__ void k_p2p_wait(P2PView v, DevState* st, int ch, int from_left, int f
 
 // ---- scalar allreduce (fixed rank order) ----------------------------------------------------
 __global__ void k_p2p_allreduce(double* buf, int count, P2PView v, DevState* st) {
-    const unsigned long long e = st->p2p_epoch[P2P_CH_SCALAR];
-    const int par = (int)(e & 1);
-    for (int r = 0; r < v.world; ++r) {
-        double* m = win_mail(v, r, par, v.rank);
-        for (int i = threadIdx.x; i < count; i += blockDim.x) m[i] = buf[i];
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence_system();
-        for (int r = 0; r < v.world; ++r) flag_release(win_flag(v, r, v.rank, P2P_CH_SCALAR), e);
-        for (int r = 0; r < v.world; ++r) flag_wait(win_flag(v, v.rank, r, P2P_CH_SCALAR), e);
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < count; i += blockDim.x) {
-        double s = 0.0;
-        for (int r = 0; r < v.world; ++r) s += win_mail(v, v.rank, par, r)[i];
-        buf[i] = s;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) st->p2p_epoch[P2P_CH_SCALAR] = e + 1;
+    p2p_allreduce_block(buf, count, v, st);
 }
 
 // ---- object gather: owned rows [lo, hi) of src (storage-local row 0 = global row st_lo) ----------

@@ -30,6 +30,49 @@ __device__ __forceinline__ void flag_release(unsigned long long* f, unsigned lon
 __device__ __forceinline__ unsigned long long* win_flag(const P2PView& v, int owner, int src, int ch) {
     return reinterpret_cast<unsigned long long*>(v.win[owner] + v.off_flags) + src * P2P_CHANNELS + ch;
 }
+__device__ __forceinline__ unsigned long long flag_acquire(const unsigned long long* f) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
+    return v;
+}
+// bounded spin: a lost peer becomes a launch failure (trap) after ~tens of seconds, not a hang
+__device__ __forceinline__ void flag_wait(const unsigned long long* f, unsigned long long e) {
+    unsigned long long spins = 0;
+    while (flag_acquire(f) < e) {
+        if (++spins == (1ull << 36)) __trap();
+    }
+}
+
+__device__ __forceinline__ double* win_mail(const P2PView& v, int owner, int par, int src) {
+    return reinterpret_cast<double*>(v.win[owner] + v.off_mail) + ((int64_t)par * v.world + src) * P2P_MBW;
+}
+
+// In-place fp64 sum over ranks of buf[0..count) by ONE block: own values into slot [rank] of every
+// window's mailbox (epoch parity), flags, wait for all ranks, sum the slots in rank order.
+__device__ __forceinline__ void p2p_allreduce_block(double* buf, int count, const P2PView& v, DevState* st) {
+    const unsigned long long e = st->p2p_epoch[P2P_CH_SCALAR];
+    const int par = (int)(e & 1);
+    __syncthreads();
+    for (int r = 0; r < v.world; ++r) {
+        double* m = win_mail(v, r, par, v.rank);
+        for (int i = threadIdx.x; i < count; i += blockDim.x) m[i] = buf[i];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        for (int r = 0; r < v.world; ++r) flag_release(win_flag(v, r, v.rank, P2P_CH_SCALAR), e);
+        for (int r = 0; r < v.world; ++r) flag_wait(win_flag(v, v.rank, r, P2P_CH_SCALAR), e);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < count; i += blockDim.x) {
+        double sum = 0.0;
+        for (int r = 0; r < v.world; ++r) sum += win_mail(v, v.rank, par, r)[i];
+        buf[i] = sum;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) st->p2p_epoch[P2P_CH_SCALAR] = e + 1;
+}
+
 // Grid-wide "all blocks stored" -> the last block raises the flags of channel ch (epoch e) in the
 // windows of the ranks to[0..nto).  st->p2p_done[ch] counts the blocks.
 __device__ __forceinline__ void grid_signal(DevState* st, int ch, const P2PView& v, const int* to, int nto,

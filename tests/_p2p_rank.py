@@ -39,7 +39,8 @@ def main():
     trs = tr1 + pt.iterate(3)
     obj = pt.get_object()
     np.savez(os.path.join(d, f"out{rank}.npz"), g1=g1, obj=obj, shrinks=np.array([t["shrinks"] for t in trs]),
-             F=np.array([t["F"] for t in trs]))
+             F=np.array([t["F"] for t in trs]), step=np.array([t["step_norm"] for t in trs]),
+             alpha=np.array([complex(t["alpha_re"], t["alpha_im"]) for t in trs]))
     pt.close()
 
 

@@ -52,6 +52,9 @@ def test_ranks_p2p_match_single_rank(tmp_path, world):
         assert rel(res[r]["g1"], g1) <= 1e-5, (r, rel(res[r]["g1"], g1))
         assert list(res[r]["shrinks"]) == [t["shrinks"] for t in tr]
         assert rel(res[r]["obj"], obj) <= 1e-4, (r, rel(res[r]["obj"], obj))
+        # the allreduced scalars: ||eta|| (trace step norm) and the DY alpha
+        assert rel(res[r]["step"], np.array([t["step_norm"] for t in tr])) <= 1e-4
+        assert rel(res[r]["alpha"][1:], np.array([complex(t["alpha_re"], t["alpha_im"]) for t in tr])[1:]) <= 1e-3
     for r in range(1, world):
         assert np.array_equal(res[0]["F"], res[r]["F"])     # rank-ordered sums: identical on all ranks
         assert np.array_equal(res[0]["obj"], res[r]["obj"])
