@@ -319,7 +319,8 @@ def main():
 
     # end-to-end through the public API from pinned HOST buffers (H2D + 1 iteration + D2H)
     e2e = None
-    if args.e2e_steps > 0 and world == 1 and d.numel() * 4 < 8e9:
+    if args.e2e_steps > 0 and d.numel() * 4 < 8e9 and (world == 1 or args.transport == "p2p"):
+        # every rank passes the same full host arrays; the library uploads its stripe only
         d_host = d.cpu().pin_memory()
         psi_h = torch.ones((w.H, w.W), dtype=torch.complex64).pin_memory()
         p_h = torch.from_numpy(p.astype(np.complex64)).pin_memory()
@@ -329,18 +330,31 @@ def main():
         t_list = []
         for _ in range(args.e2e_steps):
             torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
             t0 = time.perf_counter()
-            q = L.Ptyger(psi_h, p_h, scan, d_host, config=L.default_config(ls_batch=args.ls_batch, device=local))
+            q = L.Ptyger(psi_h, p_h, scan, d_host,
+                         config=L.default_config(ls_batch=args.ls_batch, device=local, rank=rank, world=world,
+                                                 transport=L.TRANSPORT_P2P))
+            if world > 1:
+                hs = [None] * world
+                dist.all_gather_object(hs, q.ipc_handle())
+                q.ipc_connect(hs)
             q.iterate(1, traces=False)
-            out = q.get_object(obj_pin)
+            out = q.get_object(obj_pin)      # collective when world > 1: every rank gets the object
             t_list.append(time.perf_counter() - t0)
             q.close()
         tm = float(np.median(t_list))
+        if world > 1:
+            tt = torch.tensor([tm], dtype=torch.float64, device=coll_dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            tm = float(tt.item())
         e2e = {"value": n / tm, "unit": UNIT, "h2d_bytes_per_step": int(d_host.numel() * 4 + psi_h.numel() * 8
                                                                           + p_h.numel() * 8 + scan.size * 4),
                "d2h_bytes_per_step": int(out.nbytes), "steps": args.e2e_steps,
                "note": "ptyger_init from pinned host buffers (H2D of d, psi0, probe, scan; u0 = G psi0, F0) + 1 CG "
-                       "iteration + ptyger_get_object (D2H), wall clock per step"}
+                       "iteration + ptyger_get_object (D2H), wall clock per step (max over ranks; per rank: the "
+                       "same full host arrays, its stripe uploaded)"}
     else:
         pt.close()
 
