@@ -428,19 +428,32 @@ def run_views(args, w, world, rank, local, dev, coll_dev=None):
                               config=L.default_config(ls_batch=args.ls_batch, device=local)))
         del d
     for q in views:
-        q.iterate(args.warmup, traces=False)
+        q.launch(args.warmup)
+    for q in views:
+        q.wait(traces=False)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     clk = ClockSampler(local)
     clk.start()
-    ms = 0.0
+    # all views enqueued on their own streams before any is waited for (they overlap on the GPU);
+    # device time of the batch = CUDA events: one start event every view stream waits on, one end
+    # event per view stream, max over the views
+    start = torch.cuda.Event(enable_timing=True)
+    start.record()
+    ends = []
+    for q in views:
+        xs = torch.cuda.ExternalStream(q.stream(), device=dev)
+        xs.wait_event(start)
+        q.launch(args.steps)
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(xs)
+        ends.append(e)
     shr = []
     for q in views:
-        tr = q.iterate(args.steps)
-        ms += q.last_iterate_ms()
-        shr += [t["shrinks"] for t in tr]
+        shr += [t["shrinks"] for t in q.wait()]
     torch.cuda.synchronize()
+    ms = max(start.elapsed_time(e) for e in ends) if ends else 0.0
     clocks = clk.stop()
     if world > 1:
         tt = torch.tensor([ms], dtype=torch.float64, device=coll_dev if coll_dev is not None else dev)

@@ -160,6 +160,16 @@ ptyger_status ptyger_init_subpixel(ptyger_ctx** out, const ptyger_config* cfg,
  */
 ptyger_status ptyger_cg_iterate(ptyger_ctx* ctx, int32_t n_iter, ptyger_trace* traces);
 
+/* Split form of ptyger_cg_iterate: cg_launch enqueues n_iter graph launches on the context's stream
+ * and returns at once; cg_wait synchronises, fills traces (nullable, n_iter entries) and reports
+ * E_NUMERIC like cg_iterate.  Independent contexts (e.g. the views of a 3-D batch) launched before
+ * waiting run concurrently on their own streams.  E_STATE: cg_launch twice without cg_wait. */
+ptyger_status ptyger_cg_launch(ptyger_ctx* ctx, int32_t n_iter);
+ptyger_status ptyger_cg_wait(ptyger_ctx* ctx, ptyger_trace* traces);
+
+/* The context's CUDA stream (cudaStream_t) -- for timing with events / ordering other work. */
+void* ptyger_stream(const ptyger_ctx* ctx);
+
 /* Current psi_m, H*W complex64 into a host buffer (Alg.1).  Collective when
  * world > 1 (every rank receives the full united object). */
 ptyger_status ptyger_get_object(ptyger_ctx* ctx, float* out);

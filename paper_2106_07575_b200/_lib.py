@@ -57,6 +57,9 @@ def _load():
         "ptyger_ipc_handle": (I32, [P, P]),
         "ptyger_ipc_connect": (I32, [P, P]),
         "ptyger_cg_iterate": (I32, [P, I32, P]),
+        "ptyger_cg_launch": (I32, [P, I32]),
+        "ptyger_cg_wait": (I32, [P, P]),
+        "ptyger_stream": (P, [P]),
         "ptyger_get_object": (I32, [P, P]),
         "ptyger_get_gradient": (I32, [P, P]),
         "ptyger_get_farfield": (I32, [P, P]),
@@ -230,6 +233,22 @@ class Ptyger:
         _check(lib.ptyger_cg_iterate(self.ctx, n_iter, tr if traces else None), self.ctx)
         return [tr[i].as_dict() for i in range(n_iter)] if traces else None
 
+    def launch(self, n_iter: int):
+        """Enqueue n_iter iterations on the context's stream without waiting (see wait())."""
+        self._pending = n_iter
+        _check(lib.ptyger_cg_launch(self.ctx, n_iter), self.ctx)
+
+    def wait(self, traces: bool = True):
+        n = getattr(self, "_pending", 0)
+        self._pending = 0
+        tr = (Trace * max(n, 1))()
+        _check(lib.ptyger_cg_wait(self.ctx, tr if traces else None), self.ctx)
+        return [tr[i].as_dict() for i in range(n)] if traces else None
+
+    def stream(self) -> int:
+        """cudaStream_t of the context (e.g. for torch.cuda.ExternalStream)."""
+        return int(lib.ptyger_stream(self.ctx) or 0)
+
     def _obj_buf(self):
         return np.empty((self.H, self.W), np.complex64)
 
@@ -304,7 +323,10 @@ class ViewBatch:
         self.views = [Ptyger(o, p, s, d, **cfg) for (o, p, s, d) in views]
 
     def iterate(self, n_iter: int, traces: bool = True):
-        return [v.iterate(n_iter, traces) for v in self.views]
+        """All views' iterations are enqueued before any is waited for: the views' streams overlap."""
+        for v in self.views:
+            v.launch(n_iter)
+        return [v.wait(traces) for v in self.views]
 
     def last_iterate_ms(self) -> float:
         return sum(v.last_iterate_ms() for v in self.views)

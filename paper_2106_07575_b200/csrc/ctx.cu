@@ -147,6 +147,7 @@ struct ptyger_ctx {
     bool c256g = false;  // ... and the cluster-of-four GRAD kernel (opt-in: slower than the slot kernel)
     int parts_ls = 0;    // per-CTA partial rows written by the LS pass-0 frame kernel
     int m_host = 0;
+    int pending_iters = 0;   // iterations launched by ptyger_cg_launch, not yet waited for
     int64_t launches_per_iter = 0, last_launches = 0;
     bool failed_numeric = false;
     // bands: [0] with rank-1, [1] with rank+1 (storage-local rows)
@@ -863,12 +864,13 @@ static ptyger_status check_numeric(ptyger_ctx* c) {
     return PTYGER_OK;
 }
 
-ptyger_status ptyger_cg_iterate(ptyger_ctx* c, int32_t n_iter, ptyger_trace* traces) {
-    if (!c) return set_err(nullptr, PTYGER_E_ARG, "cg_iterate: ctx is NULL");
+ptyger_status ptyger_cg_launch(ptyger_ctx* c, int32_t n_iter) {
+    if (!c) return set_err(nullptr, PTYGER_E_ARG, "cg_launch: ctx is NULL");
     std::string& err = c->err;
-    if (n_iter < 0) return set_err(c, PTYGER_E_ARG, "cg_iterate: n_iter < 0");
+    if (n_iter < 0) return set_err(c, PTYGER_E_ARG, "cg_launch: n_iter < 0");
     if (c->failed_numeric) return set_err(c, PTYGER_E_NUMERIC, "context is in a numeric-failure state; call set_state");
     if (!c->connected) return set_err(c, PTYGER_E_STATE, "P2P context not connected (ptyger_ipc_connect)");
+    if (c->pending_iters) return set_err(c, PTYGER_E_STATE, "cg_launch: previous launch not waited for");
     if (n_iter == 0) return PTYGER_OK;
     CK(cudaSetDevice(c->cfg.device));
     if (c->tr_cap < n_iter) {
@@ -893,11 +895,30 @@ ptyger_status ptyger_cg_iterate(ptyger_ctx* c, int32_t n_iter, ptyger_trace* tra
     }
     CK(cudaEventRecord(c->ev_it[1], c->stream));
     c->last_launches = c->launches_per_iter * n_iter;
+    c->pending_iters = n_iter;
+    return PTYGER_OK;
+}
+
+ptyger_status ptyger_cg_wait(ptyger_ctx* c, ptyger_trace* traces) {
+    if (!c) return set_err(nullptr, PTYGER_E_ARG, "cg_wait: ctx is NULL");
+    std::string& err = c->err;
+    const int n_iter = c->pending_iters;
+    if (n_iter == 0) return PTYGER_OK;
+    c->pending_iters = 0;
+    CK(cudaSetDevice(c->cfg.device));
     CK(cudaStreamSynchronize(c->stream));
     CK(cudaEventElapsedTime(&c->last_ms, c->ev_it[0], c->ev_it[1]));
     if (traces) CK(cudaMemcpy(traces, c->d_tr, sizeof(ptyger_trace) * n_iter, cudaMemcpyDeviceToHost));
     return check_numeric(c);
 }
+
+ptyger_status ptyger_cg_iterate(ptyger_ctx* c, int32_t n_iter, ptyger_trace* traces) {
+    const ptyger_status s = ptyger_cg_launch(c, n_iter);
+    if (s != PTYGER_OK) return s;
+    return ptyger_cg_wait(c, traces);
+}
+
+void* ptyger_stream(const ptyger_ctx* c) { return c ? (void*)c->stream : nullptr; }
 
 // full H*W array of a per-rank storage buffer (collective when world > 1)
 static ptyger_status gather_rows(ptyger_ctx* c, const float2* src, float* out) {
