@@ -25,6 +25,7 @@
 #include <stdint.h>
 
 #include "dev.cuh"
+#include "tma.cuh"
 
 namespace pty {
 
@@ -197,6 +198,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2)
     for (int64_t i = cid; i < nfr; i += ncl) {
         const int j = order[i];
         const int2 s = pos[j];
+        // this frame's u, d into L2 now: the epilogue reads them after both transforms
+        if (tid < 16) prefetch_l2_frame(u + (int64_t)j * N * N, N * N * 8, tid);
+        else if (tid < 24) prefetch_l2_frame(d + (int64_t)j * N * N, N * N * 4, tid - 16);
         // ---- row pass: rows 64 rank + 32 rd + rrow of p_s * eta[window]
 #pragma unroll 1
         for (int rd = 0; rd < 2; ++rd) {
@@ -237,13 +241,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2)
             float2* __restrict__ vb = v + fb;
             const float2* pk = blk + (T * ct) * HALF + cl;   // parked row 8 (jj*8 + ct) + k2
             if (cnt > 0) trial_dispatch(cnt, cfg.est, [&]<int KT, bool LSE>() {
+                float gk[KT];
+#pragma unroll
+                for (int k = 0; k < KT; ++k) gk[k] = sgam[k];
                 LsQState qs;
                 float2 un[4];
                 float dn[4];
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
-                    un[e] = ub[e * 2048];
-                    dn[e] = __ldg(db + e * 2048);
+                    un[e] = ldg2_na(ub + e * 2048);
+                    dn[e] = ldg1_na(db + e * 2048);
                 }
                 // groups g = 0..3: (jj = g >> 1, k2 = 4 (g & 1) + e)
 #pragma unroll 1
@@ -261,8 +268,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2)
                         const int gn = (((gi + 1) >> 1) << 10) + (((gi + 1) & 1) << 13);
 #pragma unroll
                         for (int e = 0; e < 4; ++e) {
-                            un[e] = ub[gn + e * 2048];
-                            dn[e] = __ldg(db + gn + e * 2048);
+                            un[e] = ldg2_na(ub + gn + e * 2048);
+                            dn[e] = ldg1_na(db + gn + e * 2048);
                         }
                     }
 #pragma unroll
@@ -270,10 +277,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2)
                         // parked row 8 (jj*8 + ct) + 4 (gi & 1) + e has parity e & 1
                         const float2 vv = pk[gp + e * HALF + (cl ^ ((e & 1) << 3)) - cl];
                         vb[go + e * 2048] = vv;
-                        ls_push<KT, LSE>(wq[warp], qs, uc[e], vv, dc[e], sgam, eps2, S, m, lane);
+                        ls_push<KT, LSE>(wq[warp], qs, uc[e], vv, dc[e], gk, eps2, S, m, lane);
                     }
                 }
-                ls_flush<KT, LSE>(wq[warp], qs, sgam, eps2, S, m, lane);
+                ls_flush<KT, LSE>(wq[warp], qs, gk, eps2, S, m, lane);
             });
             double dv[KC];
 #pragma unroll
