@@ -172,7 +172,8 @@ struct FFTCfg {
     static constexpr int LPR = NT / T;           // lines per round
     static constexpr int ROUNDS = LINES / LPR;   // rounds per pass
     static constexpr int FRAME_ELEMS = N * LD;
-    static constexpr size_t SMEM_BYTES = (size_t)(FPB * FRAME_ELEMS + N) * sizeof(float2);
+    // + N: twiddle table tw[m] = W_N^m; + R*T: the row-pass copy twr[k1*T + t] = W_N^{t k1}
+    static constexpr size_t SMEM_BYTES = (size_t)(FPB * FRAME_ELEMS + N + R * T) * sizeof(float2);
     static_assert(N * T * FPB % NT == 0 || FPB == 1, "bad config");
     static_assert(LINES % LPR == 0, "bad rounds");
 };
@@ -190,11 +191,25 @@ __device__ __forceinline__ void build_twiddles(float2* tw) {
 template <bool INV>
 __device__ __forceinline__ float2 twmul(float2 x, float2 w) { return INV ? cmulc(x, w) : cmul(x, w); }
 
+// Row-pass twiddles laid out [k1][t]: the T sub-threads of a row read T consecutive entries (the
+// tw[t k1] layout made those reads 2..8-way bank conflicted).  Same fp64-built values as tw.
+template <int N>
+__device__ __forceinline__ void build_row_twiddles(float2* twr) {
+    constexpr int R = N < 16 ? N : 16, T = N / R;
+    for (int i = threadIdx.x; i < R * T; i += blockDim.x) {
+        const int k1 = i / T, t = i % T;
+        double sn, cs;
+        sincospi(2.0 * (double)(t * k1) / (double)N, &sn, &cs);
+        twr[i] = make_float2((float)cs, (float)(-sn));
+    }
+}
+
 // ROW pass for one row: x[n1] = input element at column T*n1 + t.  Leaves the row's DFT
 // (unnormalised) in srow[0..N) in natural order.  The T threads of the row must be
 // consecutive lanes of one warp and all 32 lanes must call this together.
-template <int N, bool INV>
-__device__ __forceinline__ void row_fft(float2 (&x)[FFTCfg<N>::R], float2* srow, int t, const float2* tw) {
+template <int N, bool INV, bool TWR = false>
+__device__ __forceinline__ void row_fft(float2 (&x)[FFTCfg<N>::R], float2* srow, int t, const float2* tw,
+                                        const float2* twr = nullptr) {
     constexpr int R = FFTCfg<N>::R, T = FFTCfg<N>::T;
     DFT<R, INV>::run(x);
     if constexpr (T == 1) {
@@ -202,7 +217,12 @@ __device__ __forceinline__ void row_fft(float2 (&x)[FFTCfg<N>::R], float2* srow,
         for (int k = 0; k < R; ++k) srow[k] = x[k];
     } else {
 #pragma unroll
-        for (int k1 = 1; k1 < R; ++k1) x[k1] = twmul<INV>(x[k1], tw[t * k1]);
+        for (int k1 = 1; k1 < R; ++k1) {
+            if constexpr (TWR)
+                x[k1] = twmul<INV>(x[k1], twr[k1 * T + t]);
+            else
+                x[k1] = twmul<INV>(x[k1], tw[t * k1]);
+        }
 #pragma unroll
         for (int k1 = 0; k1 < R; ++k1) srow[T * k1 + (t ^ (k1 & (T - 1)))] = x[k1];
         __syncwarp();

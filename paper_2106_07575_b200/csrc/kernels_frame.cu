@@ -115,6 +115,7 @@ __global__ void __launch_bounds__(512, 1) k_grad(Geometry g, float2* __restrict_
     if (st->numeric_error) return;
     ktime_start(st, 0);
     build_twiddles<N>(tw);
+    build_row_twiddles<N>(tw + N);
     __syncthreads();
     const float gam = (float)st->gamma;
     const bool upd = gam != 0.0f;
@@ -154,7 +155,7 @@ __global__ void __launch_bounds__(512, 1) k_grad(Geometry g, float2* __restrict_
 #pragma unroll
                 for (int n1 = 0; n1 < R; ++n1) x[n1] = make_float2(0.f, 0.f);
             }
-            row_fft<N, true>(x, sf + f * C::FRAME_ELEMS + row * LD, t, tw);
+            row_fft<N, true, true>(x, sf + f * C::FRAME_ELEMS + row * LD, t, tw, tw + N);
         }
         __syncthreads();
 
@@ -217,6 +218,7 @@ __global__ void __launch_bounds__(512, 1) k_ls(Geometry g, const float2* __restr
     ls_pass_range(0, st->keff, cfg, base, cnt);
     ktime_start(st, 1);
     build_twiddles<N>(tw);
+    build_row_twiddles<N>(tw + N);
     if (tid < KC) sgam[tid] = (float)trial_gamma(cfg.gamma0, cfg.tau, base + tid);
     __syncthreads();
     const int64_t nfr = err ? 0 : g.n_local;
@@ -249,7 +251,7 @@ __global__ void __launch_bounds__(512, 1) k_ls(Geometry g, const float2* __restr
         };
         auto fft_row = [&](int rd, float2 (&x)[R]) {
             const int line = rd * C::LPR + tid / T, t = tid % T;
-            row_fft<N, false>(x, sf + (line / N) * C::FRAME_ELEMS + (line % N) * LD, t, tw);
+            row_fft<N, false, true>(x, sf + (line / N) * C::FRAME_ELEMS + (line % N) * LD, t, tw, tw + N);
         };
         if constexpr (C::ROUNDS == 2) {
             // both rounds' gathers in flight before the first transform (hides the L2 latency of
