@@ -249,13 +249,19 @@ __device__ __forceinline__ void row_fft(float2 (&x)[FFTCfg<N>::R], float2* srow,
 
 // ROW pass whose results stay in registers: X[j*T + k2] is column (j*T + t) + R*k2 of the row
 // (same arithmetic as row_fft; srow is used only for the exchange and is clobbered).
-template <int N, bool INV>
-__device__ __forceinline__ void row_fft_regs(float2 (&x)[FFTCfg<N>::R], float2* srow, int t, const float2* tw) {
+template <int N, bool INV, bool TWR = false>
+__device__ __forceinline__ void row_fft_regs(float2 (&x)[FFTCfg<N>::R], float2* srow, int t, const float2* tw,
+                                             const float2* twr = nullptr) {
     constexpr int R = FFTCfg<N>::R, T = FFTCfg<N>::T;
     static_assert(T > 1, "row_fft_regs needs T > 1");
     DFT<R, INV>::run(x);
 #pragma unroll
-    for (int k1 = 1; k1 < R; ++k1) x[k1] = twmul<INV>(x[k1], tw[t * k1]);
+    for (int k1 = 1; k1 < R; ++k1) {
+        if constexpr (TWR)
+            x[k1] = twmul<INV>(x[k1], twr[k1 * T + t]);
+        else
+            x[k1] = twmul<INV>(x[k1], tw[t * k1]);
+    }
     __syncwarp();
 #pragma unroll
     for (int k1 = 0; k1 < R; ++k1) srow[T * k1 + (t ^ (k1 & (T - 1)))] = x[k1];

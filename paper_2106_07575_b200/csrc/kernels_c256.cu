@@ -34,7 +34,7 @@ constexpr int SLD = N + 8;                  // row-scratch stride (complex)
 constexpr size_t BLK_BYTES = (size_t)N * QC * 8;           // 131072
 constexpr size_t SCR_OFF = BLK_BYTES;
 constexpr size_t TW_OFF = SCR_OFF + (size_t)SROWS * SLD * 8; // + 67584
-constexpr size_t DYN_BYTES = TW_OFF + (size_t)N * 8;         // 200704
+constexpr size_t DYN_BYTES = TW_OFF + (size_t)N * 8 + (size_t)R * T * 8;   // + row-pass table twr [k1][t]
 }  // namespace c256
 
 __device__ __forceinline__ uint32_t c4_mapa(uint32_t saddr, uint32_t rank) {
@@ -73,7 +73,7 @@ template <bool INV>
 __device__ __forceinline__ void c4_row(float2 (&x)[16], float2* srow, int t, const float2* tw, int row,
                                        const uint32_t (&cb)[4], bool first) {
     using namespace c256;
-    row_fft_regs<N, INV>(x, srow, t, tw);
+    row_fft_regs<N, INV, true>(x, srow, t, tw, tw + N);   // twr [k1][t] follows tw
     if (first) c4_wait();
 #pragma unroll
     for (int k2 = 0; k2 < T; ++k2)
@@ -122,6 +122,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(512, 1)
     const float gam = (float)st->gamma;
     const bool upd = gam != 0.0f;
     build_twiddles<N>(tw);
+    build_row_twiddles<N>(tw + N);
     uint32_t cb[4];
     {
         const uint32_t sb = static_cast<uint32_t>(__cvta_generic_to_shared(blk));
@@ -209,6 +210,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(512, 1)
     ls_pass_range(0, st->keff, cfg, base, cnt);
     ktime_start(st, 1);
     build_twiddles<N>(tw);
+    build_row_twiddles<N>(tw + N);
     if (tid < KC) sgam[tid] = (float)trial_gamma(cfg.gamma0, cfg.tau, base + tid);
     uint32_t cb[4];
     {

@@ -26,7 +26,7 @@ constexpr int ROWB = NT / T;      // 32 rows per pass-1 batch
 constexpr int COLB = 32;          // 32 columns per pass-2 batch
 constexpr int BUF = ROWB * LD;    // complex elements of the batch buffer (>= N * COLB)
 static_assert(BUF >= N * COLB, "buffer too small for a column batch");
-constexpr size_t SMEM = (size_t)(BUF + N) * sizeof(float2);   // + twiddle table
+constexpr size_t SMEM = (size_t)(BUF + N + R * T) * sizeof(float2);   // + twiddle tables (tw, twr [k1][t])
 }  // namespace n256
 
 // pass 2 of a 2-D transform: column batch cb (columns cb*32 .. +31) of slot (frame base `src`,
@@ -67,6 +67,7 @@ __global__ void __launch_bounds__(512, 1) k_grad256(Geometry g, float2* __restri
     if (st->numeric_error) return;
     ktime_start(st, 0);
     build_twiddles<N>(tw);
+    build_row_twiddles<N>(tw + N);
     __syncthreads();
     const float gam = (float)st->gamma;
     const bool upd = gam != 0.0f;
@@ -103,7 +104,7 @@ __global__ void __launch_bounds__(512, 1) k_grad256(Geometry g, float2* __restri
             for (int n1 = 0; n1 < R; ++n1) x[n1] = residual(uu[n1], dd[n1], eps2, g.est);
             float2* srow = buf + (tid / T) * LD;
             __syncwarp();
-            row_fft_regs<N, true>(x, srow, t, tw);
+            row_fft_regs<N, true, true>(x, srow, t, tw, tw + N);
             // x[k2] is column t + 16 k2; v of this row was consumed above, so the slot row is free
             float2* dst = vj + (int64_t)row * N + t;
 #pragma unroll
