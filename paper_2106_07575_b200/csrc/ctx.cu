@@ -306,15 +306,26 @@ static int enqueue_iteration(ptyger_ctx* c, int p, std::string& err, int64_t& la
             LK(launch_lsx(g, c->u, c->v, c->d, sc, pass, false, c->part_el, c->grid_el, c->st, s));
             ++launches;
         }
+        // the decision step rides on the reduction kernel unless an NCCL allreduce sits in between
+        const bool fuse_pick = !(multi && !c->p2p);
+        const PickArgs pk0 = {1, pass, 0, 0, sc}, pk1 = {1, pass, 1, pass == npass - 1, sc};
         LK(launch_reduce(fused ? c->part_fr : c->part_el, fused ? c->parts_ls : c->grid_el, wscreen,
-                         &c->st->ls_pass[0], s, c->st, pass == 0 ? 0 : 1, pass, fuse));
+                         &c->st->ls_pass[0], s, c->st, pass == 0 ? 0 : 1, pass, fuse, fuse_pick ? &pk0 : nullptr));
         ++launches;
         if (multi && !c->p2p) LK(allreduce(c, &c->st->ls_pass[0], LSW, s));
-        LK(launch_pick(c->st, sc, pass, 0, 0, s)); ++launches;
+        if (!fuse_pick) {
+            LK(launch_pick(c->st, sc, pass, 0, 0, s));
+            ++launches;
+        }
         LK(launch_lsx(g, c->u, c->v, c->d, sc, pass, true, c->part_el, c->grid_el, c->st, s)); ++launches;
-        LK(launch_reduce(c->part_el, c->grid_el, LSP, &c->st->ls_pass[0], s, c->st, 2, pass, fuse)); ++launches;
+        LK(launch_reduce(c->part_el, c->grid_el, LSP, &c->st->ls_pass[0], s, c->st, 2, pass, fuse,
+                         fuse_pick ? &pk1 : nullptr));
+        ++launches;
         if (multi && !c->p2p) LK(allreduce(c, &c->st->ls_pass[0], KC, s));
-        LK(launch_pick(c->st, sc, pass, 1, pass == npass - 1, s)); ++launches;
+        if (!fuse_pick) {
+            LK(launch_pick(c->st, sc, pass, 1, pass == npass - 1, s));
+            ++launches;
+        }
     }
     // Update stage (Alg.1 672)
     LK(launch_upd(g, c->psi, c->eta, c->st, c->grid_el, s)); ++launches;

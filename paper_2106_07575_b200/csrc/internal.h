@@ -109,10 +109,17 @@ int launch_lsx(const Geometry& g, const float2* u, const float2* v, const float*
                const SolverCfg& c, int pass, bool exact, double* part, int grid, const DevState* st,
                cudaStream_t s);
 struct P2PView;
+// LS decision step (k_pick) to run at the end of a reduction kernel
+struct PickArgs {
+    int on, pass, exact, last;
+    SolverCfg c;
+};
 // mode 0: always; 1: only while no LS trial is accepted; 2: only when pass `pass` needs its exact pass.
 // pv (peer-memory transport, st required): the rank-ordered sum over ranks follows in the same kernel.
+// pick: the LS decision of the pass follows in the same kernel (it also runs when the reduction is skipped).
 int launch_reduce(const double* part, int nblocks, int width, double* dst, cudaStream_t s,
-                  const DevState* st = nullptr, int mode = 0, int pass = 0, const P2PView* pv = nullptr);
+                  const DevState* st = nullptr, int mode = 0, int pass = 0, const P2PView* pv = nullptr,
+                  const PickArgs* pick = nullptr);
 int launch_dir(DevState* st, const SolverCfg& c, cudaStream_t s);
 int launch_eta(const Geometry& g, const float2* gcur, float2* eta, const DevState* st,
                double* part, int grid, cudaStream_t s);

@@ -209,6 +209,8 @@ __global__ void __launch_bounds__(256) k_band_add(float2* __restrict__ gcur, con
 // ----------------------------------------------------------------------------------------
 // Deterministic reduction of per-block partials: dst[w] = sum_b part[b*width + w].
 // ----------------------------------------------------------------------------------------
+__device__ void pick_body(DevState* st, const SolverCfg& c, int pass, int exact_mode, int last_pass);
+
 // Fixed-order fp64 reduction of per-CTA partials (width <= LSW columns): thread i sums rows
 // i, i + 1024, ... of every column in registers, then each column is reduced by a fixed warp
 // butterfly and a fixed-order sum over the 32 warps, so the result is bitwise reproducible.  One
@@ -217,9 +219,12 @@ __global__ void __launch_bounds__(256) k_band_add(float2* __restrict__ gcur, con
 // re-evaluation).  A skipped reduction leaves dst untouched and the matching k_pick ignores it.
 __global__ void __launch_bounds__(1024) k_reduce(const double* __restrict__ part, int nblocks, int width,
                                                  double* __restrict__ dst, const DevState* __restrict__ st,
-                                                 int mode, int pass, P2PView pv, int p2p) {
-    if (mode == 1 && (st->accepted || st->numeric_error)) return;
-    if (mode == 2 && st->need_exact != pass + 1) return;
+                                                 int mode, int pass, P2PView pv, int p2p, PickArgs pk) {
+    const bool skip = (mode == 1 && (st->accepted || st->numeric_error)) || (mode == 2 && st->need_exact != pass + 1);
+    if (skip) {   // nothing to reduce for this pass; its decision step still runs (pick_body)
+        if (pk.on && threadIdx.x == 0) pick_body(const_cast<DevState*>(st), pk.c, pk.pass, pk.exact, pk.last);
+        return;
+    }
     __shared__ double sred[32][LSW];
     const int wp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double acc[LSW];
@@ -246,6 +251,11 @@ __global__ void __launch_bounds__(1024) k_reduce(const double* __restrict__ part
     }
     // peer-memory transport: the sum over ranks follows in the same kernel (reduce + allreduce)
     if (p2p) p2p_allreduce_block(dst, width, pv, const_cast<DevState*>(st));
+    // the LS decision of this pass (k_pick) in the same kernel
+    if (pk.on) {
+        __syncthreads();
+        if (threadIdx.x == 0) pick_body(const_cast<DevState*>(st), pk.c, pk.pass, pk.exact, pk.last);
+    }
 }
 
 __global__ void k_set_F(DevState* st, const double* src, int keff0) {
@@ -446,7 +456,7 @@ __global__ void __launch_bounds__(256) k_lsx(int64_t count, const float2* __rest
 // decides from the first undecided trial on.  F += DeltaF_k* (R#11); after max_shrinks trials:
 // gamma = 0, stalled (R#9).  The last pass writes the trace and sets the next iteration's
 // adaptive pass-0 trial count keff = clamp(k* + 3, KMIN, K) (K after a stall).
-__global__ void k_pick(DevState* st, SolverCfg c, int pass, int exact_mode, int last_pass) {
+__device__ void pick_body(DevState* st, const SolverCfg& c, int pass, int exact_mode, int last_pass) {
     if (pass == 0 && !exact_mode) st->eta2 = st->ls_pass[LS_ETA];
     int base, cnt;
     ls_pass_range(pass, st->keff, c, base, cnt);
@@ -541,6 +551,10 @@ __global__ void k_pick(DevState* st, SolverCfg c, int pass, int exact_mode, int 
     st->keff = st->stalled ? c.K : min(c.K, max(KMIN, st->kstar + 3));
 }
 
+__global__ void k_pick(DevState* st, SolverCfg c, int pass, int exact_mode, int last_pass) {
+    pick_body(st, c, pass, exact_mode, last_pass);
+}
+
 // Update stage (Eq.5, Alg.1 672): psi <- psi + gamma eta over the storage rows.
 __global__ void __launch_bounds__(256) k_upd(Geometry g, float2* __restrict__ psi, const float2* __restrict__ eta,
                                              const DevState* __restrict__ st) {
@@ -621,10 +635,12 @@ int launch_scale_c(const float2* in, float2* out, int64_t n, float s, cudaStream
 }
 
 int launch_reduce(const double* part, int nblocks, int width, double* dst, cudaStream_t s, const DevState* st,
-                  int mode, int pass, const P2PView* pv) {
+                  int mode, int pass, const P2PView* pv, const PickArgs* pick) {
     P2PView v{};
     if (pv) v = *pv;
-    k_reduce<<<1, 1024, 0, s>>>(part, nblocks, width, dst, st, st ? mode : 0, pass, v, pv ? 1 : 0);
+    PickArgs pk{};
+    if (pick) pk = *pick;
+    k_reduce<<<1, 1024, 0, s>>>(part, nblocks, width, dst, st, st ? mode : 0, pass, v, pv ? 1 : 0, pk);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
