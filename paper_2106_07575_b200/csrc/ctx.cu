@@ -271,10 +271,17 @@ static int enqueue_iteration(ptyger_ctx* c, int p, std::string& err, int64_t& la
         }
     }
     const P2PView* fuse = (multi && c->p2p) ? &c->pv : nullptr;   // reduce + allreduce in one kernel
-    LK(launch_reduce(c->part_adj, nparts, NDY, &c->st->dy[0], s, c->st, 0, 0, fuse)); ++launches;
+    // DIR stage (Alg.1 651-656) rides on the DY reduction unless an NCCL allreduce sits in between
+    const bool fuse_dir = !(multi && !c->p2p);
+    const PickArgs pkd = {2, 0, 0, 0, sc};
+    LK(launch_reduce(c->part_adj, nparts, NDY, &c->st->dy[0], s, c->st, 0, 0, fuse, fuse_dir ? &pkd : nullptr));
+    ++launches;
     if (multi && !c->p2p) LK(allreduce(c, &c->st->dy[0], NDY, s));
     // DIR stage (Alg.1 651-656)
-    LK(launch_dir(c->st, sc, s)); ++launches;
+    if (!fuse_dir) {
+        LK(launch_dir(c->st, sc, s));
+        ++launches;
+    }
     LK(launch_eta(g, gcur, c->eta, c->st, c->part_el, c->grid_el, s)); ++launches;
     // ||eta||^2: summed over ranks here with the peer-memory transport (NCCL: with the pass-0 LS vector)
     LK(launch_reduce(c->part_el, c->grid_el, 1, &c->st->ls_pass[LS_ETA], s, c->st, 0, 0, fuse)); ++launches;

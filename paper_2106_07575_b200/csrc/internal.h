@@ -109,7 +109,7 @@ int launch_lsx(const Geometry& g, const float2* u, const float2* v, const float*
                const SolverCfg& c, int pass, bool exact, double* part, int grid, const DevState* st,
                cudaStream_t s);
 struct P2PView;
-// LS decision step (k_pick) to run at the end of a reduction kernel
+// step to run at the end of a reduction kernel: on = 1 the LS decision (k_pick), 2 the DIR step (k_dir)
 struct PickArgs {
     int on, pass, exact, last;
     SolverCfg c;

@@ -210,6 +210,7 @@ __global__ void __launch_bounds__(256) k_band_add(float2* __restrict__ gcur, con
 // Deterministic reduction of per-block partials: dst[w] = sum_b part[b*width + w].
 // ----------------------------------------------------------------------------------------
 __device__ void pick_body(DevState* st, const SolverCfg& c, int pass, int exact_mode, int last_pass);
+__device__ void dir_body(DevState* st, const SolverCfg& c);
 
 // Fixed-order fp64 reduction of per-CTA partials (width <= LSW columns): thread i sums rows
 // i, i + 1024, ... of every column in registers, then each column is reduced by a fixed warp
@@ -222,7 +223,7 @@ __global__ void __launch_bounds__(1024) k_reduce(const double* __restrict__ part
                                                  int mode, int pass, P2PView pv, int p2p, PickArgs pk) {
     const bool skip = (mode == 1 && (st->accepted || st->numeric_error)) || (mode == 2 && st->need_exact != pass + 1);
     if (skip) {   // nothing to reduce for this pass; its decision step still runs (pick_body)
-        if (pk.on && threadIdx.x == 0) pick_body(const_cast<DevState*>(st), pk.c, pk.pass, pk.exact, pk.last);
+        if (pk.on == 1 && threadIdx.x == 0) pick_body(const_cast<DevState*>(st), pk.c, pk.pass, pk.exact, pk.last);
         return;
     }
     __shared__ double sred[32][LSW];
@@ -251,10 +252,15 @@ __global__ void __launch_bounds__(1024) k_reduce(const double* __restrict__ part
     }
     // peer-memory transport: the sum over ranks follows in the same kernel (reduce + allreduce)
     if (p2p) p2p_allreduce_block(dst, width, pv, const_cast<DevState*>(st));
-    // the LS decision of this pass (k_pick) in the same kernel
+    // the LS decision of this pass (k_pick) or the DIR step (k_dir) in the same kernel
     if (pk.on) {
         __syncthreads();
-        if (threadIdx.x == 0) pick_body(const_cast<DevState*>(st), pk.c, pk.pass, pk.exact, pk.last);
+        if (threadIdx.x == 0) {
+            if (pk.on == 2)
+                dir_body(const_cast<DevState*>(st), pk.c);
+            else
+                pick_body(const_cast<DevState*>(st), pk.c, pk.pass, pk.exact, pk.last);
+        }
     }
 }
 
@@ -306,7 +312,7 @@ __global__ void k_begin_iter(DevState* st) {
 }
 
 // DIR stage (Alg.1 651-656): alpha from the reduced DY sums (Eq.8), restart rules (R#9).
-__global__ void k_dir(DevState* st, SolverCfg c) {
+__device__ void dir_body(DevState* st, const SolverCfg& c) {
     if (st->numeric_error) return;
     const double gg = st->dy[0];
     double are = 0.0, aim = 0.0;
@@ -358,6 +364,8 @@ __global__ void k_dir(DevState* st, SolverCfg c) {
     st->alpha_im = aim;
     st->restarted = restarted;
 }
+
+__global__ void k_dir(DevState* st, SolverCfg c) { dir_body(st, c); }
 
 // eta = -g + alpha eta (Eq.6) over the storage rows; ||eta||^2 over owned rows.
 __global__ void __launch_bounds__(256) k_eta(Geometry g, const float2* __restrict__ gcur, float2* __restrict__ eta,
