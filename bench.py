@@ -20,6 +20,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import subprocess
 import sys
@@ -62,6 +63,40 @@ def peaks():
         return float(pk["hbm_gbs"]), "measured"
     except Exception:
         return 6650.0, "fallback"
+
+
+def sm_max_mhz() -> float:
+    """Max SM clock for the nominal FP32 peak: MEASURED_PEAKS.json, else the B200 boost clock."""
+    try:
+        with open(PEAKS_PATH) as f:
+            return float(json.load(f)["sm_max_mhz"])
+    except Exception:
+        return 1965.0
+
+
+def lower_bound(N: int, n: int, H: int, W: int, ms_per_step: float, hbm_gbs: float, sm_mhz: float, world: int = 1):
+    """SURVEY 8(d) 'report three numbers', item 3: t_min / t_measured.  t_min = min over the cache
+    designs of max(HBM bytes / measured HBM bandwidth, flops / nominal FP32 peak) per frame and CG
+    iteration.  Bytes per frame pixel: S (u, v cached) 64, H (u only) 24, R (nothing) 8, plus 80 B
+    per object pixel; flops: 5 N^2 log2(N^2) per 2-D FFT (2 / 3 / 4 FFTs) + 124 elementwise flops per
+    pixel at K = 8.  FP32 peak: 148 SMs x 128 lanes x 2 flop x the SM clock (the paired
+    FP32 instructions are needed to reach it on sm_100)."""
+    px = float(N * N)
+    fft = 5.0 * px * math.log2(px)
+    obj = 80.0 * H * W / n
+    fp32 = 148 * 128 * 2 * sm_mhz * 1e6   # per GPU
+    bw = hbm_gbs * 1e9
+    per = {}
+    for name, bpx, nfft in (("S", 64.0, 2), ("H", 24.0, 3), ("R", 8.0, 4)):
+        b = bpx * px + obj
+        f = nfft * fft + 124.0 * px
+        per[name] = {"bytes": b, "flop": f, "ns_hbm": b / bw * 1e9, "ns_fp32": f / fp32 * 1e9,
+                     "ns": max(b / bw, f / fp32) * 1e9}
+    best = min(per, key=lambda k: per[k]["ns"])
+    t_meas = ms_per_step * 1e6 * world / n      # ns per frame per GPU
+    return {"t_min_ns_per_frame": per[best]["ns"], "design": best, "t_measured_ns_per_frame": t_meas,
+            "ratio": per[best]["ns"] / t_meas, "fp32_tflops": fp32 / 1e12, "hbm_gbs": hbm_gbs,
+            "design_S_ns_per_frame": per["S"]["ns"], "per_design": per}
 
 
 # ----------------------------------------------------------------------------- data
@@ -399,6 +434,8 @@ def main():
                                "peak_GBps": pk, "frac": it_bytes / (ms / args.steps) / 1e6 / pk},
         "stage_ms": {"begin": stage[0], "k_grad": stage[1], "k_adj": stage[2], "dir_eta": stage[3],
                      "k_ls": stage[4], "ls_rest_upd": stage[5], "iteration_eager": stage[6]},
+        "lower_bound": lower_bound(N, n, w.H, w.W, ms / args.steps, pk,
+                                   float(sm_max_mhz()), world),
         "mean_shrinks": float(np.mean(shrinks)),
         "clocks": clocks,
         "gpu_launches": int(launches),
@@ -476,6 +513,8 @@ def run_views(args, w, world, rank, local, dev, coll_dev=None):
                 "roofline": {"bound": "hbm", "kernel": "k_grad (view 0)", "achieved": algo / (stage[1] / 1e3) / 1e9,
                              "peak": pk, "peak_kind": pk_kind, "unit": "GB/s",
                              "frac": algo / (stage[1] / 1e3) / 1e9 / pk, "traffic": None},
+                "lower_bound": lower_bound(w.N, frames, w.H, w.W * nviews, ms / args.steps, pk,
+                                           float(sm_max_mhz()), 1),
                 "mean_shrinks": float(np.mean(shr)) if shr else None, "clocks": clocks,
                 "gpu_launches": int(launches), "e2e": None, "cpu_baseline": None}
         print(json.dumps(line))

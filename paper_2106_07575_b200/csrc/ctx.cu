@@ -6,6 +6,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -496,8 +497,19 @@ ptyger_status ptyger_fft2(const float* in, float* out, int32_t N, int64_t batch,
 
 // fr: nullptr, or 2n fractional offsets (row, col) in [0, 1) of bilinear windows at the integer
 // corners scan (ptyger_init_subpixel, R#22); all-zero offsets take the integer path unchanged.
+// PTYGER_INIT_TRACE=1: wall-clock milestones of ptyger_init on stderr (where init time goes)
+static void init_trace(const char* what) {
+    static const bool on = getenv("PTYGER_INIT_TRACE") && atoi(getenv("PTYGER_INIT_TRACE")) == 1;
+    static std::chrono::steady_clock::time_point t0;
+    if (!on) return;
+    const auto t = std::chrono::steady_clock::now();
+    if (what[0] == '^') t0 = t;
+    fprintf(stderr, "[ptyger init] %-28s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(t - t0).count());
+}
+
 static ptyger_status init_impl(ptyger_ctx* c, const float* object, const float* probe, const int32_t* scan,
                                const float* intensities, const float* fr = nullptr) {
+    init_trace("^start");
     std::string& err = c->err;
     const ptyger_config& cfg = c->cfg;
     const int N = c->N;
@@ -508,6 +520,7 @@ static ptyger_status init_impl(ptyger_ctx* c, const float* object, const float* 
     // ---- partition (host) ----
     const int foot = N + (c->subpx ? 1 : 0);
     const int rc = partition(scan, n, H, N, cfg.world, c->frame_rank, c->rows, err, foot);
+    init_trace("partition");
     if (rc) return (ptyger_status)rc;
     const int me = cfg.rank;
     const int64_t* R = &c->rows[6 * me];
@@ -566,6 +579,7 @@ static ptyger_status init_impl(ptyger_ctx* c, const float* object, const float* 
     }
     CK(cudaSetDevice(cfg.device));
     pool_setup(cfg.device);
+    init_trace("device set");
     CK(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, cfg.device));
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     c->p2p = cfg.world > 1 && cfg.transport == PTYGER_TRANSPORT_P2P;
@@ -659,17 +673,45 @@ static ptyger_status init_impl(ptyger_ctx* c, const float* object, const float* 
     }
 #undef AL
     CK(cudaStreamSynchronize(0));  // pool allocations and zero fills (legacy stream) are done
-    // Uploads are asynchronous on the context stream (from pinned host memory the DMA of d overlaps
-    // the graph capture below; pageable sources are staged before each call returns, so the host
-    // vectors below may go out of scope).  d first: contiguous runs of local frames.
-    for (int64_t i = 0; i < nl;) {
-        int64_t k = i;
-        while (k + 1 < nl && c->local_global[k + 1] == c->local_global[k] + 1) ++k;
-        const int64_t j0 = c->local_global[i];
-        CK(cudaMemcpyAsync(c->d + i * NN, intensities + j0 * NN, sizeof(float) * NN * (k - i + 1), cudaMemcpyDefault,
-                           c->stream));
-        i = k + 1;
-    }
+    init_trace("allocations");
+    // Uploads are asynchronous (from pinned host memory the DMA of d overlaps the host work and the
+    // graph capture below; pageable sources are staged before each call returns, so the host
+    // vectors below may go out of scope).  d first, contiguous runs of local frames, on an upload
+    // stream of its own: the small pageable copies on the context stream below would otherwise
+    // block the host until the whole d DMA ahead of them had drained (measured: init 39-54 ms for
+    // a 29.5 ms DMA of d at the paper config).  The context stream joins it before validating d.
+    cudaStream_t up = nullptr;
+    cudaEvent_t up_done = nullptr;
+    CK(cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&up_done, cudaEventDisableTiming));
+    struct UpGuard {
+        cudaStream_t& s;
+        cudaEvent_t& e;
+        ~UpGuard() {
+            if (s) cudaStreamSynchronize(s);   // error paths: no DMA into d may outlive init
+            if (e) cudaEventDestroy(e);
+            if (s) cudaStreamDestroy(s);
+        }
+    } up_guard{up, up_done};
+    // local frames [i0, i1) of d in contiguous runs.  Host-to-device copies drain in issue order,
+    // and a pageable copy returns only once it is staged, i.e. after everything issued before it:
+    // so a quarter of d goes first (its DMA covers the host work below), then psi, the small
+    // tables and the transform u_0 = G psi_0, then the rest of d while that transform runs.
+    auto issue_d = [&](int64_t i0, int64_t i1) -> cudaError_t {
+        for (int64_t i = i0; i < i1;) {
+            int64_t k = i;
+            while (k + 1 < i1 && c->local_global[k + 1] == c->local_global[k] + 1) ++k;
+            const int64_t j0 = c->local_global[i];
+            const cudaError_t e = cudaMemcpyAsync(c->d + i * NN, intensities + j0 * NN, sizeof(float) * NN * (k - i + 1),
+                                                  cudaMemcpyDefault, up);
+            if (e != cudaSuccess) return e;
+            i = k + 1;
+        }
+        return cudaSuccess;
+    };
+    const int64_t d_first = nl / 4;
+    CK(issue_d(0, d_first));
+    init_trace("d upload (1/4) issued");
     CK(cudaMemcpyAsync(c->psi, object + 2 * c->st_lo * W, sizeof(float2) * obj, cudaMemcpyDefault, c->stream));
     CK(cudaMemcpyAsync(c->probe, probe, sizeof(float2) * NN, cudaMemcpyDefault, c->stream));
     // probe / N (exact: N is a power of two) carries the unitary FFT scale of the frame kernels
@@ -687,6 +729,7 @@ static ptyger_status init_impl(ptyger_ctx* c, const float* object, const float* 
         if (!c->part_adj) return PTYGER_E_OOM;
         CK(cudaStreamSynchronize(0));   // the pool allocations above (legacy stream) are done
     }
+    init_trace("order + tiles built");
     std::vector<int2> p2(nl);
     for (int64_t i = 0; i < nl; ++i) p2[i] = make_int2(lpos[2 * i], lpos[2 * i + 1]);
     CK(cudaMemcpyAsync(c->pos, p2.data(), sizeof(int2) * nl, cudaMemcpyHostToDevice, c->stream));
@@ -703,20 +746,19 @@ static ptyger_status init_impl(ptyger_ctx* c, const float* object, const float* 
     }
     CK(cudaMemcpyAsync(c->tile_ptr, tptr.data(), sizeof(int) * tptr.size(), cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(c->entries, ent.data(), sizeof(int) * ent.size(), cudaMemcpyHostToDevice, c->stream));
-    // validate d on the device (result read after the graph capture)
+    init_trace("small uploads issued");
     unsigned long long* bad = dalloc<unsigned long long>(1, err, false);
     if (!bad) return PTYGER_E_OOM;
     {
         const unsigned long long init = ~0ull;
         CK(cudaMemcpyAsync(bad, &init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
-        LK(launch_validate_d(c->d, nl * NN, NN, bad, c->stream));
     }
     DevState hs;
     std::memset(&hs, 0, sizeof(hs));
     hs.tk_start[0] = hs.tk_start[1] = ~0ull;   // disarmed frame-kernel timers
     for (int ch = 0; ch < 4; ++ch) hs.p2p_epoch[ch] = 1;   // peer flags start at 0
     CK(cudaMemcpyAsync(c->st, &hs, sizeof(hs), cudaMemcpyHostToDevice, c->stream));
-    if (c->p2p) {   // the forward pass and the graphs need the peers: ptyger_ipc_connect
+    auto check_bad = [&]() -> ptyger_status {
         unsigned long long hb = 0;
         CK(cudaMemcpyAsync(&hb, bad, sizeof(hb), cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
@@ -726,30 +768,45 @@ static ptyger_status init_impl(ptyger_ctx* c, const float* object, const float* 
                   " has a negative or non-finite value";
             return PTYGER_E_DATA;
         }
+        return PTYGER_OK;
+    };
+    // u_0 = G psi_0 needs no d: the transform runs while the rest of d is in flight (F(psi_0) below)
+    if (!c->p2p)
+        LK(launch_fwd(c->geo, c->psi, c->probe, c->pos, c->order, nullptr, c->u, c->part_fr, c->grid_fr,
+                      (float)c->sc.eps, c->stream));
+    CK(issue_d(d_first, nl));
+    CK(cudaEventRecord(up_done, up));
+    init_trace("d upload issued");
+    if (c->p2p) {   // the forward pass and the graphs need the peers: ptyger_ipc_connect
+        CK(cudaStreamWaitEvent(c->stream, up_done, 0));   // d has landed
+        LK(launch_validate_d(c->d, nl * NN, NN, bad, c->stream));
+        const ptyger_status rs = check_bad();
+        if (rs != PTYGER_OK) return rs;
         c->connected = false;
         return PTYGER_OK;
     }
     int rc2 = build_graphs(c, err);   // host-side capture + instantiation overlaps the uploads
+    init_trace("graphs built");
     if (rc2) {
         cudaStreamSynchronize(c->stream);
         cudaFreeAsync(bad, 0);
         return (ptyger_status)rc2;
     }
-    {
-        unsigned long long hb = 0;
-        CK(cudaMemcpyAsync(&hb, bad, sizeof(hb), cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaStreamSynchronize(c->stream));
+    // d has landed: check it and form F(psi_0) (Eq.2) from u_0 and d in one pass
+    CK(cudaStreamWaitEvent(c->stream, up_done, 0));
+    LK(launch_f0_validate(c->u, c->d, nl * NN, NN, bad, c->part_fr, c->grid_fr, (float)c->sc.eps, c->geo.est,
+                          c->stream));
+    LK(launch_reduce(c->part_fr, c->grid_fr, 1, c->scratch, c->stream));
+    if (cfg.world > 1 && allreduce(c, c->scratch, 1, c->stream) != 0) {
+        cudaStreamSynchronize(c->stream);
         cudaFreeAsync(bad, 0);
-        if (hb != ~0ull) {
-            err = "intensities: frame " + std::to_string(c->local_global[(int64_t)hb]) +
-                  " has a negative or non-finite value";
-            return PTYGER_E_DATA;
-        }
+        err = "allreduce(F0) failed";
+        return PTYGER_E_NCCL;
     }
-    // F(psi_0), u_0
-    rc2 = run_forward(c, err);
-    if (rc2) return (ptyger_status)rc2;
-    return PTYGER_OK;
+    LK(launch_set_F(c->st, c->scratch, c->sc.K, c->stream));
+    const ptyger_status rs = check_bad();
+    init_trace("F0 + d check done");
+    return rs;
 }
 
 static ptyger_status create_ctx(ptyger_ctx** out, const ptyger_config* cfg_in, const float* object, int64_t H,

@@ -131,6 +131,9 @@ int launch_timers(DevState* st, double* out, int reset, cudaStream_t s);
 int launch_fold(const Geometry& g, float2* u, const float2* v, DevState* st, int grid, cudaStream_t s);
 int launch_validate_d(const float* d, int64_t count, int64_t frame_elems, unsigned long long* bad,
                       cudaStream_t s);
+// init: d >= 0 / finite check fused with the F(psi_0) partials over u_0 (part[grid])
+int launch_f0_validate(const float2* u, const float* d, int64_t count, int64_t frame_elems, unsigned long long* bad,
+                       double* part, int grid, float eps, int est, cudaStream_t s);
 int launch_set_F(DevState* st, const double* src, int keff0, cudaStream_t s);
 // half-frame cluster kernels for N = 128 (kernels_hf128.cu); probe_s = probe / N
 int hf_ls_parts(int64_t nfr);

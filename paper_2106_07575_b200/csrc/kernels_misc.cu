@@ -692,6 +692,31 @@ int launch_validate_d(const float* d, int64_t count, int64_t frame_elems, unsign
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
+// Init: the d check of k_validate_d and the F(psi_0) partials (Eq.2 per pixel, objective_term)
+// over u_0 = G psi_0 in one pass, so the transform k_fwd<d = nullptr> can run while d is still in
+// flight from the host.  Terms in fp32 (as k_fwd), sums in fp64; per-CTA partials in part[block]
+// (fixed grid, grid-stride order: deterministic).
+__global__ void __launch_bounds__(512) k_f0_validate(const float2* __restrict__ u, const float* __restrict__ d,
+                                                     int64_t count, int64_t frame_elems, unsigned long long* bad,
+                                                     double* __restrict__ part, float eps2, int est) {
+    __shared__ double sred[16];
+    double acc = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+        const float x = d[i];
+        if (!(x >= 0.0f) || isinf(x)) atomicMin(bad, (unsigned long long)(i / frame_elems));
+        const float2 uu = u[i];
+        acc += (double)objective_term(fmaf(uu.x, uu.x, uu.y * uu.y), x, eps2, est);
+    }
+    const double t = block_sum<512>(acc, sred);
+    if (threadIdx.x == 0) part[blockIdx.x] = t;
+}
+
+int launch_f0_validate(const float2* u, const float* d, int64_t count, int64_t frame_elems, unsigned long long* bad,
+                       double* part, int grid, float eps, int est, cudaStream_t s) {
+    k_f0_validate<<<grid, 512, 0, s>>>(u, d, count, frame_elems, bad, part, eps * eps, est);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
 int launch_set_F(DevState* st, const double* src, int keff0, cudaStream_t s) {
     k_set_F<<<1, 1, 0, s>>>(st, src, keff0);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
