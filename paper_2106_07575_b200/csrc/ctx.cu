@@ -695,8 +695,9 @@ static ptyger_status init_impl(ptyger_ctx* c, const float* object, const float* 
     } up_guard{up, up_done};
     // local frames [i0, i1) of d in contiguous runs.  Host-to-device copies drain in issue order,
     // and a pageable copy returns only once it is staged, i.e. after everything issued before it:
-    // so a quarter of d goes first (its DMA covers the host work below), then psi, the small
-    // tables and the transform u_0 = G psi_0, then the rest of d while that transform runs.
+    // so half of d goes first (its DMA, 15 ms at paper scale, covers the host work below: 6-12 ms
+    // measured), then psi, the small tables and the transform u_0 = G psi_0, then the rest of d
+    // while that transform runs.
     auto issue_d = [&](int64_t i0, int64_t i1) -> cudaError_t {
         for (int64_t i = i0; i < i1;) {
             int64_t k = i;
@@ -709,9 +710,9 @@ static ptyger_status init_impl(ptyger_ctx* c, const float* object, const float* 
         }
         return cudaSuccess;
     };
-    const int64_t d_first = nl / 4;
+    const int64_t d_first = nl / 2;
     CK(issue_d(0, d_first));
-    init_trace("d upload (1/4) issued");
+    init_trace("d upload (1/2) issued");
     CK(cudaMemcpyAsync(c->psi, object + 2 * c->st_lo * W, sizeof(float2) * obj, cudaMemcpyDefault, c->stream));
     CK(cudaMemcpyAsync(c->probe, probe, sizeof(float2) * NN, cudaMemcpyDefault, c->stream));
     // probe / N (exact: N is a power of two) carries the unitary FFT scale of the frame kernels
@@ -794,9 +795,11 @@ static ptyger_status init_impl(ptyger_ctx* c, const float* object, const float* 
     }
     // d has landed: check it and form F(psi_0) (Eq.2) from u_0 and d in one pass
     CK(cudaStreamWaitEvent(c->stream, up_done, 0));
-    LK(launch_f0_validate(c->u, c->d, nl * NN, NN, bad, c->part_fr, c->grid_fr, (float)c->sc.eps, c->geo.est,
+    // grid: 4 CTAs of 512 per SM (part_fr holds >= grid_fr * LSW >= that many partials)
+    const int f0_grid = (int)std::min<int64_t>((int64_t)c->grid_fr * 4, std::max<int64_t>(1, nl * NN / 2048));
+    LK(launch_f0_validate(c->u, c->d, nl * NN, NN, bad, c->part_fr, f0_grid, (float)c->sc.eps, c->geo.est,
                           c->stream));
-    LK(launch_reduce(c->part_fr, c->grid_fr, 1, c->scratch, c->stream));
+    LK(launch_reduce(c->part_fr, f0_grid, 1, c->scratch, c->stream));
     if (cfg.world > 1 && allreduce(c, c->scratch, 1, c->stream) != 0) {
         cudaStreamSynchronize(c->stream);
         cudaFreeAsync(bad, 0);

@@ -694,18 +694,28 @@ int launch_validate_d(const float* d, int64_t count, int64_t frame_elems, unsign
 
 // Init: the d check of k_validate_d and the F(psi_0) partials (Eq.2 per pixel, objective_term)
 // over u_0 = G psi_0 in one pass, so the transform k_fwd<d = nullptr> can run while d is still in
-// flight from the host.  Terms in fp32 (as k_fwd), sums in fp64; per-CTA partials in part[block]
-// (fixed grid, grid-stride order: deterministic).
-__global__ void __launch_bounds__(512) k_f0_validate(const float2* __restrict__ u, const float* __restrict__ d,
-                                                     int64_t count, int64_t frame_elems, unsigned long long* bad,
-                                                     double* __restrict__ part, float eps2, int est) {
+// flight from the host.  Four consecutive pixels per thread and step (one 16-B d load, two 16-B u
+// loads: enough bytes in flight for HBM), terms in fp32 (as k_fwd), sums in fp64; per-CTA partials
+// in part[block] (fixed grid, grid-stride order: deterministic).  count % 4 == 0 (N^2 per frame).
+__global__ void __launch_bounds__(512) k_f0_validate(const float4* __restrict__ u2, const float4* __restrict__ d4,
+                                                     int64_t count4, int64_t frame_elems,
+                                                     unsigned long long* bad, double* __restrict__ part, float eps2,
+                                                     int est) {
     __shared__ double sred[16];
     double acc = 0.0;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
-        const float x = d[i];
-        if (!(x >= 0.0f) || isinf(x)) atomicMin(bad, (unsigned long long)(i / frame_elems));
-        const float2 uu = u[i];
-        acc += (double)objective_term(fmaf(uu.x, uu.x, uu.y * uu.y), x, eps2, est);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count4; i += (int64_t)gridDim.x * blockDim.x) {
+        const float4 x = d4[i];
+        const float4 ua = u2[2 * i], ub = u2[2 * i + 1];
+        const float xs[4] = {x.x, x.y, x.z, x.w};
+        const float cs[4] = {fmaf(ua.x, ua.x, ua.y * ua.y), fmaf(ua.z, ua.z, ua.w * ua.w),
+                             fmaf(ub.x, ub.x, ub.y * ub.y), fmaf(ub.z, ub.z, ub.w * ub.w)};
+        float f = 0.f;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            if (!(xs[e] >= 0.0f) || isinf(xs[e])) atomicMin(bad, (unsigned long long)((4 * i + e) / frame_elems));
+            f += objective_term(cs[e], xs[e], eps2, est);
+        }
+        acc += (double)f;
     }
     const double t = block_sum<512>(acc, sred);
     if (threadIdx.x == 0) part[blockIdx.x] = t;
@@ -713,7 +723,9 @@ __global__ void __launch_bounds__(512) k_f0_validate(const float2* __restrict__ 
 
 int launch_f0_validate(const float2* u, const float* d, int64_t count, int64_t frame_elems, unsigned long long* bad,
                        double* part, int grid, float eps, int est, cudaStream_t s) {
-    k_f0_validate<<<grid, 512, 0, s>>>(u, d, count, frame_elems, bad, part, eps * eps, est);
+    if (count % 4) return -2;
+    k_f0_validate<<<grid, 512, 0, s>>>(reinterpret_cast<const float4*>(u), reinterpret_cast<const float4*>(d),
+                                       count / 4, frame_elems, bad, part, eps * eps, est);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 

@@ -239,6 +239,13 @@ def test_bad_data_is_rejected(L):
     d[13, 2, 3] = np.nan
     with pytest.raises(L.PtygerError):
         L.Ptyger(psi_true, p, scan, d)
+    # d is uploaded in two parts (first quarter, rest): the first bad frame is named in either part
+    d[13, 2, 3] = 1.0
+    d[2, 0, 0] = np.inf
+    d[40, 5, 5] = -2.0
+    with pytest.raises(L.PtygerError) as ei:
+        L.Ptyger(psi_true, p, scan, d)
+    assert ei.value.status == 3 and "frame 2 " in str(ei.value)
 
 
 def test_single_frame_and_device_inputs(L):
