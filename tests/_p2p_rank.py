@@ -1,4 +1,4 @@
-"""Worker for tests/test_gpu_p2p_ranks.py: one rank of a world-2 reconstruction over the peer-memory
+"""Worker for tests/test_gpu_p2p_ranks.py: one rank of a world-P reconstruction over the peer-memory
 transport (both ranks may share one GPU).  Usage: python tests/_p2p_rank.py <rank> <world> <dir>."""
 import os
 import sys
@@ -15,7 +15,7 @@ from paper_2106_07575_b200 import _lib as L  # noqa: E402
 
 def main():
     rank, world, d = int(sys.argv[1]), int(sys.argv[2]), sys.argv[3]
-    psi0, p, scan, inten = fixture()
+    psi0, p, scan, inten = fixture(world)
     psi0 = np.load(os.path.join(d, "psi0.npy"))   # warm start written by the test
     cfg = L.default_config(world=world, rank=rank, transport=L.TRANSPORT_P2P, device=0)
     pt = L.Ptyger(psi0, p, scan, inten, config=cfg)

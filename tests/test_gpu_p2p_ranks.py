@@ -1,4 +1,4 @@
-"""Multi-rank path on hardware: 2, 3 and 4 ranks (processes sharing the one GPU of the test box) run the
+"""Multi-rank path on hardware: 2, 3, 4 and 8 ranks (processes sharing the one GPU of the test box) run the
 stripe-partitioned iteration over the peer-memory transport (band exchange of partial gradients and
 rank-ordered fp64 scalar sums through CUDA-IPC-mapped windows, R#15 / R#18), compared with the
 single-rank run on the same inputs (only the summation order differs).  From a
@@ -22,13 +22,13 @@ def rel(a, b):
     return float(np.linalg.norm(a - b) / np.linalg.norm(b))
 
 
-@pytest.mark.parametrize("world", [2, 3, 4])
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
 def test_ranks_p2p_match_single_rank(tmp_path, world):
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
     from tests.p2p_fixture import fixture
     from paper_2106_07575_b200 import _lib as L
-    psi0, p, scan, d = fixture()
+    psi0, p, scan, d = fixture(world)
     warm = L.Ptyger(psi0, p, scan, d)
     warm.iterate(30, traces=False)
     psi_w = warm.get_object()
