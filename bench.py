@@ -65,6 +65,24 @@ def peaks():
         return 6650.0, "fallback"
 
 
+def host_cpu() -> dict:
+    """the CPU model and the cores available to this process (the oracle uses one)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        avail = len(os.sched_getaffinity(0))
+    except AttributeError:
+        avail = os.cpu_count()
+    return {"cpu_model": model, "cores_available": avail}
+
+
 def sm_max_mhz() -> float:
     """Max SM clock for the nominal FP32 peak: MEASURED_PEAKS.json, else the B200 boost clock."""
     try:
@@ -402,7 +420,7 @@ def main():
     if not args.no_cpu_baseline and world == 1:
         v, desc, shr, t_one = oracle_sample_run(w, args.cpu_seconds, psi_true, p, scan,
                                                 lambda k: d[:k].cpu().numpy())
-        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc}
+        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc, "host": host_cpu()}
 
     line = {
         "metric": METRIC,
@@ -547,7 +565,8 @@ def reference_arm(args, w, world, rank):
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": w.name, "H": w.H, "W": w.W, "N": w.N, "frames": w.n},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc,
+                             "host": host_cpu()},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
 
