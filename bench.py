@@ -65,6 +65,26 @@ def peaks():
         return 6650.0, "fallback"
 
 
+def frames_config(w: I.Workload, args, world: int) -> dict:
+    """The JSON line's config for a single-view workload (both arms print the same one)."""
+    n, N = w.n, w.N
+    return {"workload": f"{w.name}: {w.H}x{w.W} object, {N}^2 probe/detector, {n} frames "
+                        f"({w.k}^2 raster, step {w.step}, jitter {w.jitter}), photons {w.photons:g}, Poisson",
+            "H": w.H, "W": w.W, "N": N, "frames": n, "ls_batch": args.ls_batch,
+            "parallelism": f"stripes{world}",
+            "transport": args.transport if world > 1 else None,
+            "l2": "inputs larger than L2 (u, v, d resident in HBM: %.1f GB)" % (n * N * N * 20 / 1e9)}
+
+
+def views_config(w: I.Workload, args, world: int) -> dict:
+    """The JSON line's config for the 3-D view batch (both arms print the same one)."""
+    nviews = args.views or w.views
+    return {"workload": f"{w.name}: {nviews} views x {w.H}^2 object, {w.N}^2 detector, {w.n} frames "
+                        "per view, views sharded over ranks (no communication)",
+            "views": nviews, "frames": nviews * w.n, "parallelism": f"views{world}",
+            "l2": "inputs larger than L2"}
+
+
 def host_cpu() -> dict:
     """the CPU model and the cores available to this process (the oracle uses one)."""
     model = None
@@ -435,12 +455,7 @@ def main():
         "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic",
-        "config": {"workload": f"{w.name}: {w.H}x{w.W} object, {w.N}^2 probe/detector, {n} frames "
-                               f"({w.k}^2 raster, step {w.step}, jitter {w.jitter}), photons {w.photons:g}, Poisson",
-                   "H": w.H, "W": w.W, "N": w.N, "frames": n, "ls_batch": args.ls_batch,
-                   "parallelism": f"stripes{world}",
-                   "transport": args.transport if world > 1 else None,
-                   "l2": "inputs larger than L2 (u, v, d resident in HBM: %.1f GB)" % (n * N * N * 20 / 1e9)},
+        "config": frames_config(w, args, world),
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": pk, "peak_kind": pk_kind,
                      "unit": "GB/s", "frac": achieved / pk, "traffic": traffic,
                      "algorithmic_bytes_per_launch": algo_bytes, "avg_launch_ms": dur_ms,
@@ -524,10 +539,7 @@ def run_views(args, w, world, rank, local, dev, coll_dev=None):
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
                 "data": "synthetic",
-                "config": {"workload": f"{w.name}: {nviews} views x {w.H}^2 object, {w.N}^2 detector, {w.n} frames "
-                                       "per view, views sharded over ranks (no communication)",
-                           "views": nviews, "frames": frames, "parallelism": f"views{world}",
-                           "l2": "inputs larger than L2"},
+                "config": views_config(w, args, world),
                 "roofline": {"bound": "hbm", "kernel": "k_grad (view 0)", "achieved": algo / (stage[1] / 1e3) / 1e9,
                              "peak": pk, "peak_kind": pk_kind, "unit": "GB/s",
                              "frac": algo / (stage[1] / 1e3) / 1e9 / pk, "traffic": None},
@@ -564,7 +576,7 @@ def reference_arm(args, w, world, rank):
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": w.name, "H": w.H, "W": w.W, "N": w.N, "frames": w.n},
+            "config": views_config(w, args, world) if w.views > 1 else frames_config(w, args, world),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc,
                              "host": host_cpu()},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
