@@ -81,7 +81,7 @@ typedef struct {
     int32_t rank;         /* this process's rank, 0..world-1                              */
     int32_t world;        /* number of ranks (one GPU each)                               */
     const void* nccl_id;  /* 128-byte ncclUniqueId from ptyger_nccl_unique_id (world > 1, NCCL transport) */
-    int32_t transport;    /* world > 1: PTYGER_TRANSPORT_NCCL (default) or PTYGER_TRANSPORT_P2P        */
+    int32_t transport;    /* world > 1: PTYGER_TRANSPORT_P2P (default) or PTYGER_TRANSPORT_NCCL        */
 } ptyger_config;
 
 /* Transports of the per-iteration exchanges when world > 1 (band partial gradients, fp64 scalar
@@ -109,7 +109,7 @@ typedef struct {
 } ptyger_trace;
 
 /* Fill cfg with the paper's defaults (gamma0 1, tau 0.5, t 0, eps 1e-16, max_shrinks 32,
- * direction DY, ls_batch 16, device 0, rank 0, world 1, nccl_id NULL). */
+ * direction DY, ls_batch 16, device 0, rank 0, world 1, nccl_id NULL, transport P2P). */
 void ptyger_config_default(ptyger_config* cfg);
 
 /*

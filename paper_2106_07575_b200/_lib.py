@@ -191,10 +191,19 @@ class Ptyger:
         self.H, self.W = (o.shape[0], o.shape[1]) if o.ndim == 3 else (obj.shape[0], obj.shape[1])
         self.N = int(probe.shape[0])
         # a floating-point scan array selects the fractional-position (bilinear window) entry point
+        if hasattr(scan, "data_ptr"):   # torch tensor (host or CUDA): positions are read on the host
+            scan = scan.detach().cpu().numpy()
         self.subpixel = np.issubdtype(np.asarray(scan).dtype, np.floating)
         sc = np.ascontiguousarray(np.asarray(scan), dtype=np.float32 if self.subpixel else np.int32)
         self.n = len(sc)
-        dd = d if hasattr(d, "data_ptr") else np.ascontiguousarray(d, dtype=np.float32)
+        if hasattr(d, "data_ptr"):      # torch tensor: float32, contiguous, on its own device
+            dd = d.detach().to(dtype=__import__("torch").float32).contiguous()
+            nel = dd.numel()
+        else:
+            dd = np.ascontiguousarray(d, dtype=np.float32)
+            nel = dd.size
+        if nel != self.n * self.N * self.N:
+            raise PtygerError(3, f"intensities hold {nel} values, expected n*N*N = {self.n * self.N * self.N}")
         po, ko = _ptr(o)
         pp, kp = _ptr(p)
         pd, kd = _ptr(dd)

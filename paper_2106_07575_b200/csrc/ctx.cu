@@ -143,9 +143,6 @@ struct ptyger_ctx {
     cudaEvent_t ev_it[2] = {nullptr, nullptr};
     float last_ms = 0.f;
     int grid_fr = 0, grid_el = 0;
-    bool hf = false;     // N = 128 half-frame cluster kernels (kernels_hf128.cu)
-    bool c256 = false;   // N = 256 cluster-of-four LS kernel (kernels_c256.cu)
-    bool c256g = false;  // ... and the cluster-of-four GRAD kernel (opt-in: slower than the slot kernel)
     int parts_ls = 0;    // per-CTA partial rows written by the LS pass-0 frame kernel
     int m_host = 0;
     int pending_iters = 0;   // iterations launched by ptyger_cg_launch, not yet waited for
@@ -225,13 +222,7 @@ static int enqueue_iteration(ptyger_ctx* c, int p, std::string& err, int64_t& la
     LK(launch_begin_iter(c->st, s)); ++launches;
     EV(1);
     // GRAD stage (Alg.1 648-649)
-    if (c->hf) {
-        LK(launch_grad_hf(g, c->u, c->v, c->d, c->probe_s, c->st, eps, s));
-    } else if (c->c256g) {
-        LK(launch_grad_c256(g, c->u, c->v, c->d, c->probe_s, c->st, eps, s));
-    } else {
-        LK(launch_grad(g, c->u, c->v, c->d, c->probe, c->probe_s, c->st, eps, c->grid_fr, s));
-    }
+    LK(launch_grad(g, c->u, c->v, c->d, c->probe, c->probe_s, c->st, eps, c->grid_fr, s));
     ++launches;
     EV(2);
     LK(launch_adj(g, c->v, c->tile_ptr, c->entries, c->ntx, c->nty, gcur, gprev, c->eta, c->part_adj, c->st, s,
@@ -290,18 +281,7 @@ static int enqueue_iteration(ptyger_ctx* c, int p, std::string& err, int64_t& la
     // LS stage (Alg.1 659-668).  Pass 0 computes v = G eta and screens trials 0..K-1; every pass
     // is followed by an exact re-evaluation that runs only when the screening left it undecided;
     // further passes (trials pK..pK+K-1) run only while nothing was accepted.
-    // split mode (PTYGER_LS_SPLIT): transform-only frame kernel, then the elementwise screening
-    // kernel for pass 0 (higher occupancy for the MUFU/FMA-bound trial terms, +8 B/px of v reads)
-    const bool split = getenv("PTYGER_LS_SPLIT") != nullptr;
-    if (split) {
-        LK(launch_fwd(g, c->eta, c->probe, c->pos, c->order, nullptr, c->v, c->part_fr, c->grid_fr, (float)sc.eps, s));
-    } else if (c->hf) {
-        LK(launch_ls_hf(g, c->eta, c->probe_s, c->pos, c->order, c->u, c->v, c->d, sc, c->part_fr, c->st, s));
-    } else if (c->c256) {
-        LK(launch_ls_c256(g, c->eta, c->probe_s, c->pos, c->order, c->u, c->v, c->d, sc, c->part_fr, c->st, s));
-    } else {
-        LK(launch_ls(g, c->eta, c->probe, c->probe_s, c->pos, c->order, c->u, c->v, c->d, sc, c->part_fr, c->grid_fr, c->st, s));
-    }
+    LK(launch_ls(g, c->eta, c->probe, c->probe_s, c->pos, c->order, c->u, c->v, c->d, sc, c->part_fr, c->grid_fr, c->st, s));
     ++launches;
     EV(5);
     // pass 0 evaluates keff trials (adaptive on the device, >= KMIN), later passes K each
@@ -309,7 +289,7 @@ static int enqueue_iteration(ptyger_ctx* c, int p, std::string& err, int64_t& la
     const int npass = 1 + (rest + sc.K - 1) / sc.K;
     const int wscreen = LSP;
     for (int pass = 0; pass < npass; ++pass) {
-        const bool fused = pass == 0 && !split;
+        const bool fused = pass == 0;
         if (!fused) {
             LK(launch_lsx(g, c->u, c->v, c->d, sc, pass, false, c->part_el, c->grid_el, c->st, s));
             ++launches;
@@ -437,7 +417,7 @@ void ptyger_config_default(ptyger_config* cfg) {
     cfg->device = 0;
     cfg->rank = 0;
     cfg->world = 1;
-    cfg->transport = PTYGER_TRANSPORT_NCCL;
+    cfg->transport = PTYGER_TRANSPORT_P2P;
     cfg->nccl_id = nullptr;
 }
 
@@ -618,15 +598,11 @@ static ptyger_status init_impl(ptyger_ctx* c, const float* object, const float* 
     c->grid_fr = (int)std::max<int64_t>(1, std::min<int64_t>(c->sms, nl));
     c->grid_el = c->sms * 8;
     c->band_grid = c->sms * 2;
-    c->hf = N == 128 && !c->subpx && getenv("PTYGER_HF") && atoi(getenv("PTYGER_HF")) == 1;   // opt-in (r1_history)
-    // N = 256: the LS pass runs on clusters of four CTAs (large config: 96.7 -> 71.6 ms) unless
-    // PTYGER_N256_SLOT=1; the GRAD pass keeps the v-slot transpose kernel (51 ms; its cluster version
-    // measured 63.7 ms), the cluster one is selectable with PTYGER_N256_GRAD_C=1
-    c->c256 = N == 256 && !(getenv("PTYGER_N256_SLOT") && atoi(getenv("PTYGER_N256_SLOT")) == 1);
-    c->c256g = c->c256 && getenv("PTYGER_N256_GRAD_C") && atoi(getenv("PTYGER_N256_GRAD_C")) == 1;
-    c->parts_ls = c->hf ? hf_ls_parts(nl) : c->c256 ? c256_ls_parts(nl) : c->grid_fr;
+    // N = 256: the LS pass runs on clusters of four CTAs (large config: 96.7 -> 71.6 ms against the
+    // v-slot transpose kernel); the GRAD pass keeps the v-slot kernel (kernels_n256.cu)
+    c->parts_ls = N == 256 ? c256_ls_parts(nl) : c->grid_fr;
     if (c->parts_ls <= 0) {
-        err = "half-frame kernel setup failed";
+        err = "cluster LS kernel setup failed";
         return PTYGER_E_CUDA;
     }
     AL(c->probe_s, float2, NN);

@@ -86,13 +86,8 @@ int launch_fwd(const Geometry& g, const float2* psi, const float2* probe, const 
 // probe_s = probe / N (power-of-two scale, exact): the unitary 1/N of the FFTs rides on the probe
 int launch_grad(const Geometry& g, float2* u, float2* v, const float* d, const float2* probe,
                 const float2* probe_s, const DevState* st, float eps, int grid, cudaStream_t s);
-int launch_grad128(const Geometry& g, float2* u, float2* v, const float* d, const float2* probe_s,
-                   const DevState* st, float eps, int grid, cudaStream_t s);
 int launch_grad256(const Geometry& g, float2* u, float2* v, const float* d, const float2* probe, const DevState* st,
                    float eps, int grid, cudaStream_t s);
-int launch_ls256(const Geometry& g, const float2* eta, const float2* probe, const int2* pos, const int* order,
-                 const float2* u, float2* v, const float* d, const SolverCfg& c, double* part, int grid,
-                 const DevState* st, cudaStream_t s);
 int launch_fwd256(const Geometry& g, const float2* psi, const float2* probe, const int2* pos, const int* order,
                   const float* d, float2* u, double* part, int grid, float eps, cudaStream_t s);
 int launch_fft2_256(const float2* in, float2* out, int64_t batch, bool inv, cudaStream_t s);
@@ -135,20 +130,11 @@ int launch_validate_d(const float* d, int64_t count, int64_t frame_elems, unsign
 int launch_f0_validate(const float2* u, const float* d, int64_t count, int64_t frame_elems, unsigned long long* bad,
                        double* part, int grid, float eps, int est, cudaStream_t s);
 int launch_set_F(DevState* st, const double* src, int keff0, cudaStream_t s);
-// half-frame cluster kernels for N = 128 (kernels_hf128.cu); probe_s = probe / N
-int hf_ls_parts(int64_t nfr);
-int launch_ls_hf(const Geometry& g, const float2* eta, const float2* probe_s, const int2* pos, const int* order,
-                 const float2* u, float2* v, const float* d, const SolverCfg& c, double* part, const DevState* st,
-                 cudaStream_t s);
-int launch_grad_hf(const Geometry& g, float2* u, float2* v, const float* d, const float2* probe_s,
-                   const DevState* st, float eps, cudaStream_t s);
 // cluster-of-four frame kernels for N = 256 (kernels_c256.cu); probe_s = probe / N
 int c256_ls_parts(int64_t nfr);
 int launch_ls_c256(const Geometry& g, const float2* eta, const float2* probe_s, const int2* pos, const int* order,
                    const float2* u, float2* v, const float* d, const SolverCfg& c, double* part, const DevState* st,
                    cudaStream_t s);
-int launch_grad_c256(const Geometry& g, float2* u, float2* v, const float* d, const float2* probe_s,
-                     const DevState* st, float eps, cudaStream_t s);
 int launch_scale_c(const float2* in, float2* out, int64_t n, float s, cudaStream_t st);
 int launch_band_add(float2* gcur, const float2* recv, int64_t row_lo, int64_t rows, int64_t W,
                     const float2* gprev, const float2* eta, int64_t own_lo, int64_t own_hi,

@@ -14,8 +14,6 @@
 // across 16 threads per dimension, fp64-built twiddles, paired-FP32 complex arithmetic); the
 // unitary 1/N rides on the prescaled probe (probe_s = p / N).
 //
-//   k_grad_c256  GRAD stage frame part (Alg.1 648-649): u <- u + gamma v, r = u - d/u^*,
-//                y = conj(p) F^H r into v's slot
 //   k_ls_c256    LS pass 0 (Alg.1 659-668, Eq.7 on the Eq.2 objective): v = F(p eta[window]) and
 //                the screening partials of the pass-0 trials against (u, d)
 #include <cuda_runtime.h>
@@ -66,6 +64,9 @@ __device__ __forceinline__ void c4_arrive_relaxed() {
 }
 __device__ __forceinline__ void c4_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
 
+// The GRAD pass keeps the v-slot kernel of kernels_n256.cu: a cluster version of it measured
+// 63.7 ms against 46.6 ms at the large config (phase-locked CTAs, one per SM) and was removed.
+
 // Row pass of one row (16 sub-threads t of one row, consecutive lanes): x[n1] = input at column
 // 16 n1 + t.  After the transform x[k2] is output column t + 16 k2, owned by CTA k2 / 4 at local
 // column t + 16 (k2 % 4).  `first` (round 0): wait until every peer has released its block.
@@ -101,88 +102,6 @@ __device__ __forceinline__ void c4_col2(const float2* blk, int cl, int t, float2
 #pragma unroll
     for (int n2 = 0; n2 < T; ++n2) X[n2] = blk[(T * t + n2) * QC + cl];
     DFT<T, INV>::run(X);
-}
-
-// ----------------------------------------------------------------------------------------
-// k_grad_c256
-// ----------------------------------------------------------------------------------------
-__global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(512, 1)
-    k_grad_c256(Geometry g, float2* __restrict__ u, float2* __restrict__ v, const float* __restrict__ d,
-                const float2* __restrict__ probe_s, const DevState* __restrict__ st, float eps) {
-    using namespace c256;
-    extern __shared__ __align__(16) unsigned char smraw[];
-    float2* blk = reinterpret_cast<float2*>(smraw);
-    float2* scr = reinterpret_cast<float2*>(smraw + SCR_OFF);
-    float2* tw = reinterpret_cast<float2*>(smraw + TW_OFF);
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const uint32_t rank = c4_rank();
-    const int64_t cid = c4_id(), ncl = c4_count();
-    const bool err = st->numeric_error != 0;
-    ktime_start(st, 0);
-    const float gam = (float)st->gamma;
-    const bool upd = gam != 0.0f;
-    build_twiddles<N>(tw);
-    build_row_twiddles<N>(tw + N);
-    uint32_t cb[4];
-    {
-        const uint32_t sb = static_cast<uint32_t>(__cvta_generic_to_shared(blk));
-#pragma unroll
-        for (int q = 0; q < 4; ++q) cb[q] = c4_mapa(sb, q);
-    }
-    __syncthreads();
-    c4_arrive_relaxed();   // "my block is free" for the first frame
-    const int64_t nfr = err ? 0 : g.n_local;
-    const float eps2 = eps * eps;
-    const int rt = tid & 15, rrow = tid >> 4;
-    for (int64_t j = cid; j < nfr; j += ncl) {
-#pragma unroll 1
-        for (int rd = 0; rd < QR / SROWS; ++rd) {
-            const int row = (int)rank * QR + rd * SROWS + rrow;
-            const int64_t b0 = j * (N * N) + (int64_t)row * N + rt;
-            float2 uu[R];
-            float dd[R];
-#pragma unroll
-            for (int n1 = 0; n1 < R; ++n1) {
-                uu[n1] = u[b0 + T * n1];
-                dd[n1] = __ldg(d + b0 + T * n1);
-            }
-            if (upd) {
-                float2 vv[R];
-#pragma unroll
-                for (int n1 = 0; n1 < R; ++n1) vv[n1] = v[b0 + T * n1];
-#pragma unroll
-                for (int n1 = 0; n1 < R; ++n1) {
-                    uu[n1] = make_float2(fmaf(gam, vv[n1].x, uu[n1].x), fmaf(gam, vv[n1].y, uu[n1].y));
-                    u[b0 + T * n1] = uu[n1];
-                }
-            }
-            float2 x[R];
-#pragma unroll
-            for (int n1 = 0; n1 < R; ++n1) x[n1] = residual(uu[n1], dd[n1], eps2, g.est);
-            c4_row<true>(x, scr + rrow * SLD, rt, tw, row, cb, rd == 0);
-        }
-        c4_arrive();
-        c4_wait();   // all four quarters of every row have landed
-#pragma unroll 1
-        for (int rd = 0; rd < QC / 32; ++rd) c4_col1<true>(blk, rd * 32 + lane, warp, tw);
-        __syncthreads();
-#pragma unroll 1
-        for (int rd = 0; rd < QC / 32; ++rd) {
-            const int cl = rd * 32 + lane;
-            const int c = (int)rank * QC + cl;
-            float2 X[R];
-            c4_col2<true>(blk, cl, warp, X);
-#pragma unroll
-            for (int k2 = 0; k2 < T; ++k2) {
-                const int k = warp + R * k2;
-                v[j * (N * N) + (int64_t)k * N + c] = cconjmul(ldg2(probe_s + k * N + c), X[k2]);
-            }
-        }
-        __syncthreads();
-        c4_arrive_relaxed();
-    }
-    c4_wait();
-    ktime_end(st, 0);
 }
 
 // ----------------------------------------------------------------------------------------
@@ -322,9 +241,9 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(512, 1)
 // launchers: grid = 4 x (resident clusters, capped by the frame count)
 // ----------------------------------------------------------------------------------------
 template <typename K>
-static int c256_grid(K* kern, int slot, int64_t nfr) {
-    static int cached[2] = {0, 0};
-    if (cached[slot] == 0) {
+static int c256_grid(K* kern, int64_t nfr) {
+    static int cached = 0;
+    if (cached == 0) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c256::DYN_BYTES) !=
             cudaSuccess)
             return -1;
@@ -344,28 +263,20 @@ static int c256_grid(K* kern, int slot, int64_t nfr) {
             cudaGetLastError();
             ncl = 148 / 4;
         }
-        cached[slot] = ncl;
+        cached = ncl;
     }
-    const int64_t ncl = nfr < cached[slot] ? (nfr > 0 ? nfr : 1) : cached[slot];
+    const int64_t ncl = nfr < cached ? (nfr > 0 ? nfr : 1) : cached;
     return (int)(4 * ncl);
 }
 
-int c256_ls_parts(int64_t nfr) { return c256_grid(k_ls_c256, 0, nfr); }
+int c256_ls_parts(int64_t nfr) { return c256_grid(k_ls_c256, nfr); }
 
 int launch_ls_c256(const Geometry& g, const float2* eta, const float2* probe_s, const int2* pos, const int* order,
                    const float2* u, float2* v, const float* d, const SolverCfg& c, double* part, const DevState* st,
                    cudaStream_t s) {
-    const int grid = c256_grid(k_ls_c256, 0, g.n_local);
+    const int grid = c256_grid(k_ls_c256, g.n_local);
     if (grid < 0) return -1;
     k_ls_c256<<<grid, c256::NT, c256::DYN_BYTES, s>>>(g, eta, probe_s, pos, order, u, v, d, c, part, st);
-    return cudaGetLastError() == cudaSuccess ? 0 : -1;
-}
-
-int launch_grad_c256(const Geometry& g, float2* u, float2* v, const float* d, const float2* probe_s,
-                     const DevState* st, float eps, cudaStream_t s) {
-    const int grid = c256_grid(k_grad_c256, 1, g.n_local);
-    if (grid < 0) return -1;
-    k_grad_c256<<<grid, c256::NT, c256::DYN_BYTES, s>>>(g, u, v, d, probe_s, st, eps);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 

@@ -433,10 +433,8 @@ int launch_grad(const Geometry& g, float2* u, float2* v, const float* d, const f
         case 32: return grad_n<32>(g, u, v, d, probe_s, st, eps, grid, s);
         case 64: return grad_n<64>(g, u, v, d, probe_s, st, eps, grid, s);
         case 128:
-            // direct-load k_grad<128> (2.57 ms, 88 % of HBM at paper scale) beats the TMA-ring
-            // k_grad128 (3.13 ms) since the residual lost its division slow path; the ring kernel
-            // stays selectable for comparison (PTYGER_GRAD_TMA=1)
-            if (getenv("PTYGER_GRAD_TMA")) return launch_grad128(g, u, v, d, probe_s, st, eps, grid, s);
+            // direct-load k_grad<128> (2.57 ms, 88 % of HBM at paper scale); a TMA-ring variant
+            // (cp.async.bulk rows into a 2 x 43 KB ring) measured 3.13 ms and was removed
             return grad_n<128>(g, u, v, d, probe_s, st, eps, grid, s);
         case 256: return launch_grad256(g, u, v, d, probe, st, eps, grid, s);
     }
@@ -463,7 +461,7 @@ int launch_ls(const Geometry& g, const float2* eta, const float2* probe, const f
         case 32: return ls_n<32>(g, eta, probe_s, pos, order, u, v, d, c, part, grid, st, s);
         case 64: return ls_n<64>(g, eta, probe_s, pos, order, u, v, d, c, part, grid, st, s);
         case 128: return ls_n<128>(g, eta, probe_s, pos, order, u, v, d, c, part, grid, st, s);
-        case 256: return launch_ls256(g, eta, probe, pos, order, u, v, d, c, part, grid, st, s);
+        case 256: return launch_ls_c256(g, eta, probe_s, pos, order, u, v, d, c, part, st, s);
     }
     return -2;
 }

@@ -468,16 +468,34 @@ __device__ void pick_body(DevState* st, const SolverCfg& c, int pass, int exact_
     if (pass == 0 && !exact_mode) st->eta2 = st->ls_pass[LS_ETA];
     int base, cnt;
     ls_pass_range(pass, st->keff, c, base, cnt);
-    if (c.direction == PTYGER_DIR_GD && !exact_mode && !st->numeric_error && pass == 0) {
-        // Eq.4: the constant step gamma0 is taken whatever F does (no line search); the
-        // (screened) DeltaF only updates the cached F for the trace
-        st->ls_hist[0] = st->ls_pass[0];
-        st->ls_bnd[0] = 0.0;
-        st->n_eval = 1;
-        st->accepted = 1;
-        st->kstar = 0;
-        st->gamma = c.gamma0;
-        st->F += st->ls_pass[0];
+    if (c.direction == PTYGER_DIR_GD && !st->numeric_error && pass == 0) {
+        // Eq.4: the constant step gamma0 is taken whatever F does (no line search).  The cached F
+        // is always updated from the EXACT evaluation of DeltaF_0 (guarded definition R#4), never
+        // from the screened value, which may be non-finite where |u| < eps.
+        if (!exact_mode) {
+            st->ls_hist[0] = st->ls_pass[0];
+            st->ls_bnd[0] = LS_EPS_D * st->ls_pass[KC + 1] +
+                            LS_EPS_R * (st->ls_pass[KC] + c.gamma0 * st->ls_pass[KC + 2] +
+                                        c.gamma0 * c.gamma0 * st->ls_pass[KC + 3]);
+            st->n_eval = 1;
+            st->accepted = 1;
+            st->kstar = 0;
+            st->gamma = c.gamma0;
+            st->need_exact = 1;
+            st->k_unc = 0;
+        } else if (st->need_exact == 1) {
+            const double dF = st->ls_pass[0];
+            st->ls_hist[0] = dF;
+            st->ls_bnd[0] = 0.0;
+            st->n_exact += 1;
+            if (!isfinite(dF)) {
+                st->numeric_error = 2;
+                st->err_iter = st->m;
+                st->gamma = 0.0;
+            } else {
+                st->F += dF;
+            }
+        }
     }
     if (!st->numeric_error && !st->accepted && cnt > 0) {
         if (!exact_mode) {

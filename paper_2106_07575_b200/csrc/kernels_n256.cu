@@ -131,41 +131,28 @@ __global__ void __launch_bounds__(512, 1) k_grad256(Geometry g, float2* __restri
 }
 
 // ---------------------------------------------------------------------------------------------
-// k_ls (N = 256): v = F(p * eta[window]) (pass 1 rows -> v slot, pass 2 columns), then the LS
-// screening terms against (u, d); per-CTA partials [S | A | sum d, sum|a|, sum b].
-// k_fwd (N = 256) shares the structure: u = F(p * psi[window]) and the Eq.2 objective.
+// k_fwd (N = 256): u = F(p * psi[window]) (pass 1 rows -> u slot, pass 2 columns) and the Eq.2
+// objective partials (init / set_state; the LS pass runs on clusters of four, kernels_c256.cu).
 // ---------------------------------------------------------------------------------------------
-template <int K, bool FWD>
-__global__ void __launch_bounds__(512, 1) k_lsfwd256(Geometry g, const float2* __restrict__ obj,
-                                                     const float2* __restrict__ probe, const int2* __restrict__ pos,
-                                                     const int* __restrict__ order, float2* __restrict__ u,
-                                                     float2* __restrict__ v, const float* __restrict__ d, SolverCfg cfg,
-                                                     double* __restrict__ part, const DevState* __restrict__ st) {
+__global__ void __launch_bounds__(512, 1) k_fwd256(Geometry g, const float2* __restrict__ obj,
+                                                   const float2* __restrict__ probe, const int2* __restrict__ pos,
+                                                   const int* __restrict__ order, float2* __restrict__ u,
+                                                   const float* __restrict__ d, double* __restrict__ part, float eps) {
     using namespace n256;
     extern __shared__ float2 smem[];
     float2* buf = smem;
     float2* tw = smem + BUF;
-    __shared__ double sred[16][K];
-    __shared__ double smom[16][4];
-    __shared__ float sgam[K];
-    __shared__ LsWarpQ wq[FWD ? 1 : 16];
-    const int tid = threadIdx.x, lane = tid & 31;
-    const bool err = !FWD && st->numeric_error != 0;
-    int base = 0, cnt = 0;
-    if (!FWD) ls_pass_range(0, st->keff, cfg, base, cnt);
-    if (!FWD) ktime_start(st, 1);
+    __shared__ double sred[16];
+    const int tid = threadIdx.x;
     build_twiddles<N>(tw);
-    if (tid < K) sgam[tid] = (float)trial_gamma(cfg.gamma0, cfg.tau, base + tid);
     __syncthreads();
-    const int64_t nfr = err ? 0 : g.n_local;
-    const float eps2 = (float)(cfg.eps * cfg.eps), scale = 1.0f / (float)N;
-    float2* out = FWD ? u : v;
-    double tot = 0.0, facc = 0.0;
-    double mom[4] = {0.0, 0.0, 0.0, 0.0};
+    const int64_t nfr = g.n_local;
+    const float eps2 = eps * eps, scale = 1.0f / (float)N;
+    double facc = 0.0;
     for (int64_t i = blockIdx.x; i < nfr; i += gridDim.x) {
         const int64_t j = order[i];
         const int2 s = pos[j];
-        float2* oj = out + j * N * N;
+        float2* oj = u + j * N * N;
 #pragma unroll 1
         for (int rb = 0; rb < N / ROWB; ++rb) {
             const int row = rb * ROWB + tid / T, t = tid % T;
@@ -185,57 +172,21 @@ __global__ void __launch_bounds__(512, 1) k_lsfwd256(Geometry g, const float2* _
             int c;
             n256_column<false>(oj, cb, buf, tw, X, c);
             const int t = tid >> 5;
-            if constexpr (FWD) {
-                float fs = 0.f;
+            float fs = 0.f;
 #pragma unroll
-                for (int k2 = 0; k2 < T; ++k2) {
-                    const int64_t o = j * N * N + (int64_t)(t + R * k2) * N + c;
-                    const float2 uu = cscale(X[k2], scale);
-                    u[o] = uu;
-                    const float cc = uu.x * uu.x + uu.y * uu.y;
-                    if (d) fs += objective_term(cc, __ldg(d + o), eps2, g.est);
-                }
-                facc += (double)fs;
-            } else {
-                float S[K];
-                LsMom m;
-#pragma unroll
-                for (int kk = 0; kk < K; ++kk) S[kk] = 0.f;
-                // park X in the thread's own phase-2 rows of buf so the epilogue can be a rolled
-                // loop (instruction-cache friendly, no local-memory array)
-                float2* mine = buf + (T * t) * COLB + (c - cb * COLB);
-#pragma unroll
-                for (int k2 = 0; k2 < T; ++k2) mine[k2 * COLB] = X[k2];
-                if (cnt > 0) trial_dispatch(cnt, cfg.est, [&]<int KT, bool LSE>() {
-                    LsQState qs;
-#pragma unroll 1
-                    for (int k2 = 0; k2 < T; ++k2) {
-                        const int64_t o = j * N * N + (int64_t)(t + R * k2) * N + c;
-                        const float2 vv = cscale(mine[k2 * COLB], scale);
-                        v[o] = vv;
-                        ls_push<KT, LSE>(wq[tid >> 5], qs, u[o], vv, __ldg(d + o), sgam, eps2, S, m, lane);
-                    }
-                    ls_flush<KT, LSE>(wq[tid >> 5], qs, sgam, eps2, S, m, lane);
-                });
-                double dv[K];
-#pragma unroll
-                for (int kk = 0; kk < K; ++kk) dv[kk] = (double)S[kk];
-                tot += warp_reduce_scatter<K>(dv, lane);
-                mom[0] += (double)m.A;
-                mom[1] += (double)m.D;
-                mom[2] += (double)m.sa;
-                mom[3] += (double)m.sb;
+            for (int k2 = 0; k2 < T; ++k2) {
+                const int64_t o = j * N * N + (int64_t)(t + R * k2) * N + c;
+                const float2 uu = cscale(X[k2], scale);
+                u[o] = uu;
+                const float cc = uu.x * uu.x + uu.y * uu.y;
+                if (d) fs += objective_term(cc, __ldg(d + o), eps2, g.est);
             }
+            facc += (double)fs;
         }
         __syncthreads();
     }
-    if (FWD) {
-        const double s2 = block_sum<512>(facc, &sred[0][0]);
-        if (tid == 0) part[blockIdx.x] = s2;
-        return;
-    }
-    if (!FWD) ktime_end(st, 1);
-    ls_block_out<K, 16>(tot, mom, sred, smom, part);
+    const double s2 = block_sum<512>(facc, sred);
+    if (tid == 0) part[blockIdx.x] = s2;
 }
 
 // Batched 2-D FFT (ptyger_fft2, N = 256): pass 1 writes row transforms into `out`, pass 2 reads
@@ -295,24 +246,10 @@ int launch_grad256(const Geometry& g, float2* u, float2* v, const float* d, cons
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
-int launch_ls256(const Geometry& g, const float2* eta, const float2* probe, const int2* pos, const int* order,
-                 const float2* u, float2* v, const float* d, const SolverCfg& c, double* part, int grid,
-                 const DevState* st, cudaStream_t s) {
-    float2* uu = const_cast<float2*>(u);
-    if (n256_smem(k_lsfwd256<KC, false>)) return -1;
-    k_lsfwd256<KC, false><<<grid, 512, n256::SMEM, s>>>(g, eta, probe, pos, order, uu, v, d, c, part, st);
-    return cudaGetLastError() == cudaSuccess ? 0 : -1;
-}
-
 int launch_fwd256(const Geometry& g, const float2* psi, const float2* probe, const int2* pos, const int* order,
                   const float* d, float2* u, double* part, int grid, float eps, cudaStream_t s) {
-    SolverCfg c{};
-    c.eps = eps;
-    c.gamma0 = 1.0;
-    c.tau = 0.5;
-    c.K = 1;
-    if (n256_smem(k_lsfwd256<1, true>)) return -1;
-    k_lsfwd256<1, true><<<grid, 512, n256::SMEM, s>>>(g, psi, probe, pos, order, u, nullptr, d, c, part, nullptr);
+    if (n256_smem(k_fwd256)) return -1;
+    k_fwd256<<<grid, 512, n256::SMEM, s>>>(g, psi, probe, pos, order, u, d, part, eps);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 

@@ -368,55 +368,6 @@ def test_view_batch_equals_independent_views(L):
     vb.close()
 
 
-# ------------------------------------------------------------------ alternative N = 128 kernels
-
-@pytest.mark.parametrize("env", ["PTYGER_HF", "PTYGER_GRAD_TMA", "PTYGER_LS_SPLIT"])
-def test_alternative_n128_kernels(L, env, monkeypatch):
-    """The opt-in N = 128 paths (half-frame cluster pair with a DSMEM transpose, PTYGER_HF=1;
-    TMA-ring k_grad128, PTYGER_GRAD_TMA=1; transform-only frame kernel + elementwise screening
-    pass, PTYGER_LS_SPLIT=1) meet the same teacher-forced tolerance as the default."""
-    monkeypatch.setenv(env, "1")
-    psi_true, p, scan, d = get_fixture("n128")
-    d64 = d.astype(np.float64)
-    p64 = c128(p)
-    pt = L.Ptyger(np.ones_like(psi_true), p, scan, d)
-    for m in range(3):
-        psi_m, g_prev, eta_prev, _, _ = pt.get_state()
-        pt.set_state(psi_m, g_prev, eta_prev, m)
-        g_ref, _, _, _, u_ref = O.grad_at(c128(psi_m), c128(g_prev), c128(eta_prev), m, p64, scan, d64)
-        tr = pt.iterate(1)[0]
-        e32 = rel(O.gradient_f32(psi_m, p, scan, d), g_ref)
-        assert rel(pt.get_gradient(), g_ref) <= max(1e-4, 4 * e32)
-        _, _, eta_m, _, _ = pt.get_state()
-        v_ref = O.forward_G(c128(eta_m), p64, scan)
-        refs = [O.ls_delta(u_ref, v_ref, d64, 0.5 ** k) for k in range(tr["shrinks"] + 1)]
-        assert refs[-1] <= 0 and all(r > 0 for r in refs[:-1])
-    pt.close()
-
-
-@pytest.mark.parametrize("env", ["PTYGER_N256_SLOT", "PTYGER_N256_GRAD_C"])
-def test_alternative_n256_kernels(L, env, monkeypatch):
-    """N = 256 kernel variants: all-slot (v-slot transpose for both passes, PTYGER_N256_SLOT=1) and
-    the cluster-of-four GRAD kernel (PTYGER_N256_GRAD_C=1) meet the teacher-forced tolerance."""
-    monkeypatch.setenv(env, "1")
-    psi_true, p, scan, d = get_fixture("n256")
-    d64 = d.astype(np.float64)
-    p64 = c128(p)
-    pt = L.Ptyger(np.ones_like(psi_true), p, scan, d)
-    for m in range(3):
-        psi_m, g_prev, eta_prev, _, _ = pt.get_state()
-        pt.set_state(psi_m, g_prev, eta_prev, m)
-        g_ref, _, _, _, u_ref = O.grad_at(c128(psi_m), c128(g_prev), c128(eta_prev), m, p64, scan, d64)
-        tr = pt.iterate(1)[0]
-        e32 = rel(O.gradient_f32(psi_m, p, scan, d), g_ref)
-        assert rel(pt.get_gradient(), g_ref) <= max(1e-4, 4 * e32)
-        _, _, eta_m, _, _ = pt.get_state()
-        v_ref = O.forward_G(c128(eta_m), p64, scan)
-        refs = [O.ls_delta(u_ref, v_ref, d64, 0.5 ** k) for k in range(tr["shrinks"] + 1)]
-        assert refs[-1] <= 0 and all(r > 0 for r in refs[:-1])
-    pt.close()
-
-
 def test_kernel_timers_cover_every_launch(L):
     """ptyger_kernel_times: one GRAD and one LS pass-0 launch per iteration, positive durations that
     fit inside the iteration time, and reset semantics."""

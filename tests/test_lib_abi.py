@@ -98,8 +98,12 @@ def test_init_validation_before_device(L):
         L.Ptyger(psi, p, scan, d, ls_batch=17)
     assert ei.value.status == 2
     with pytest.raises(L.PtygerError) as ei:
-        L.Ptyger(np.ones((64, 64), complex), np.ones((24, 24), complex), scan, d)
+        L.Ptyger(np.ones((64, 64), complex), np.ones((24, 24), complex), scan, np.ones((len(scan), 24, 24), np.float32))
     assert ei.value.status == 2
+    # intensities that do not hold n*N*N values are rejected before any pointer reaches the library
+    with pytest.raises(L.PtygerError) as ei:
+        L.Ptyger(psi, p, scan, d[:-1])
+    assert ei.value.status == 3 and "n*N*N" in str(ei.value)
 
 
 def test_header_documents_boundary():
