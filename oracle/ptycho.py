@@ -114,18 +114,43 @@ def scatter_add_bilinear(acc: np.ndarray, patch: np.ndarray, pos) -> None:
         acc[r:r + N, c:c + N] += w * patch
 
 
+# FFT_WORKERS > 1: the same unitary transform from scipy.fft with that many threads (a library
+# primitive of the same step; the pins in tests/test_oracle_operators.py cover both backends).  Used
+# by large-size parity checks and the multi-core CPU baseline variant; 1 = NumPy.
+FFT_WORKERS = 1
+
+
+def set_fft_workers(n: int) -> None:
+    global FFT_WORKERS
+    FFT_WORKERS = max(1, int(n))
+
+
 def ufft2(x: np.ndarray) -> np.ndarray:
     """Unitary 2-D DFT, e^{-2 pi i k.n/N}, DC at [0,0], no shift (R#1, R#2).
 
     F in Eq.1.  Scale 1/N per 2-D transform so F^H = F^{-1}.
     Applied over the last two axes.
     """
+    if FFT_WORKERS > 1:
+        import scipy.fft
+        return scipy.fft.fft2(x, norm="ortho", workers=FFT_WORKERS)
     return np.fft.fft2(x, norm="ortho")
 
 
 def uifft2(x: np.ndarray) -> np.ndarray:
     """Unitary inverse 2-D DFT = F^H ("F^H is the inverse Fourier transform")."""
+    if FFT_WORKERS > 1:
+        import scipy.fft
+        return scipy.fft.ifft2(x, norm="ortho", workers=FFT_WORKERS)
     return np.fft.ifft2(x, norm="ortho")
+
+
+def forward_G_batch(psi: np.ndarray, probe: np.ndarray, scan: np.ndarray) -> np.ndarray:
+    """forward_G with the windows of all frames stacked and transformed in one batched call (same
+    arithmetic per frame: p * window, then ufft2 over the last two axes).  Integer positions only."""
+    N = probe.shape[0]
+    win = np.stack([extract(psi, s, N) for s in scan]) if len(scan) else np.zeros((0, N, N), psi.dtype)
+    return ufft2(probe * win)
 
 
 def forward_G(psi: np.ndarray, probe: np.ndarray, scan: np.ndarray) -> np.ndarray:

@@ -102,6 +102,31 @@ def random_complex(shape, seed: int, scale: float = 1.0) -> np.ndarray:
     return scale * (rng.standard_normal(shape) + 1j * rng.standard_normal(shape))
 
 
+def smooth_field(shape, seed: int, modes: int = 6) -> np.ndarray:
+    """Smooth complex random field (a few low-frequency separable cosine modes, 1..3 periods across
+    the image), scaled to max |.| = 1.  Used to build well-conditioned object states."""
+    rng = np.random.default_rng(seed)
+    H, W = shape
+    yy, xx = np.meshgrid(np.arange(H) / H, np.arange(W) / W, indexing="ij")
+    out = np.zeros(shape, np.complex128)
+    for _ in range(modes):
+        a, b = rng.integers(1, 4, 2)
+        ph = rng.uniform(0.0, 2.0 * np.pi, 2)
+        amp = rng.standard_normal() + 1j * rng.standard_normal()
+        out += amp * np.cos(2 * np.pi * a * yy + ph[0]) * np.cos(2 * np.pi * b * xx + ph[1])
+    return out / np.abs(out).max()
+
+
+def conditioned_state(psi_true: np.ndarray, photons: float, seed: int = 5) -> np.ndarray:
+    """A well-conditioned object state for parity checks at production sizes:
+    sqrt(photons) psi_true (1.2 + 0.2 S), S = smooth_field.  Near the data's scale (R#14: the ML
+    solution is ~ sqrt(photons) psi_true) but 20 % off in amplitude with a smooth complex
+    modulation, so the gradient is far from zero and G psi has no near-zeros where d > 0 (a white
+    perturbation or the flat psi_0 = 1 produces speckle zeros that make the float32 residual
+    d/u* ill-conditioned)."""
+    return np.sqrt(photons) * psi_true * (1.2 + 0.2 * smooth_field(psi_true.shape, seed))
+
+
 def workload_inputs(w: Workload):
     """(psi_true, probe, scan) for a workload; data are the caller's job."""
     img = siemens_star(w.H, w.W)

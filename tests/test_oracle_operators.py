@@ -112,3 +112,32 @@ def test_linearity():
     lhs = O.forward_G(0.3 * a + (0.2 - 1j) * b, p, scan)
     rhs = 0.3 * O.forward_G(a, p, scan) + (0.2 - 1j) * O.forward_G(b, p, scan)
     assert np.max(np.abs(lhs - rhs)) < 1e-12 * np.max(np.abs(lhs))
+
+
+@pytest.fixture
+def scipy_workers():
+    O.set_fft_workers(4)
+    yield
+    O.set_fft_workers(1)
+
+
+@pytest.mark.parametrize("N", [4, 8, 16])
+def test_scipy_backend_matches_brute_force(N, scipy_workers):
+    """FFT_WORKERS > 1 switches ufft2 / uifft2 to scipy.fft: the same brute-force pins hold."""
+    x = I.random_complex((N, N), seed=N + 1)
+    assert np.max(np.abs(O.ufft2(x) - brute_dft2(x))) < 1e-12 * max(1.0, np.max(np.abs(x))) * N
+    assert np.max(np.abs(O.uifft2(O.ufft2(x)) - x)) < 1e-13
+
+
+def test_forward_G_batch_equals_per_frame():
+    H, N = 48, 16
+    psi = I.random_complex((H, H), seed=4)
+    p = I.make_probe(N)
+    scan = I.make_scan(H, H, N, 4, 10, 1, 2)
+    ref = O.forward_G(psi, p, scan)
+    assert np.max(np.abs(O.forward_G_batch(psi, p, scan) - ref)) < 1e-13 * np.max(np.abs(ref))
+    O.set_fft_workers(3)
+    try:
+        assert np.max(np.abs(O.forward_G_batch(psi, p, scan) - ref)) < 1e-12 * np.max(np.abs(ref))
+    finally:
+        O.set_fft_workers(1)

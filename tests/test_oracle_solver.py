@@ -292,3 +292,34 @@ def test_gradient_f32_yardstick_tracks_fp64(est):
     assert e < 1e-5
     g_nodata = O.adjoint_GH(far, p, scan, psi.shape)
     assert np.linalg.norm(g_nodata - g64) / np.linalg.norm(g64) > 1e-2
+
+
+def test_pr_plus_clip():
+    """PR+ (R#20): beta = max(0, Re<g, g - g_prev>) / ||g_prev||^2.  g_prev = 2 g makes the
+    numerator -||g||^2 < 0, so the clip must give beta = 0 and eta = -g exactly (a dropped clip
+    gives beta = -1/4); g_prev = g / 2 gives the closed form beta = (||g||^2 / 2) / (||g||^2 / 4) = 2."""
+    g = I.random_complex((5, 5), seed=31)
+    eta_prev = I.random_complex((5, 5), seed=32)
+    eta, beta, rs = O.polak_ribiere(g, 2.0 * g, eta_prev)
+    assert beta == 0 and not rs and np.array_equal(eta, -g)
+    eta, beta, rs = O.polak_ribiere(g, 0.5 * g, eta_prev)
+    assert abs(beta - 2.0) < 1e-13 and not rs
+    assert np.max(np.abs(eta - (-g + 2.0 * eta_prev))) < 1e-13
+
+
+def test_cg_converges_faster_than_steepest_descent():
+    """conjugate directions converge faster than gradient descent.  Both runs use the
+    same Eq.7 line search from psi_0 = 1 on the tiny fixture with Poisson data (photons 1e3, the
+    setting the ML estimator is built for); steepest descent is the same iteration with eta = -g
+    every time (the state's m reset to 0).  Measured F: DY 2112 / 1959 against SD 2177 / 2022 after
+    40 / 100 iterations.  (On the NOISELESS tiny fixture steepest descent with this backtracking line
+    search is ahead of DY-complex at every checkpoint up to 100 iterations: DESIGN.md R#23.)"""
+    psi_true, p, scan, d = tiny_problem(noisy=True)
+    _, trs = O.run_cg(np.ones_like(psi_true), p, scan, d, 100)
+    st = O.CGState(psi=np.ones_like(psi_true))
+    sd = {}
+    for it in range(100):
+        st, tr, _, _ = O.cg_iterate(O.CGState(psi=st.psi, F=st.F, m=0), p, scan, d)
+        sd[it + 1] = tr.F
+    for it in (40, 100):
+        assert trs[it - 1].F < sd[it] - 20.0, (it, trs[it - 1].F, sd[it])
