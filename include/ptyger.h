@@ -106,6 +106,12 @@ typedef struct {
     double alpha_im;
     double grad_norm;     /* ||grad F(psi_m)||_2                                          */
     double step_norm;     /* gamma ||eta_m||_2                                            */
+    /* device time of this iteration's stages (ms, GPU global timer stamps between the stages of the
+     * graph-launched iteration; SURVEY 8(b), P:284-287 time breakdown): GRAD (frame kernel + adjoint,
+     * incl. the band exchange when world > 1), DIR (DY sums, alpha, eta), LS (all passes and
+     * decisions), Update; ms_comm = the band-exchange part of ms_grad (0 when world = 1; the fp64
+     * scalar sums over ranks ride inside the DIR / LS reductions). */
+    float ms_grad, ms_dir, ms_ls, ms_update, ms_comm;
 } ptyger_trace;
 
 /* Fill cfg with the paper's defaults (gamma0 1, tau 0.5, t 0, eps 1e-16, max_shrinks 32,
@@ -247,11 +253,12 @@ const char* ptyger_last_error(const ptyger_ctx* ctx);
  * from before its first graph launch to after its last. */
 float ptyger_last_iterate_ms(const ptyger_ctx* ctx);
 
-/* Run n_iter REAL iterations eagerly (no graph) with CUDA events between the kernels and
- * accumulate device ms into ms[7]: [0] begin, [1] k_grad, [2] k_adj, [3] DY reduce + DIR +
- * eta (+ band exchange / allreduce), [4] k_ls, [5] LS reduce/pick/extra passes + update,
- * [6] whole iteration.  For the bench roofline (kernel duration on its launching stream). */
-ptyger_status ptyger_stage_times(ptyger_ctx* ctx, int32_t n_iter, double* ms);
+/* Measured FP32 FMA-pipe peak of `device` in TFLOP/s (the FP32 roofline of the lower
+ * bound t_min): a microbenchmark kernel of independent fma chains on every SM, 2 flop per FMA lane-op,
+ * best of three timed launches.  paired != 0: Blackwell's paired FFMA2 (fma.rn.f32x2, the form the
+ * frame kernels use), else scalar FFMA.  Runs on the legacy default stream of `device` and makes it
+ * current.  Errors: E_ARG (null), E_CUDA (no such device / launch failure). */
+ptyger_status ptyger_fp32_peak(int32_t device, int32_t paired, double* tflops);
 
 /* Number of kernel launches the last ptyger_cg_iterate call issued (graph nodes counted). */
 int64_t ptyger_kernel_launches(const ptyger_ctx* ctx);

@@ -38,7 +38,9 @@ class Config(C.Structure):
 class Trace(C.Structure):
     _fields_ = [("iter", C.c_int32), ("shrinks", C.c_int32), ("restarted", C.c_int32), ("stalled", C.c_int32),
                 ("F", C.c_double), ("gamma", C.c_double), ("alpha_re", C.c_double), ("alpha_im", C.c_double),
-                ("grad_norm", C.c_double), ("step_norm", C.c_double)]
+                ("grad_norm", C.c_double), ("step_norm", C.c_double),
+                ("ms_grad", C.c_float), ("ms_dir", C.c_float), ("ms_ls", C.c_float), ("ms_update", C.c_float),
+                ("ms_comm", C.c_float)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -73,8 +75,8 @@ def _load():
         "ptyger_last_error": (C.c_char_p, [P]),
         "ptyger_kernel_launches": (I64, [P]),
         "ptyger_last_iterate_ms": (C.c_float, [P]),
-        "ptyger_stage_times": (I32, [P, I32, P]),
         "ptyger_kernel_times": (I32, [P, P, P, I32]),
+        "ptyger_fp32_peak": (I32, [I32, I32, P]),
         "ptyger_destroy": (None, [P]),
         "ptyger_version": (C.c_char_p, []),
     }
@@ -168,6 +170,13 @@ def fft2(x, inverse: bool = False, out=None):
     stream = torch.cuda.current_stream(x.device).cuda_stream
     _check(lib.ptyger_fft2(x.data_ptr(), out.data_ptr(), N, batch, int(inverse), stream))
     return out
+
+
+def fp32_peak(device: int = 0, paired: bool = True) -> float:
+    """Measured FP32 FMA-pipe peak of the device in TFLOP/s (ptyger_fp32_peak)."""
+    out = C.c_double()
+    _check(lib.ptyger_fp32_peak(device, int(paired), C.byref(out)))
+    return float(out.value)
 
 
 def nccl_unique_id() -> bytes:
@@ -304,11 +313,6 @@ class Ptyger:
 
     def last_iterate_ms(self) -> float:
         return float(lib.ptyger_last_iterate_ms(self.ctx))
-
-    def stage_times(self, n_iter: int):
-        ms = np.zeros(7, np.float64)
-        _check(lib.ptyger_stage_times(self.ctx, n_iter, ms.ctypes.data), self.ctx)
-        return ms
 
     def kernel_times(self, reset: bool = True):
         """{"k_grad": (total ms, launches), "k_ls": (total ms, launches)} since the last reset."""

@@ -13,7 +13,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libptyger.so")
 OBJ = os.path.join(PKG, "_build")
-SOURCES = ["kernels_frame.cu", "kernels_c256.cu", "kernels_p2p.cu", "kernels_n256.cu", "kernels_misc.cu", "kernels_fft.cu", "ctx.cu",
+SOURCES = ["kernels_frame.cu", "kernels_ls128.cu", "kernels_c256.cu", "kernels_p2p.cu", "kernels_n256.cu", "kernels_misc.cu", "kernels_fft.cu", "kernels_peak.cu", "ctx.cu",
            "host.cpp"]
 HEADERS = ["fft.cuh", "dev.cuh", "tma.cuh", "internal.h", "host.h", "p2p.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -206,11 +206,8 @@ static int allreduce(ptyger_ctx* c, double* buf, int count, cudaStream_t s) {
 // One iteration as a sequence of launches on c->stream (captured into a graph).
 // parity p: gcur = g[p], gprev = g[1-p].
 // ------------------------------------------------------------------------------------------
-static int enqueue_iteration(ptyger_ctx* c, int p, std::string& err, int64_t& launches,
-                             cudaEvent_t* ev = nullptr) {
+static int enqueue_iteration(ptyger_ctx* c, int p, std::string& err, int64_t& launches) {
     const bool multi = c->cfg.world > 1;
-#define EV(i) \
-    if (ev) CK(cudaEventRecord(ev[i], c->stream))
     float2* gcur = c->g[p];
     float2* gprev = c->g[1 - p];
     cudaStream_t s = c->stream;
@@ -218,18 +215,18 @@ static int enqueue_iteration(ptyger_ctx* c, int p, std::string& err, int64_t& la
     const SolverCfg& sc = c->sc;
     const float eps = (float)sc.eps;
     launches = 0;
-    EV(0);
-    LK(launch_begin_iter(c->st, s)); ++launches;
-    EV(1);
+    LK(launch_begin_iter(c->st, s)); ++launches;   // stage stamp 0
     // GRAD stage (Alg.1 648-649)
     LK(launch_grad(g, c->u, c->v, c->d, c->probe, c->probe_s, c->st, eps, c->grid_fr, s));
     ++launches;
-    EV(2);
     LK(launch_adj(g, c->v, c->tile_ptr, c->entries, c->ntx, c->nty, gcur, gprev, c->eta, c->part_adj, c->st, s,
                   (multi && c->p2p) ? &c->pv : nullptr));
     ++launches;
-    EV(3);
     int nparts = c->ntx * c->nty;
+    if (multi) {
+        LK(launch_stamp(c->st, 5, s));   // adjoint done, band exchange next
+        ++launches;
+    }
     if (multi && c->p2p) {
         // band exchange fused into k_adj (its band tiles stored into the neighbours' windows and its
         // last tile raised the flags); wait for the neighbours' bands, then add them
@@ -262,6 +259,8 @@ static int enqueue_iteration(ptyger_ctx* c, int p, std::string& err, int64_t& la
             nparts += c->band_grid;
         }
     }
+    LK(launch_stamp(c->st, 1, s));   // GRAD stage done
+    ++launches;
     const P2PView* fuse = (multi && c->p2p) ? &c->pv : nullptr;   // reduce + allreduce in one kernel
     // DIR stage (Alg.1 651-656) rides on the DY reduction unless an NCCL allreduce sits in between
     const bool fuse_dir = !(multi && !c->p2p);
@@ -277,13 +276,13 @@ static int enqueue_iteration(ptyger_ctx* c, int p, std::string& err, int64_t& la
     LK(launch_eta(g, gcur, c->eta, c->st, c->part_el, c->grid_el, s)); ++launches;
     // ||eta||^2: summed over ranks here with the peer-memory transport (NCCL: with the pass-0 LS vector)
     LK(launch_reduce(c->part_el, c->grid_el, 1, &c->st->ls_pass[LS_ETA], s, c->st, 0, 0, fuse)); ++launches;
-    EV(4);
+    LK(launch_stamp(c->st, 2, s));   // DIR stage done
+    ++launches;
     // LS stage (Alg.1 659-668).  Pass 0 computes v = G eta and screens trials 0..K-1; every pass
     // is followed by an exact re-evaluation that runs only when the screening left it undecided;
     // further passes (trials pK..pK+K-1) run only while nothing was accepted.
     LK(launch_ls(g, c->eta, c->probe, c->probe_s, c->pos, c->order, c->u, c->v, c->d, sc, c->part_fr, c->grid_fr, c->st, s));
     ++launches;
-    EV(5);
     // pass 0 evaluates keff trials (adaptive on the device, >= KMIN), later passes K each
     const int rest = sc.max_shrinks > KMIN ? sc.max_shrinks - KMIN : 0;
     const int npass = 1 + (rest + sc.K - 1) / sc.K;
@@ -315,10 +314,12 @@ static int enqueue_iteration(ptyger_ctx* c, int p, std::string& err, int64_t& la
             ++launches;
         }
     }
+    LK(launch_stamp(c->st, 3, s));   // LS stage done
+    ++launches;
     // Update stage (Alg.1 672)
     LK(launch_upd(g, c->psi, c->eta, c->st, c->grid_el, s)); ++launches;
-    EV(6);
-#undef EV
+    LK(launch_stamp(c->st, 4, s));   // Update done: stage ms into the trace entry
+    ++launches;
     return 0;
 }
 
@@ -1093,33 +1094,17 @@ ptyger_status ptyger_get_ls_partials(ptyger_ctx* c, double* dF, double* bound, i
 
 float ptyger_last_iterate_ms(const ptyger_ctx* c) { return c ? c->last_ms : 0.f; }
 
-ptyger_status ptyger_stage_times(ptyger_ctx* c, int32_t n_iter, double* ms) {
-    if (!c || !ms || n_iter < 1) return set_err(c, PTYGER_E_ARG, "stage_times: bad arguments");
-    if (!c->connected) return set_err(c, PTYGER_E_STATE, "P2P context not connected (ptyger_ipc_connect)");
-    if (c->failed_numeric) return set_err(c, PTYGER_E_NUMERIC, "context is in a numeric-failure state");
-    std::string& err = c->err;
-    CK(cudaSetDevice(c->cfg.device));
-    cudaEvent_t ev[7];
-    for (int i = 0; i < 7; ++i) CK(cudaEventCreate(&ev[i]));
-    for (int i = 0; i < 7; ++i) ms[i] = 0.0;
-    struct { int idx, cap; } hdr = {0, 0};
-    CK(cudaMemcpyAsync(&c->st->trace_idx, &hdr, sizeof(int) * 2, cudaMemcpyHostToDevice, c->stream));
-    for (int it = 0; it < n_iter; ++it) {
-        int64_t launches = 0;
-        const int rc = enqueue_iteration(c, c->m_host & 1, err, launches, ev);
-        if (rc) return (ptyger_status)rc;
-        c->m_host += 1;
-        CK(cudaStreamSynchronize(c->stream));
-        float t;
-        for (int i = 0; i < 6; ++i) {
-            CK(cudaEventElapsedTime(&t, ev[i], ev[i + 1]));
-            ms[i] += t;
-        }
-        CK(cudaEventElapsedTime(&t, ev[0], ev[6]));
-        ms[6] += t;
+ptyger_status ptyger_fp32_peak(int32_t device, int32_t paired, double* tflops) {
+    if (!tflops) return set_err(nullptr, PTYGER_E_ARG, "fp32_peak: null pointer");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0 || device < 0 || device >= ndev) {
+        cudaGetLastError();
+        return set_err(nullptr, PTYGER_E_CUDA, "fp32_peak: no such CUDA device");
     }
-    for (int i = 0; i < 7; ++i) cudaEventDestroy(ev[i]);
-    return check_numeric(c);
+    const double t = measure_fp32_peak(device, paired != 0);
+    if (t <= 0) return set_err(nullptr, PTYGER_E_CUDA, "fp32_peak: microbenchmark launch failed");
+    *tflops = t;
+    return PTYGER_OK;
 }
 
 ptyger_status ptyger_kernel_times(ptyger_ctx* c, double* ms, int32_t* count, int32_t reset) {

@@ -47,6 +47,11 @@ struct DevState {
     unsigned int p2p_done[4];
     double tk_sum_ms[2];
     int tk_cnt[2];
+    // per-stage device timestamps of the current iteration (globaltimer ns): [0] begin, [1] GRAD frame
+    // kernels + adjoint done, [2] DIR done, [3] LS done, [4] update done, [5] adjoint done before the
+    // band exchange (world > 1); the final stamp folds them into the iteration's trace entry
+    unsigned long long stamp[6];
+    int trace_written;       // pick_body wrote this iteration's trace entry (slot trace_idx - 1)
     int trace_idx;           // slot of the current iteration in the trace buffer
     int trace_cap;           // capacity of trace_ptr
     ptyger_trace* trace_ptr; // device trace buffer of the current ptyger_cg_iterate call
@@ -122,6 +127,8 @@ int launch_pick(DevState* st, const SolverCfg& c, int pass, int exact_mode, int 
 int launch_upd(const Geometry& g, float2* psi, const float2* eta, const DevState* st, int grid,
                cudaStream_t s);
 int launch_begin_iter(DevState* st, cudaStream_t s);
+// stage timestamp `slot` (see DevState::stamp); slot 4 also writes the stage ms into the trace entry
+int launch_stamp(DevState* st, int slot, cudaStream_t s);
 int launch_timers(DevState* st, double* out, int reset, cudaStream_t s);
 int launch_fold(const Geometry& g, float2* u, const float2* v, DevState* st, int grid, cudaStream_t s);
 int launch_validate_d(const float* d, int64_t count, int64_t frame_elems, unsigned long long* bad,
@@ -130,6 +137,12 @@ int launch_validate_d(const float* d, int64_t count, int64_t frame_elems, unsign
 int launch_f0_validate(const float2* u, const float* d, int64_t count, int64_t frame_elems, unsigned long long* bad,
                        double* part, int grid, float eps, int est, cudaStream_t s);
 int launch_set_F(DevState* st, const double* src, int keff0, cudaStream_t s);
+// FP32 FMA-pipe peak of `device` in TFLOP/s (kernels_peak.cu), paired FFMA2 or scalar FFMA; < 0 on error
+double measure_fp32_peak(int device, bool paired);
+// warp-specialised LS pass 0 for N = 128 (kernels_ls128.cu): FFT group + epilogue group, TMEM hand-off
+int launch_ls_ws(const Geometry& g, const float2* eta, const float2* probe_s, const int2* pos, const int* order,
+                 const float2* u, float2* v, const float* d, const SolverCfg& c, double* part, int grid,
+                 const DevState* st, cudaStream_t s);
 // cluster-of-four frame kernels for N = 256 (kernels_c256.cu); probe_s = probe / N
 int c256_ls_parts(int64_t nfr);
 int launch_ls_c256(const Geometry& g, const float2* eta, const float2* probe_s, const int2* pos, const int* order,

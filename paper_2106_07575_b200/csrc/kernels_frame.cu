@@ -460,7 +460,11 @@ int launch_ls(const Geometry& g, const float2* eta, const float2* probe, const f
         case 16: return ls_n<16>(g, eta, probe_s, pos, order, u, v, d, c, part, grid, st, s);
         case 32: return ls_n<32>(g, eta, probe_s, pos, order, u, v, d, c, part, grid, st, s);
         case 64: return ls_n<64>(g, eta, probe_s, pos, order, u, v, d, c, part, grid, st, s);
-        case 128: return ls_n<128>(g, eta, probe_s, pos, order, u, v, d, c, part, grid, st, s);
+        case 128: {
+            static const bool ws = !(getenv("PTYGER_LS_WS") && atoi(getenv("PTYGER_LS_WS")) == 0);
+            if (ws) return launch_ls_ws(g, eta, probe_s, pos, order, u, v, d, c, part, grid, st, s);
+            return ls_n<128>(g, eta, probe_s, pos, order, u, v, d, c, part, grid, st, s);
+        }
         case 256: return launch_ls_c256(g, eta, probe_s, pos, order, u, v, d, c, part, st, s);
     }
     return -2;

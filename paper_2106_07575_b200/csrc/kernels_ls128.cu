@@ -1,0 +1,315 @@
+// LS pass 0 for N = 128 frames, WARP-SPECIALISED (Alg.1 659-668, Eq.7 on the Eq.2 objective; the
+// screening contract of k_ls<N> in kernels_frame.cu is unchanged).
+//
+// r2 measurement of the single-group k_ls<128> (profiles/r2_history.md): its three phases --
+// window gathers (0.61 ms), the two FFT passes + v store (1.39 ms) and the screening epilogue
+// (1.24 ms at 10 trials) -- ADD UP (3.17 ms): all 16 warps run the same phase at the same time, so
+// the gather latency, the shared-memory FFT and the MUFU / u,d-streaming epilogue never overlap.
+// Here one persistent 512-thread CTA per SM splits into two groups that work on different frames:
+//
+//   FFT group (warps 0-7):  frame j's eta window -> shared memory by the TMA engine (one 1-D bulk
+//       copy per row, cp.async.bulk, issued as soon as the frame buffer is free, so the copy flies
+//       while the group finishes the previous frame), x = (p / N) eta, row pass, column pass; the
+//       column-pass outputs v_j go to TENSOR MEMORY (tcgen05.st), not back to shared memory;
+//   epilogue group (warps 8-15): frame j-1's v from tensor memory (tcgen05.ld), v store to HBM,
+//       u / d streamed from HBM (bulk L2 prefetch one frame ahead), the screening terms of the
+//       pass-0 trials (dev.cuh ls_push / ls_flush).
+//
+// Tensor memory (256 KB per SM, otherwise unused here: nothing in the path is a dense contraction)
+// is the hand-off buffer: 2 slots x 128 KB = one frame of v each, double-buffered.  Lane quarter
+// rule: warp w may only touch TMEM lanes 32 (w % 4) .. +31, so FFT warp w and epilogue warp w + 8 share
+// a quarter; w / 4 picks the 128-column half.  Per thread and frame: 4 column rounds x 16 complex =
+// 128 32-bit columns.  Hand-off with named barriers (bar.arrive / bar.sync, 512 threads): FULL[b]
+// (FFT -> epilogue, slot b written) and EMPTY[b] (epilogue -> FFT, slot b read), plus the
+// tcgen05.fence::before/after_thread_sync pair around each.
+//
+// Everything else is the arithmetic of the other frame kernels (fft.cuh radix-16 x radix-8 lines,
+// fp64-built twiddles, paired FP32); the trial sums, moments and partial layout are those of k_ls,
+// so k_reduce / k_pick consume them unchanged.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "dev.cuh"
+#include "tma.cuh"
+
+namespace pty {
+
+namespace ws {
+constexpr int N = 128, R = 16, T = 8, LD = N + 8;
+constexpr int NT = 512, NF = 256;             // FFT group = threads [0, 256), epilogue group = [256, 512)
+constexpr int RROWS = NF / T;                 // 32 rows per row-pass round
+constexpr int ROUNDS = N / RROWS;             // 4 row rounds
+constexpr int CROUNDS = N * T / NF;           // 4 column rounds of 32 columns
+constexpr size_t FRAME_BYTES = (size_t)N * LD * 8;                  // 139 264
+constexpr size_t TW_OFF = FRAME_BYTES;                              // tw[N], twr[R*T]
+constexpr size_t DYN_BYTES = TW_OFF + (size_t)(N + R * T) * 8;
+constexpr int TMEM_COLS = 512;
+// named barrier ids (0 is __syncthreads)
+constexpr int BAR_FFT = 1, BAR_FULL = 2, BAR_EMPTY = 4;
+}  // namespace ws
+
+__device__ __forceinline__ void bar_sync_n(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void bar_arrive_n(int id, int n) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// 16 complex (32 words) of this thread into TMEM columns [col, col + 32) of the warp's lane quarter
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float2 (&x)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr),
+        "f"(x[0].x), "f"(x[0].y), "f"(x[1].x), "f"(x[1].y), "f"(x[2].x), "f"(x[2].y), "f"(x[3].x), "f"(x[3].y),
+        "f"(x[4].x), "f"(x[4].y), "f"(x[5].x), "f"(x[5].y), "f"(x[6].x), "f"(x[6].y), "f"(x[7].x), "f"(x[7].y),
+        "f"(x[8].x), "f"(x[8].y), "f"(x[9].x), "f"(x[9].y), "f"(x[10].x), "f"(x[10].y), "f"(x[11].x), "f"(x[11].y),
+        "f"(x[12].x), "f"(x[12].y), "f"(x[13].x), "f"(x[13].y), "f"(x[14].x), "f"(x[14].y), "f"(x[15].x),
+        "f"(x[15].y)
+        : "memory");
+}
+// 4 complex (8 words) from TMEM columns [col, col + 8)
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float2 (&x)[4]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=f"(x[0].x), "=f"(x[0].y), "=f"(x[1].x), "=f"(x[1].y), "=f"(x[2].x), "=f"(x[2].y), "=f"(x[3].x),
+                   "=f"(x[3].y)
+                 : "r"(taddr)
+                 : "memory");
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+template <bool DMA>
+__global__ void __launch_bounds__(512, 1) k_ls_ws(Geometry g, const float2* __restrict__ eta,
+                                                  const float2* __restrict__ probe_s, const int2* __restrict__ pos,
+                                                  const int* __restrict__ order, const float2* __restrict__ u,
+                                                  float2* __restrict__ v, const float* __restrict__ d, SolverCfg cfg,
+                                                  double* __restrict__ part, const DevState* __restrict__ st) {
+    using namespace ws;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    float2* sf = reinterpret_cast<float2*>(smraw);
+    float2* tw = reinterpret_cast<float2*>(smraw + TW_OFF);
+    __shared__ double sred[16][KC];
+    __shared__ double smom[16][4];
+    __shared__ float sgam[KC];
+    __shared__ LsWarpQ wq[8];
+    __shared__ uint32_t s_tmem;
+    __shared__ __align__(8) uint64_t s_mbar;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const bool err = st->numeric_error != 0;
+    int base, cnt;
+    ls_pass_range(0, st->keff, cfg, base, cnt);
+    ktime_start(st, 1);
+    build_twiddles<N>(tw);
+    build_row_twiddles<N>(tw + N);
+    if (tid < KC) sgam[tid] = (float)trial_gamma(cfg.gamma0, cfg.tau, base + tid);
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
+                     "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        mbar_init(&s_mbar, 1);
+        fence_mbar_init();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tbase = s_tmem;
+    const int64_t nfr = err ? 0 : g.n_local;
+    const int64_t W = g.W;
+    // quarter / half of this warp's TMEM region (FFT warp w and epilogue warp w + 8 share it)
+    const int wq4 = warp & 3, whalf = (warp & 7) >> 2;
+    const uint32_t tq = tbase + ((uint32_t)(32 * wq4) << 16) + (uint32_t)(128 * whalf);
+
+    // TMA bulk copies of frame i's eta window rows into the frame buffer (warp 0 of the FFT group).
+    // Row r goes to sf + r LD; a window starting at an odd column is copied from the column before it
+    // (16-B alignment, 130 elements), so the row pass reads it at offset 1.
+    auto issue_dma = [&](int64_t i) {
+        const int j = order[i];
+        const int2 s = pos[j];
+        const int off = s.y & 1;
+        const uint32_t bytes = (uint32_t)(N + 2 * off) * 8u;
+        if (lane == 0) mbar_arrive_expect_tx(&s_mbar, bytes * N);
+        __syncwarp();
+        const float2* src = eta + (int64_t)s.x * W + (s.y - off);
+#pragma unroll
+        for (int q = 0; q < N / 32; ++q) {
+            const int r = q * 32 + lane;
+            bulk_g2s(sf + r * LD, src + (int64_t)r * W, bytes, &s_mbar);
+        }
+    };
+
+    double tot = 0.0;
+    double mom[4] = {0.0, 0.0, 0.0, 0.0};
+    if (tid < NF) {
+        // ============================ FFT group ============================
+        const int ft = tid;
+        if (DMA && warp == 0 && blockIdx.x < nfr) issue_dma(blockIdx.x);
+        int it = 0;
+        for (int64_t i = blockIdx.x; i < nfr; i += gridDim.x, ++it) {
+            const int b = it & 1;
+            const int j = order[i];
+            const int2 s = pos[j];
+            if (DMA) mbar_wait(&s_mbar, (uint32_t)(it & 1));
+            // ---- row pass: 4 rounds of 32 rows, two rounds' inputs in flight at a time
+            const int t = ft % T, rrow = ft / T;
+            auto load_row = [&](int rd, float2 (&x)[R]) {
+                const int row = rd * RROWS + rrow;
+                const float2* pp = probe_s + row * N + t;
+                if constexpr (DMA) {
+                    const float2* se = sf + row * LD + (s.y & 1) + t;
+#pragma unroll
+                    for (int n1 = 0; n1 < R; ++n1) x[n1] = cmul(ldg2(pp + T * n1), se[T * n1]);
+                } else {
+                    window_row<R, T>(eta, g, s, j, row, t, pp, x);
+                }
+            };
+#pragma unroll 1
+            for (int rp = 0; rp < ROUNDS; rp += 2) {
+                float2 xa[R], xb[R];
+                load_row(rp, xa);
+                load_row(rp + 1, xb);
+                __syncwarp();   // every lane of the warp has read its rows before any exchange write
+                row_fft<N, false, true>(xa, sf + (rp * RROWS + rrow) * LD, t, tw, tw + N);
+                row_fft<N, false, true>(xb, sf + ((rp + 1) * RROWS + rrow) * LD, t, tw, tw + N);
+            }
+            bar_sync_n(BAR_FFT, NF);
+            // ---- column pass phase 1: 4 rounds of 32 columns, sub-thread t = warp
+#pragma unroll 1
+            for (int rd = 0; rd < CROUNDS; ++rd) col_fft_phase1<N, false>(sf + rd * 32 + lane, warp, tw);
+            bar_sync_n(BAR_FFT, NF);
+            // ---- slot b must have been read by the epilogue (frame it - 2)
+            if (it >= 2) {
+                bar_sync_n(BAR_EMPTY + b, NT);
+                tc_fence_after();
+            }
+            // ---- column pass phase 2 -> tensor memory slot b, 32 columns per round
+#pragma unroll 1
+            for (int rd = 0; rd < CROUNDS; ++rd) {
+                float2 X[R];
+                col_fft_phase2<N, false>(sf + rd * 32 + lane, warp, X);
+                tmem_st32(tq + (uint32_t)(256 * b + 32 * rd), X);
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            tc_fence_before();
+            bar_arrive_n(BAR_FULL + b, NT);
+            // ---- the frame buffer is free: the next frame's window copy flies during the wait
+            if (DMA) {
+                fence_proxy_async();
+                bar_sync_n(BAR_FFT, NF);
+                if (warp == 0 && i + gridDim.x < nfr) issue_dma(i + gridDim.x);
+            } else {
+                bar_sync_n(BAR_FFT, NF);
+            }
+        }
+    } else {
+        // ============================ epilogue group ============================
+        const int ew = warp - 8;                  // = the FFT warp whose outputs this warp reads
+        const float eps2 = (float)(cfg.eps * cfg.eps);
+        int nmine = 0;
+        for (int64_t i = blockIdx.x; i < nfr; i += gridDim.x) ++nmine;
+        trial_dispatch(cnt, cfg.est, [&]<int KT, bool LSE>() {
+            float gk[KT];   // trial gammas in registers for the whole run
+#pragma unroll
+            for (int k = 0; k < KT; ++k) gk[k] = sgam[k];
+            int it = 0;
+            for (int64_t i = blockIdx.x; i < nfr; i += gridDim.x, ++it) {
+                const int b = it & 1;
+                const int64_t jf = order[i];
+                // this frame's u, d into L2 while its transform is still running
+                if (ew == 0) prefetch_l2_frame(u + jf * N * N, N * N * 8, lane);
+                else if (ew == 1) prefetch_l2_frame(d + jf * N * N, N * N * 4, lane);
+                bar_sync_n(BAR_FULL + b, NT);
+                tc_fence_after();
+#pragma unroll 1
+                for (int rd = 0; rd < CROUNDS; ++rd) {
+                    // column c = 32 rd + lane; element q of the thread sits at row (q / T) T + ew + R (q % T)
+                    const int c = rd * 32 + lane;
+                    const int64_t fb = jf * (int64_t)(N * N) + (int64_t)ew * N + c;
+                    const float2* __restrict__ ub = u + fb;
+                    const float* __restrict__ db = d + fb;
+                    float2* __restrict__ vb = v + fb;
+                    float S[KC];
+                    LsMom m;
+#pragma unroll
+                    for (int k = 0; k < KC; ++k) S[k] = 0.f;
+                    LsQState qs;
+                    float2 un[4];
+                    float dn[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        un[e] = ldg2_na(ub + e * R * N);
+                        dn[e] = ldg1_na(db + e * R * N);
+                    }
+#pragma unroll 1
+                    for (int gi = 0; gi < R / 4; ++gi) {
+                        // groups of 4 consecutive q share j = q / T: offsets step by R N inside a group
+                        const int q0 = 4 * gi;
+                        const int go = ((q0 / T) * T + R * (q0 % T)) * N;
+                        float2 uc[4];
+                        float dc[4];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            uc[e] = un[e];
+                            dc[e] = dn[e];
+                        }
+                        if (gi + 1 < R / 4) {
+                            const int q1 = q0 + 4;
+                            const int gn = ((q1 / T) * T + R * (q1 % T)) * N;
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                un[e] = ldg2_na(ub + gn + e * R * N);
+                                dn[e] = ldg1_na(db + gn + e * R * N);
+                            }
+                        }
+                        float2 X[4];
+                        tmem_ld8(tq + (uint32_t)(256 * b + 32 * rd + 8 * gi), X);
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            vb[go + e * R * N] = X[e];
+                            ls_push<KT, LSE>(wq[ew], qs, uc[e], X[e], dc[e], gk, eps2, S, m, lane);
+                        }
+                    }
+                    ls_flush<KT, LSE>(wq[ew], qs, gk, eps2, S, m, lane);
+                    double dv[KC];
+#pragma unroll
+                    for (int k = 0; k < KC; ++k) dv[k] = (double)S[k];
+                    tot += warp_reduce_scatter<KC>(dv, lane);
+                    mom[0] += (double)m.A;
+                    mom[1] += (double)m.D;
+                    mom[2] += (double)m.sa;
+                    mom[3] += (double)m.sb;
+                }
+                // slot b read: the FFT group may overwrite it (frame it + 2) -- no arrival without a waiter
+                tc_fence_before();
+                if (it + 2 < nmine) bar_arrive_n(BAR_EMPTY + b, NT);
+            }
+        });
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(TMEM_COLS));
+    ktime_end(st, 1);
+    ls_block_out<KC, 16>(tot, mom, sred, smom, part);
+}
+
+int launch_ls_ws(const Geometry& g, const float2* eta, const float2* probe_s, const int2* pos, const int* order,
+                 const float2* u, float2* v, const float* d, const SolverCfg& c, double* part, int grid,
+                 const DevState* st, cudaStream_t s) {
+    // the row DMA needs 16-B aligned window rows: even object width, integer positions
+    const bool dma = (g.W % 2 == 0) && g.frac == nullptr;
+    if (dma) {
+        if (cudaFuncSetAttribute(k_ls_ws<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ws::DYN_BYTES) !=
+            cudaSuccess)
+            return -1;
+        k_ls_ws<true><<<grid, ws::NT, ws::DYN_BYTES, s>>>(g, eta, probe_s, pos, order, u, v, d, c, part, st);
+    } else {
+        if (cudaFuncSetAttribute(k_ls_ws<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ws::DYN_BYTES) !=
+            cudaSuccess)
+            return -1;
+        k_ls_ws<false><<<grid, ws::NT, ws::DYN_BYTES, s>>>(g, eta, probe_s, pos, order, u, v, d, c, part, st);
+    }
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+}  // namespace pty

@@ -300,6 +300,9 @@ int launch_timers(DevState* st, double* out, int reset, cudaStream_t s) {
 }
 
 __global__ void k_begin_iter(DevState* st) {
+    st->stamp[0] = gtimer();
+    st->stamp[5] = 0ull;
+    st->trace_written = 0;
     fold_timers(st);
     st->accepted = 0;
     st->kstar = -1;
@@ -571,10 +574,35 @@ __device__ void pick_body(DevState* st, const SolverCfg& c, int pass, int exact_
     t.alpha_im = st->alpha_im;
     t.grad_norm = sqrt(st->dy[0]);
     t.step_norm = st->gamma * sqrt(st->eta2);
+    t.ms_grad = t.ms_dir = t.ms_ls = t.ms_update = t.ms_comm = 0.f;   // filled by the final stamp
     if (st->trace_ptr && st->trace_idx < st->trace_cap) st->trace_ptr[st->trace_idx] = t;
     st->trace_idx += 1;
+    st->trace_written = 1;
     st->m += 1;
     st->keff = st->stalled ? c.K : min(c.K, max(KMIN, st->kstar + 3));
+}
+
+// Stage timestamps (ptyger_trace ms_* fields): a one-thread kernel between the stages of
+// the captured iteration; it runs after everything before it on the stream, so the differences are
+// the stages' device durations.  Slot 4 (after the update) writes them into this iteration's entry.
+__global__ void k_stamp(DevState* st, int slot) {
+    const unsigned long long t = gtimer();
+    st->stamp[slot] = t;
+    if (slot != 4 || !st->trace_written) return;
+    const int i = st->trace_idx - 1;
+    if (!st->trace_ptr || i < 0 || i >= st->trace_cap) return;
+    ptyger_trace* tr = st->trace_ptr + i;
+    const unsigned long long* s = st->stamp;
+    tr->ms_grad = (float)((double)(s[1] - s[0]) * 1e-6);
+    tr->ms_dir = (float)((double)(s[2] - s[1]) * 1e-6);
+    tr->ms_ls = (float)((double)(s[3] - s[2]) * 1e-6);
+    tr->ms_update = (float)((double)(t - s[3]) * 1e-6);
+    tr->ms_comm = s[5] ? (float)((double)(s[1] - s[5]) * 1e-6) : 0.f;
+}
+
+int launch_stamp(DevState* st, int slot, cudaStream_t s) {
+    k_stamp<<<1, 1, 0, s>>>(st, slot);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
 __global__ void k_pick(DevState* st, SolverCfg c, int pass, int exact_mode, int last_pass) {

@@ -1,10 +1,15 @@
-"""Multi-rank path on hardware: 2, 3, 4 and 8 ranks (processes sharing the one GPU of the test box) run the
-stripe-partitioned iteration over the peer-memory transport (band exchange of partial gradients and
-rank-ordered fp64 scalar sums through CUDA-IPC-mapped windows, R#15 / R#18), compared with the
-single-rank run on the same inputs (only the summation order differs).  From a
-warm start (the single-rank iterate 30; free-running trajectories from a flat start are chaotic,
-SURVEY 8(c).4 item 1): gradient after the first iteration rel L2 <= 1e-5, identical shrink sequences,
-object after four iterations rel L2 <= 1e-4; all ranks hold bitwise identical F and object."""
+"""Multi-rank path on hardware, compared with the single-rank run on the same inputs (SURVEY 8(c).4
+item 5: only the summation order differs; R#15 / R#18):
+
+* 2, 3, 4 and 8 ranks as processes sharing the test box's one GPU over the peer-memory transport
+  (CUDA IPC within a device; the GPU time-slices the contexts);
+* 2 ranks on 2 DISTINCT GPUs over the peer-memory transport (NVLink P2P stores) and over the NCCL
+  transport (ncclSend/Recv band exchange, ncclAllReduce scalars) -- skipped on a one-GPU box.
+
+From a warm start (the single-rank iterate 30; free-running trajectories from a flat start are
+chaotic): gradient after the first iteration rel L2 <= 1e-6 (the survey's
+P-parity bar), identical shrink sequences, object after four iterations rel L2 <= 1e-4; all ranks
+hold bitwise identical F and object."""
 import os
 import subprocess
 import sys
@@ -22,10 +27,7 @@ def rel(a, b):
     return float(np.linalg.norm(a - b) / np.linalg.norm(b))
 
 
-@pytest.mark.parametrize("world", [2, 3, 4, 8])
-def test_ranks_p2p_match_single_rank(tmp_path, world):
-    if not torch.cuda.is_available():
-        pytest.skip("no GPU")
+def run_ranks(tmp_path, world, transport="p2p", devices=None):
     from tests.p2p_fixture import fixture
     from paper_2106_07575_b200 import _lib as L
     psi0, p, scan, d = fixture(world)
@@ -34,12 +36,20 @@ def test_ranks_p2p_match_single_rank(tmp_path, world):
     psi_w = warm.get_object()
     warm.close()
     np.save(os.path.join(tmp_path, "psi0.npy"), psi_w)
+    devices = devices or [0] * world
+    env = dict(os.environ)
+    if transport == "nccl":
+        env.setdefault("NCCL_DEBUG", "INFO")
+        env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     procs = [subprocess.Popen([sys.executable, os.path.join(ROOT, "tests", "_p2p_rank.py"), str(r), str(world),
-                               str(tmp_path)], stdout=subprocess.PIPE, stderr=subprocess.STDOUT, cwd=ROOT)
+                               str(tmp_path), transport, str(devices[r])],
+                              stdout=subprocess.PIPE, stderr=subprocess.STDOUT, cwd=ROOT, env=env)
              for r in range(world)]
     outs = [pr.communicate(timeout=600)[0].decode(errors="replace") for pr in procs]
     for r, pr in enumerate(procs):
         assert pr.returncode == 0, f"rank {r} failed:\n{outs[r][-3000:]}"
+    if transport == "nccl":
+        print("\n".join(l for l in outs[0].splitlines() if "NCCL INFO" in l)[-2000:])
     res = [np.load(os.path.join(tmp_path, f"out{r}.npz")) for r in range(world)]
     ref = L.Ptyger(psi_w, p, scan, d)
     tr = ref.iterate(1)
@@ -49,7 +59,9 @@ def test_ranks_p2p_match_single_rank(tmp_path, world):
     ref.close()
     for r in range(world):
         # every rank receives the united gradient / object (collective gathers) and the same scalars
-        assert rel(res[r]["g1"], g1) <= 1e-5, (r, rel(res[r]["g1"], g1))
+        print(f"{transport} world {world} rank {r}: g1 rel {rel(res[r]['g1'], g1):.2e}, "
+              f"object rel {rel(res[r]['obj'], obj):.2e}")
+        assert rel(res[r]["g1"], g1) <= 1e-6, (r, rel(res[r]["g1"], g1))
         assert list(res[r]["shrinks"]) == [t["shrinks"] for t in tr]
         assert rel(res[r]["obj"], obj) <= 1e-4, (r, rel(res[r]["obj"], obj))
         # the allreduced scalars: ||eta|| (trace step norm) and the DY alpha
@@ -58,3 +70,20 @@ def test_ranks_p2p_match_single_rank(tmp_path, world):
     for r in range(1, world):
         assert np.array_equal(res[0]["F"], res[r]["F"])     # rank-ordered sums: identical on all ranks
         assert np.array_equal(res[0]["obj"], res[r]["obj"])
+
+
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
+def test_ranks_p2p_match_single_rank(tmp_path, world):
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    run_ranks(tmp_path, world)
+
+
+@pytest.mark.parametrize("transport", ["p2p", "nccl"])
+def test_two_devices_match_single_rank(tmp_path, transport):
+    """2 ranks on GPUs 0 and 1 (NVLink on a B200 node): the peer-memory transport's P2P stores / flags
+    cross devices, and the NCCL transport (band Send/Recv + AllReduce captured in the iteration graph)
+    runs at all -- both must reproduce the single-rank run."""
+    if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    run_ranks(tmp_path, 2, transport, devices=[0, 1])
