@@ -460,6 +460,10 @@ def time_frames(args, w, world, rank, local, dev, coll_dev, steps, warmup, with_
                                "peak_GBps": pk, "frac": it_bytes / (ms / steps) / 1e6 / pk},
         "stage_ms": stage_ms(trs),
         "mean_shrinks": float(np.mean(shrinks)),
+        "shrinks": [int(x) for x in shrinks],
+        # LS passes over the cached far fields per timed iteration: [screened, exact] (1, 0 = all
+        # decided in the pass fused into the LS frame kernel)
+        "ls_passes": [[int(t["ls_passes"]), int(t["ls_exact_passes"])] for t in trs] if trs else None,
         "clocks": clocks,
         "gpu_launches": int(launches),
         "e2e": e2e,
@@ -592,7 +596,7 @@ def main():
         "lower_bound": lower_bound(w.N, n, w.H, w.W, main_f["ms_per_step"], peaks()[0],
                                    float(sm_max_mhz()), world, fp32["paired_ffma2_tflops"]),
         "fp32_peak_measured": fp32,
-        **{k: main_f[k] for k in ("mean_shrinks", "clocks", "gpu_launches", "e2e")},
+        **{k: main_f[k] for k in ("mean_shrinks", "shrinks", "ls_passes", "clocks", "gpu_launches", "e2e")},
         "cpu_baseline": cpu,
         "large_view": large,
         "multi_gpu": multi,

@@ -112,6 +112,10 @@ typedef struct {
      * decisions), Update; ms_comm = the band-exchange part of ms_grad (0 when world = 1; the fp64
      * scalar sums over ranks ride inside the DIR / LS reductions). */
     float ms_grad, ms_dir, ms_ls, ms_update, ms_comm;
+    int32_t ls_passes;        /* line-search passes over the cached far fields this iteration: the
+                                 screened pass 0 (fused into the LS frame kernel) plus every further
+                                 K-trial pass (no trial of the earlier passes accepted)             */
+    int32_t ls_exact_passes;  /* exact re-evaluations of a pass the screening left undecided        */
 } ptyger_trace;
 
 /* Fill cfg with the paper's defaults (gamma0 1, tau 0.5, t 0, eps 1e-16, max_shrinks 32,

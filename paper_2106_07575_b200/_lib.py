@@ -40,7 +40,7 @@ class Trace(C.Structure):
                 ("F", C.c_double), ("gamma", C.c_double), ("alpha_re", C.c_double), ("alpha_im", C.c_double),
                 ("grad_norm", C.c_double), ("step_norm", C.c_double),
                 ("ms_grad", C.c_float), ("ms_dir", C.c_float), ("ms_ls", C.c_float), ("ms_update", C.c_float),
-                ("ms_comm", C.c_float)]
+                ("ms_comm", C.c_float), ("ls_passes", C.c_int32), ("ls_exact_passes", C.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -310,44 +310,52 @@ __device__ __forceinline__ float lg2_ftz(float x) {
     return y;
 }
 
-// Per-thread moments of the screening bound.
+// Per-thread moments of the screening bound.  sa2 = sum |a| / 2 (a / 2 = Re(u* v) is what the
+// pixel loop forms; ls_run_out doubles it).
 struct LsMom {
-    float A = 0.f, D = 0.f, sa = 0.f, sb = 0.f;
+    float A = 0.f, D = 0.f, sa2 = 0.f, sb = 0.f;
 };
 
 // ---------------------------------------------------------------------------------------------
 // Sparse-data screening.  Poisson counts are 0 on most detector pixels (59 % at the bench
 // workload), and where d = 0 the log term vanishes EXACTLY: t_k = q_k = gamma_k a + gamma_k^2 b,
 // so those pixels only add to two moments (za, zb) folded into S_k at the end.  The d > 0 pixels
-// are compacted per warp through a 64-entry shared-memory ring (ballot + popc) and screened in
-// full 32-lane batches, so the per-trial MUFU/FMA work scales with the nonzero fraction.
+// are compacted per warp into a shared-memory queue (ballot + popc; u, v as one 16-B entry, d as a
+// second word) and screened in full 32-lane batches, so the per-trial MUFU/FMA work scales with
+// the nonzero fraction.  The queue is linear: a lane's NP pixels of one push land at
+// pending + prefix, full batches are screened from the front and the (< 32) remainder moves
+// to the front, so no wrap arithmetic is needed; capacity 31 + 32 NP entries.
 // All 32 lanes must call ls_push / ls_flush together (inactive lanes push zeros).
 // ---------------------------------------------------------------------------------------------
+template <int NP>
 struct LsWarpQ {
-    float2 u[64];
-    float2 v[64];
-    float d[64];
+    static constexpr int CAP = 31 + 32 * NP;
+    float4 uv[CAP];
+    float d[CAP];
 };
 
 // LSE = false: Poisson ML terms (screened, MUFU log2).  LSE = true: least-squares estimator terms
 // t = q (1 - 2 sqrt(d) / (|u + g v| + |u|)) with correctly rounded sqrt / reciprocal: a few ulp per
 // term, no transcendental approximation, so A stays 0 and the bound reduces to its rounding part.
+//
+// ML: cn = |u + gamma v|^2 is formed from the components of u + gamma v (each an fma of exact
+// inputs, correctly rounded), so w = cn / c keeps a few-ulp RELATIVE accuracy even when u + gamma v
+// nearly cancels (a pre-scaled u / |u| would lose it).
 template <int KT, bool LSE, int K, typename G>
-__device__ __forceinline__ void ls_screen_nz(float2 uu, float2 vv, float dd, const G& sgam, float eps2,
-                                             float (&S)[K], LsMom& m) {
-    const float c = fmaf(uu.x, uu.x, uu.y * uu.y);
+__device__ __forceinline__ void ls_screen_nz(float4 uv, float dd, const G& sgam, float eps2, float (&S)[K],
+                                             LsMom& m) {
+    const float2 uu = make_float2(uv.x, uv.y), vv = make_float2(uv.z, uv.w);
     if constexpr (LSE) {
         ls_screen_lse<KT>(uu, vv, dd, sgam, S);
     } else {
+        const float c = fmaf(uu.x, uu.x, uu.y * uu.y);
+        // |u| < eps: rc = 0, w = 0, log2 = -inf, a non-finite S and therefore the exact pass, which
+        // applies the guarded definition R#4 (as does an FTZ underflow of w)
         const float rc = (c >= eps2) ? __fdividef(1.0f, c) : 0.0f;
         const float dl = dd * 0.693147182464599609375f;
         float amax = 0.f;
-        // only the log part: q_k = gamma_k a + gamma_k^2 b of EVERY pixel goes to the (za, zb)
-        // moments in ls_push (one op per trial less than forming cn - c here).  No clamp of cn:
-        // cn * rc = 0 (|u + gamma v| or |u| below eps, or an FTZ underflow) gives log2 = -inf, a
-        // non-finite S and therefore the exact pass, which applies the guarded definition R#4.
         // Trials run in pairs on the paired FP32 pipe (FFMA2 / FMUL2: per lane the same fp32
-        // operations as the scalar form, so the screened sums are bit-identical to it).
+        // operations as the scalar form).
 #pragma unroll
         for (int k = 0; k + 1 < KT; k += 2) {
             const float2 g2 = make_float2(sgam[k], sgam[k + 1]);
@@ -372,66 +380,136 @@ __device__ __forceinline__ void ls_screen_nz(float2 uu, float2 vv, float dd, con
     }
 }
 
-// za, zb: per lane sums of a, b.  Poisson ML: over ALL pixels (q_k = gamma_k a + gamma_k^2 b is
+// za2, zb: per lane sums of a / 2, b.  Poisson ML: over ALL pixels (q_k = gamma_k a + gamma_k^2 b is
 // the whole non-log part of t_k, so the d > 0 screening only adds -d ln w_k).  Its rounding is
 // inside the screening bound: gamma |err a| <= 2^-23 (c + gamma^2 b) (AM-GM on 2|u||v|), covered
 // by the 0.12 c part of D and the gamma^2 sum b term.  LS estimator: over the d = 0 pixels only
 // (its d > 0 term is not separable).
 struct LsQState {
-    int head = 0, pending = 0;   // warp-uniform
-    float za = 0.f, zb = 0.f;
+    int pending = 0;   // warp-uniform queue fill
+    float za2 = 0.f, zb = 0.f;
 };
 
-template <int KT, bool LSE, int K, typename G>
-__device__ __forceinline__ void ls_push(LsWarpQ& q, LsQState& qs, float2 uu, float2 vv, float dd, const G& sgam,
-                                        float eps2, float (&S)[K], LsMom& m, int lane) {
-    const float a = 2.0f * fmaf(uu.x, vv.x, uu.y * vv.y);
-    const float b = fmaf(vv.x, vv.x, vv.y * vv.y);
-    const float c = fmaf(uu.x, uu.x, uu.y * uu.y);
-    m.D += fmaf(0.12f, c, dd);
-    m.sa += fabsf(a);
-    if (LSE) m.sb += b;   // Poisson ML: sum b is zb (all pixels), folded in at ls_flush
-    const bool nz = dd != 0.0f;
-    if (!LSE || !nz) {
-        qs.za += a;
-        qs.zb += b;
-    }
-    const unsigned mask = __ballot_sync(FULLMASK, nz);
-    if (nz) {
-        const int slot = (qs.head + qs.pending + __popc(mask & ((1u << lane) - 1u))) & 63;
-        q.u[slot] = uu;
-        q.v[slot] = vv;
-        q.d[slot] = dd;
-    }
-    qs.pending += __popc(mask);
-    if (qs.pending >= 32) {
-        __syncwarp();
-        const int slot = (qs.head + lane) & 63;
-        ls_screen_nz<KT, LSE>(q.u[slot], q.v[slot], q.d[slot], sgam, eps2, S, m);
-        qs.head = (qs.head + 32) & 63;
-        qs.pending -= 32;
-        __syncwarp();
-    }
+// Elements [O, O + M) of a register array as an array reference (for fixed-width pushes).
+template <int O, int M, typename E, int N>
+__device__ __forceinline__ E (&slice(E (&a)[N]))[M] {
+    static_assert(O + M <= N, "slice out of range");
+    return *reinterpret_cast<E(*)[M]>(a + O);
 }
 
-// Drain the ring and fold the (za, zb) moments into S (call once per accumulation run).
-template <int KT, bool LSE, int K, typename G>
-__device__ __forceinline__ void ls_flush(LsWarpQ& q, LsQState& qs, const G& sgam, float eps2, float (&S)[K],
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned r;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
+    return r;
+}
+
+// Screen every full batch of 32 queued pixels; move the remainder to the front of the queue.
+template <int KT, bool LSE, int QN, int K, typename G>
+__device__ __forceinline__ void ls_drain_full(LsWarpQ<QN>& q, LsQState& qs, const G& sgam, float eps2,
+                                              float (&S)[K], LsMom& m, int lane) {
+    __syncwarp();
+    int b = 0;
+#pragma unroll 1
+    for (; b + 32 <= qs.pending; b += 32) ls_screen_nz<KT, LSE>(q.uv[b + lane], q.d[b + lane], sgam, eps2, S, m);
+    const int rem = qs.pending - b;
+    float4 tu = make_float4(0.f, 0.f, 0.f, 0.f);
+    float td = 0.f;
+    if (lane < rem) {
+        tu = q.uv[b + lane];
+        td = q.d[b + lane];
+    }
+    __syncwarp();
+    if (lane < rem) {
+        q.uv[lane] = tu;
+        q.d[lane] = td;
+    }
+    __syncwarp();
+    qs.pending = rem;
+}
+
+// Push NP pixels per lane (all lanes together) into a queue sized for QN >= NP.
+template <int KT, bool LSE, int QN, int NP, int K, typename G>
+__device__ __forceinline__ void ls_push(LsWarpQ<QN>& q, LsQState& qs, const float2 (&uu)[NP],
+                                        const float2 (&vv)[NP], const float (&dd)[NP], const G& sgam, float eps2,
+                                        float (&S)[K], LsMom& m, int lane) {
+    static_assert(NP <= QN, "queue too small for the push width");
+    const unsigned lt = lanemask_lt();
+    int off = qs.pending;
+#pragma unroll
+    for (int e = 0; e < NP; ++e) {
+        const float2 u = uu[e], v = vv[e];
+        const float a2 = fmaf(u.x, v.x, u.y * v.y);   // a / 2
+        const float b = fmaf(v.x, v.x, v.y * v.y);
+        const float c = fmaf(u.x, u.x, u.y * u.y);
+        m.D += fmaf(0.12f, c, dd[e]);
+        m.sa2 += fabsf(a2);
+        if (LSE) m.sb += b;   // Poisson ML: sum b is zb (all pixels), folded in at ls_flush
+        const bool nz = dd[e] != 0.0f;
+        if (!LSE || !nz) {
+            qs.za2 += a2;
+            qs.zb += b;
+        }
+        const unsigned mask = __ballot_sync(FULLMASK, nz);
+        if (nz) {
+            const int slot = off + __popc(mask & lt);
+            q.uv[slot] = make_float4(u.x, u.y, v.x, v.y);
+            q.d[slot] = dd[e];
+        }
+        off += __popc(mask);
+    }
+    qs.pending = off;
+    if (off >= 32) ls_drain_full<KT, LSE>(q, qs, sgam, eps2, S, m, lane);
+}
+
+// Drain the queue and fold the (za, zb) moments into S (call once per accumulation run).
+template <int KT, bool LSE, int QN, int K, typename G>
+__device__ __forceinline__ void ls_flush(LsWarpQ<QN>& q, LsQState& qs, const G& sgam, float eps2, float (&S)[K],
                                          LsMom& m, int lane) {
     if (qs.pending > 0) {
         __syncwarp();
-        if (lane < qs.pending) {
-            const int slot = (qs.head + lane) & 63;
-            ls_screen_nz<KT, LSE>(q.u[slot], q.v[slot], q.d[slot], sgam, eps2, S, m);
-        }
-        qs.head = (qs.head + qs.pending) & 63;
+        if (lane < qs.pending) ls_screen_nz<KT, LSE>(q.uv[lane], q.d[lane], sgam, eps2, S, m);
         qs.pending = 0;
         __syncwarp();
     }
+    const float za = 2.0f * qs.za2;
 #pragma unroll
-    for (int k = 0; k < KT; ++k) S[k] += sgam[k] * fmaf(sgam[k], qs.zb, qs.za);
+    for (int k = 0; k < KT; ++k) S[k] += sgam[k] * fmaf(sgam[k], qs.zb, za);
     if (!LSE) m.sb += qs.zb;
-    qs.za = qs.zb = 0.f;
+    qs.za2 = qs.zb = 0.f;
+}
+
+// Warp reduce-scatter of the K per-lane fp32 trial sums in fp32 (5 rounding levels of 2^-24 relative
+// to the sum of |partials|, inside the LS_EPS_R part of the bound); returns, as fp64, the warp total
+// of entry lane >> (5 - log2 K).
+template <int K>
+__device__ __forceinline__ double warp_reduce_scatter_f(float (&v)[K], int lane) {
+    constexpr int P = Log2<K>::value;
+#pragma unroll
+    for (int s = 0; s < P; ++s) {
+        const int h = K >> (s + 1);
+        const int msk = 16 >> s;
+        const bool upper = (lane & msk) != 0;
+#pragma unroll
+        for (int i = 0; i < h; ++i) {
+            const float send = upper ? v[i] : v[i + h];
+            const float keep = upper ? v[i + h] : v[i];
+            v[i] = keep + __shfl_xor_sync(FULLMASK, send, msk);
+        }
+    }
+    float r = v[0];
+#pragma unroll
+    for (int msk = (32 >> P) >> 1; msk >= 1; msk >>= 1) r += __shfl_xor_sync(FULLMASK, r, msk);
+    return (double)r;
+}
+
+// Fold one accumulation run (per-lane S, moments) into the thread's fp64 running totals.
+template <int K>
+__device__ __forceinline__ void ls_run_out(float (&S)[K], const LsMom& m, double& tot, double (&mom)[4], int lane) {
+    tot += warp_reduce_scatter_f<K>(S, lane);
+    mom[0] += (double)m.A;
+    mom[1] += (double)m.D;
+    mom[2] += 2.0 * (double)m.sa2;
+    mom[3] += (double)m.sb;
 }
 
 // Run body.template operator()<KT>() with KT = cnt (4..10) or cnt rounded up to an even count (<= 16):

@@ -174,6 +174,8 @@ struct FFTCfg {
     static constexpr int FRAME_ELEMS = N * LD;
     // + N: twiddle table tw[m] = W_N^m; + R*T: the row-pass copy twr[k1*T + t] = W_N^{t k1}
     static constexpr size_t SMEM_BYTES = (size_t)(FPB * FRAME_ELEMS + N + R * T) * sizeof(float2);
+    // with the pre-swapped float4 tables (build_twiddles4)
+    static constexpr size_t SMEM_BYTES4 = (size_t)FPB * FRAME_ELEMS * sizeof(float2) + (size_t)(N + R * T) * 16;
     static_assert(N * T * FPB % NT == 0 || FPB == 1, "bad config");
     static_assert(LINES % LPR == 0, "bad rounds");
 };
@@ -191,6 +193,31 @@ __device__ __forceinline__ void build_twiddles(float2* tw) {
 template <bool INV>
 __device__ __forceinline__ float2 twmul(float2 x, float2 w) { return INV ? cmulc(x, w) : cmul(x, w); }
 
+// Pre-swapped twiddle entries w4 = (c, s, -s, c) for w = c + i s (the direction's sign already in s):
+// x w = x.x (c, s) + x.y (-s, c) is one FMUL2 + one FFMA2 straight from the 16-B table entry (the
+// float2 table needs a negation to form (-s, c) for every multiply).
+__device__ __forceinline__ float2 twmul4(float2 x, float4 w) {
+    return fma2(bc2(x.y), make_float2(w.z, w.w), mul2(bc2(x.x), make_float2(w.x, w.y)));
+}
+template <bool INV>
+__device__ __forceinline__ float2 twm(float2 x, const float2* tw, int i) { return twmul<INV>(x, tw[i]); }
+template <bool INV>
+__device__ __forceinline__ float2 twm(float2 x, const float4* tw, int i) { return twmul4(x, tw[i]); }
+
+// float4 tables: tw4[m] = W^m and the row-pass copy tw4[N + k1*T + t] = W^{t k1}, W = exp(-/+ 2 pi i / N)
+// (INV: +), built in double precision (same values as build_twiddles / build_row_twiddles).
+template <int N, bool INV>
+__device__ __forceinline__ void build_twiddles4(float4* tw4) {
+    constexpr int R = N < 16 ? N : 16, T = N / R;
+    for (int i = threadIdx.x; i < N + R * T; i += blockDim.x) {
+        const int m = i < N ? i : ((i - N) % T) * ((i - N) / T);
+        double sn, cs;
+        sincospi(2.0 * (double)m / (double)N, &sn, &cs);
+        const float c = (float)cs, sg = INV ? (float)sn : (float)(-sn);
+        tw4[i] = make_float4(c, sg, -sg, c);
+    }
+}
+
 // Row-pass twiddles laid out [k1][t]: the T sub-threads of a row read T consecutive entries (the
 // tw[t k1] layout made those reads 2..8-way bank conflicted).  Same fp64-built values as tw.
 template <int N>
@@ -207,9 +234,9 @@ __device__ __forceinline__ void build_row_twiddles(float2* twr) {
 // ROW pass for one row: x[n1] = input element at column T*n1 + t.  Leaves the row's DFT
 // (unnormalised) in srow[0..N) in natural order.  The T threads of the row must be
 // consecutive lanes of one warp and all 32 lanes must call this together.
-template <int N, bool INV, bool TWR = false>
-__device__ __forceinline__ void row_fft(float2 (&x)[FFTCfg<N>::R], float2* srow, int t, const float2* tw,
-                                        const float2* twr = nullptr) {
+template <int N, bool INV, bool TWR = false, typename TW = float2>
+__device__ __forceinline__ void row_fft(float2 (&x)[FFTCfg<N>::R], float2* srow, int t, const TW* tw,
+                                        const TW* twr = nullptr) {
     constexpr int R = FFTCfg<N>::R, T = FFTCfg<N>::T;
     DFT<R, INV>::run(x);
     if constexpr (T == 1) {
@@ -219,9 +246,9 @@ __device__ __forceinline__ void row_fft(float2 (&x)[FFTCfg<N>::R], float2* srow,
 #pragma unroll
         for (int k1 = 1; k1 < R; ++k1) {
             if constexpr (TWR)
-                x[k1] = twmul<INV>(x[k1], twr[k1 * T + t]);
+                x[k1] = twm<INV>(x[k1], twr, k1 * T + t);
             else
-                x[k1] = twmul<INV>(x[k1], tw[t * k1]);
+                x[k1] = twm<INV>(x[k1], tw, t * k1);
         }
 #pragma unroll
         for (int k1 = 0; k1 < R; ++k1) srow[T * k1 + (t ^ (k1 & (T - 1)))] = x[k1];
@@ -249,18 +276,18 @@ __device__ __forceinline__ void row_fft(float2 (&x)[FFTCfg<N>::R], float2* srow,
 
 // ROW pass whose results stay in registers: X[j*T + k2] is column (j*T + t) + R*k2 of the row
 // (same arithmetic as row_fft; srow is used only for the exchange and is clobbered).
-template <int N, bool INV, bool TWR = false>
-__device__ __forceinline__ void row_fft_regs(float2 (&x)[FFTCfg<N>::R], float2* srow, int t, const float2* tw,
-                                             const float2* twr = nullptr) {
+template <int N, bool INV, bool TWR = false, typename TW = float2>
+__device__ __forceinline__ void row_fft_regs(float2 (&x)[FFTCfg<N>::R], float2* srow, int t, const TW* tw,
+                                             const TW* twr = nullptr) {
     constexpr int R = FFTCfg<N>::R, T = FFTCfg<N>::T;
     static_assert(T > 1, "row_fft_regs needs T > 1");
     DFT<R, INV>::run(x);
 #pragma unroll
     for (int k1 = 1; k1 < R; ++k1) {
         if constexpr (TWR)
-            x[k1] = twmul<INV>(x[k1], twr[k1 * T + t]);
+            x[k1] = twm<INV>(x[k1], twr, k1 * T + t);
         else
-            x[k1] = twmul<INV>(x[k1], tw[t * k1]);
+            x[k1] = twm<INV>(x[k1], tw, t * k1);
     }
     __syncwarp();
 #pragma unroll
@@ -280,8 +307,8 @@ __device__ __forceinline__ void row_fft_regs(float2 (&x)[FFTCfg<N>::R], float2* 
 
 // COLUMN pass phase 1 for column scol (pointer to element [0][c]); sub-thread t.
 // Reads rows T*n1 + t, writes the twiddled radix-R outputs back to rows T*k1 + t.
-template <int N, bool INV>
-__device__ __forceinline__ void col_fft_phase1(float2* scol, int t, const float2* tw) {
+template <int N, bool INV, typename TW = float2>
+__device__ __forceinline__ void col_fft_phase1(float2* scol, int t, const TW* tw) {
     constexpr int R = FFTCfg<N>::R, T = FFTCfg<N>::T, LD = FFTCfg<N>::LD;
     float2 x[R];
 #pragma unroll
@@ -289,7 +316,7 @@ __device__ __forceinline__ void col_fft_phase1(float2* scol, int t, const float2
     DFT<R, INV>::run(x);
     if constexpr (T > 1) {
 #pragma unroll
-        for (int k1 = 1; k1 < R; ++k1) x[k1] = twmul<INV>(x[k1], tw[t * k1]);
+        for (int k1 = 1; k1 < R; ++k1) x[k1] = twm<INV>(x[k1], tw, t * k1);
     }
 #pragma unroll
     for (int k1 = 0; k1 < R; ++k1) scol[(T * k1 + t) * LD] = x[k1];

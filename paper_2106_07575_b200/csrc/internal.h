@@ -38,6 +38,7 @@ struct DevState {
     int need_exact;          // pass + 1 when the screening pick left that pass undecided
     int k_unc;               // first undecided trial
     int n_exact;             // exact re-evaluations so far (diagnostic)
+    int n_pass, n_xpass;     // LS passes over the frames this iteration: screening, exact
     // device-side kernel timers (globaltimer ns) of the two frame kernels, [0] GRAD, [1] LS pass 0:
     // first CTA start / last CTA end of the current launch, folded into sums by k_begin_iter
     unsigned long long tk_start[2], tk_end[2];

@@ -120,7 +120,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(512, 1)
     __shared__ double sred[NW][KC];
     __shared__ double smom[NW][4];
     __shared__ float sgam[KC];
-    __shared__ LsWarpQ wq[NW];
+    __shared__ LsWarpQ<1> wq[NW];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t rank = c4_rank();
     const int64_t cid = c4_id(), ncl = c4_count();
@@ -213,21 +213,16 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(512, 1)
                     }
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
-                        const float2 vv = mine[(gi * 4 + e) * QC];
-                        st2_hint(vb + go + e * R * N, vv, pol);
-                        ls_push<KT, LSE>(wq[warp], qs, uc[e], vv, dc[e], gk, eps2, S, m, lane);
+                        float2 vv[1] = {mine[(gi * 4 + e) * QC]};
+                        float2 uu[1] = {uc[e]};
+                        float dd[1] = {dc[e]};
+                        st2_hint(vb + go + e * R * N, vv[0], pol);
+                        ls_push<KT, LSE>(wq[warp], qs, uu, vv, dd, gk, eps2, S, m, lane);
                     }
                 }
                 ls_flush<KT, LSE>(wq[warp], qs, gk, eps2, S, m, lane);
             });
-            double dv[KC];
-#pragma unroll
-            for (int k = 0; k < KC; ++k) dv[k] = (double)S[k];
-            tot += warp_reduce_scatter<KC>(dv, lane);
-            mom[0] += (double)m.A;
-            mom[1] += (double)m.D;
-            mom[2] += (double)m.sa;
-            mom[3] += (double)m.sb;
+            ls_run_out<KC>(S, m, tot, mom, lane);
         }
         __syncthreads();
         c4_arrive_relaxed();

@@ -111,11 +111,10 @@ __global__ void __launch_bounds__(512, 1) k_grad(Geometry g, float2* __restrict_
     constexpr int R = C::R, T = C::T, LD = C::LD;
     extern __shared__ float2 smem[];
     float2* sf = smem;
-    float2* tw = smem + C::FPB * C::FRAME_ELEMS;
+    float4* tw = reinterpret_cast<float4*>(smem + C::FPB * C::FRAME_ELEMS);
     if (st->numeric_error) return;
     ktime_start(st, 0);
-    build_twiddles<N>(tw);
-    build_row_twiddles<N>(tw + N);
+    build_twiddles4<N, true>(tw);
     __syncthreads();
     const float gam = (float)st->gamma;
     const bool upd = gam != 0.0f;
@@ -207,18 +206,17 @@ __global__ void __launch_bounds__(512, 1) k_ls(Geometry g, const float2* __restr
     constexpr int R = C::R, T = C::T, LD = C::LD;
     extern __shared__ float2 smem[];
     float2* sf = smem;
-    float2* tw = smem + C::FPB * C::FRAME_ELEMS;
+    float4* tw = reinterpret_cast<float4*>(smem + C::FPB * C::FRAME_ELEMS);
     __shared__ double sred[16][KC];
     __shared__ double smom[16][4];
     __shared__ float sgam[KC];
-    __shared__ LsWarpQ wq[16];
+    __shared__ LsWarpQ<2> wq[16];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const bool err = st->numeric_error != 0;
     int base, cnt;
     ls_pass_range(0, st->keff, cfg, base, cnt);
     ktime_start(st, 1);
-    build_twiddles<N>(tw);
-    build_row_twiddles<N>(tw + N);
+    build_twiddles4<N, false>(tw);
     if (tid < KC) sgam[tid] = (float)trial_gamma(cfg.gamma0, cfg.tau, base + tid);
     __syncthreads();
     const int64_t nfr = err ? 0 : g.n_local;
@@ -343,41 +341,38 @@ __global__ void __launch_bounds__(512, 1) k_ls(Geometry g, const float2* __restr
                                 dn[e] = ldg1_na(db + gn + e * R * N);
                             }
                         }
+                        float2 vc[4];
 #pragma unroll
                         for (int e = 0; e < 4; ++e) {
-                            float2 vv = sp[e * LD];
-                            if (valid) vb[go + e * R * N] = vv;
-                            else vv = make_float2(0.f, 0.f);
-                            ls_push<KT, LSE>(wq[warp], qs, uc[e], vv, dc[e], gk, eps2, S, m, lane);
+                            vc[e] = sp[e * LD];
+                            if (valid) vb[go + e * R * N] = vc[e];
+                            else vc[e] = make_float2(0.f, 0.f);
                         }
+                        ls_push<KT, LSE>(wq[warp], qs, slice<0, 2>(uc), slice<0, 2>(vc), slice<0, 2>(dc), gk, eps2,
+                                         S, m, lane);
+                        ls_push<KT, LSE>(wq[warp], qs, slice<2, 2>(uc), slice<2, 2>(vc), slice<2, 2>(dc), gk, eps2,
+                                         S, m, lane);
                     }
                 } else {
                     auto off = [&](int q) -> int { return ((q / T) * T + R * (q % T)) * N; };
 #pragma unroll 1
                     for (int q = 0; q < R; ++q) {
-                        float2 vv = scol[(T * ((q / T) * T + t) + q % T) * LD];
-                        float2 uu = make_float2(0.f, 0.f);
-                        float dd = 0.f;
+                        float2 vv[1] = {scol[(T * ((q / T) * T + t) + q % T) * LD]};
+                        float2 uu[1] = {make_float2(0.f, 0.f)};
+                        float dd[1] = {0.f};
                         if (valid) {
-                            uu = ub[off(q)];
-                            dd = __ldg(db + off(q));
-                            vb[off(q)] = vv;
+                            uu[0] = ub[off(q)];
+                            dd[0] = __ldg(db + off(q));
+                            vb[off(q)] = vv[0];
                         } else {
-                            vv = make_float2(0.f, 0.f);
+                            vv[0] = make_float2(0.f, 0.f);
                         }
                         ls_push<KT, LSE>(wq[warp], qs, uu, vv, dd, gk, eps2, S, m, lane);
                     }
                 }
                 ls_flush<KT, LSE>(wq[warp], qs, gk, eps2, S, m, lane);
             });
-            double dv[KC];
-#pragma unroll
-            for (int k = 0; k < KC; ++k) dv[k] = (double)S[k];
-            tot += warp_reduce_scatter<KC>(dv, lane);
-            mom[0] += (double)m.A;
-            mom[1] += (double)m.D;
-            mom[2] += (double)m.sa;
-            mom[3] += (double)m.sb;
+            ls_run_out<KC>(S, m, tot, mom, lane);
         }
         __syncthreads();
     }
@@ -421,8 +416,8 @@ template <int N>
 static int grad_n(const Geometry& g, float2* u, float2* v, const float* d, const float2* probe,
                   const DevState* st, float eps, int grid, cudaStream_t s) {
     using C = FFTCfg<N>;
-    if (set_smem(k_grad<N>, C::SMEM_BYTES)) return -1;
-    k_grad<N><<<grid, C::NT, C::SMEM_BYTES, s>>>(g, u, v, d, probe, st, eps);
+    if (set_smem(k_grad<N>, C::SMEM_BYTES4)) return -1;
+    k_grad<N><<<grid, C::NT, C::SMEM_BYTES4, s>>>(g, u, v, d, probe, st, eps);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
@@ -446,10 +441,10 @@ static int ls_n(const Geometry& g, const float2* eta, const float2* probe, const
                 const int* order, const float2* u, float2* v, const float* d, const SolverCfg& c,
                 double* part, int grid, const DevState* st, cudaStream_t s) {
     using C = FFTCfg<N>;
-    if (set_smem(k_ls<N>, C::SMEM_BYTES)) return -1;
+    if (set_smem(k_ls<N>, C::SMEM_BYTES4)) return -1;
     // L2 prefetch of each frame's u, d at its start (measured: k_ls 3.29 -> 3.23 ms at paper scale)
     static const int pf = getenv("PTYGER_PF") ? atoi(getenv("PTYGER_PF")) : 1;
-    k_ls<N><<<grid, C::NT, C::SMEM_BYTES, s>>>(g, eta, probe, pos, order, u, v, d, c, part, st, pf != 0);
+    k_ls<N><<<grid, C::NT, C::SMEM_BYTES4, s>>>(g, eta, probe, pos, order, u, v, d, c, part, st, pf != 0);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 

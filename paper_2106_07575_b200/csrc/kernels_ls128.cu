@@ -41,8 +41,11 @@ constexpr int RROWS = NF / T;                 // 32 rows per row-pass round
 constexpr int ROUNDS = N / RROWS;             // 4 row rounds
 constexpr int CROUNDS = N * T / NF;           // 4 column rounds of 32 columns
 constexpr size_t FRAME_BYTES = (size_t)N * LD * 8;                  // 139 264
-constexpr size_t TW_OFF = FRAME_BYTES;                              // tw[N], twr[R*T]
-constexpr size_t DYN_BYTES = TW_OFF + (size_t)(N + R * T) * 8;
+constexpr size_t TW_OFF = FRAME_BYTES;                              // float4 tw[N], twr[R*T]
+constexpr int SROWS = N / 2;                  // window rows staged ahead of the frame buffer
+constexpr int SLD = N + 8;                    // staged row stride (complex), same bank offset as LD
+constexpr size_t STG_OFF = TW_OFF + (size_t)(N + R * T) * 16;
+constexpr size_t DYN_BYTES = STG_OFF + (size_t)SROWS * SLD * 8;
 constexpr int TMEM_COLS = 512;
 // named barrier ids (0 is __syncthreads)
 constexpr int BAR_FFT = 1, BAR_FULL = 2, BAR_EMPTY = 4;
@@ -86,20 +89,20 @@ __global__ void __launch_bounds__(512, 1) k_ls_ws(Geometry g, const float2* __re
     using namespace ws;
     extern __shared__ __align__(16) unsigned char smraw[];
     float2* sf = reinterpret_cast<float2*>(smraw);
-    float2* tw = reinterpret_cast<float2*>(smraw + TW_OFF);
+    float4* tw = reinterpret_cast<float4*>(smraw + TW_OFF);
     __shared__ double sred[16][KC];
     __shared__ double smom[16][4];
     __shared__ float sgam[KC];
-    __shared__ LsWarpQ wq[8];
+    __shared__ LsWarpQ<2> wq[8];
     __shared__ uint32_t s_tmem;
-    __shared__ __align__(8) uint64_t s_mbar;
+    __shared__ __align__(8) uint64_t s_mbar[2];   // [0] staged rows 0..63, [1] rows 64..127 in sf
+    float2* stg = reinterpret_cast<float2*>(smraw + STG_OFF);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const bool err = st->numeric_error != 0;
     int base, cnt;
     ls_pass_range(0, st->keff, cfg, base, cnt);
     ktime_start(st, 1);
-    build_twiddles<N>(tw);
-    build_row_twiddles<N>(tw + N);
+    build_twiddles4<N, false>(tw);
     if (tid < KC) sgam[tid] = (float)trial_gamma(cfg.gamma0, cfg.tau, base + tid);
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
@@ -107,7 +110,8 @@ __global__ void __launch_bounds__(512, 1) k_ls_ws(Geometry g, const float2* __re
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     if (tid == 0) {
-        mbar_init(&s_mbar, 1);
+        mbar_init(&s_mbar[0], 1);
+        mbar_init(&s_mbar[1], 1);
         fence_mbar_init();
     }
     tc_fence_before();
@@ -120,21 +124,27 @@ __global__ void __launch_bounds__(512, 1) k_ls_ws(Geometry g, const float2* __re
     const int wq4 = warp & 3, whalf = (warp & 7) >> 2;
     const uint32_t tq = tbase + ((uint32_t)(32 * wq4) << 16) + (uint32_t)(128 * whalf);
 
-    // TMA bulk copies of frame i's eta window rows into the frame buffer (warp 0 of the FFT group).
-    // Row r goes to sf + r LD; a window starting at an odd column is copied from the column before it
-    // (16-B alignment, 130 elements), so the row pass reads it at offset 1.
-    auto issue_dma = [&](int64_t i) {
+    // TMA bulk copies of frame i's eta window rows [h 64, h 64 + 64) (warp 0 of the FFT group, one
+    // row per lane and step): h = 0 into the staging buffer, issued as soon as the previous frame's
+    // row pass has read it (so it flies during that frame's column pass and epilogue hand-off);
+    // h = 1 into rows 64..127 of the frame buffer, issued once the previous frame's column pass
+    // has released it (it flies during this frame's first two row rounds).  A window starting at an
+    // odd column is copied from the column before it (16-B alignment, 130 elements) and read at
+    // offset 1.
+    auto issue_dma = [&](int64_t i, int h) {
         const int j = order[i];
         const int2 s = pos[j];
         const int off = s.y & 1;
         const uint32_t bytes = (uint32_t)(N + 2 * off) * 8u;
-        if (lane == 0) mbar_arrive_expect_tx(&s_mbar, bytes * N);
+        if (lane == 0) mbar_arrive_expect_tx(&s_mbar[h], bytes * SROWS);
         __syncwarp();
-        const float2* src = eta + (int64_t)s.x * W + (s.y - off);
+        const float2* src = eta + (int64_t)(s.x + h * SROWS) * W + (s.y - off);
+        float2* dst = h ? sf + SROWS * LD : stg;
+        const int ld = h ? LD : SLD;
 #pragma unroll
-        for (int q = 0; q < N / 32; ++q) {
+        for (int q = 0; q < SROWS / 32; ++q) {
             const int r = q * 32 + lane;
-            bulk_g2s(sf + r * LD, src + (int64_t)r * W, bytes, &s_mbar);
+            bulk_g2s(dst + r * ld, src + (int64_t)r * W, bytes, &s_mbar[h]);
         }
     };
 
@@ -143,20 +153,22 @@ __global__ void __launch_bounds__(512, 1) k_ls_ws(Geometry g, const float2* __re
     if (tid < NF) {
         // ============================ FFT group ============================
         const int ft = tid;
-        if (DMA && warp == 0 && blockIdx.x < nfr) issue_dma(blockIdx.x);
+        if (DMA && warp == 0 && blockIdx.x < nfr) {
+            issue_dma(blockIdx.x, 0);
+            issue_dma(blockIdx.x, 1);
+        }
         int it = 0;
         for (int64_t i = blockIdx.x; i < nfr; i += gridDim.x, ++it) {
             const int b = it & 1;
             const int j = order[i];
             const int2 s = pos[j];
-            if (DMA) mbar_wait(&s_mbar, (uint32_t)(it & 1));
             // ---- row pass: 4 rounds of 32 rows, two rounds' inputs in flight at a time
             const int t = ft % T, rrow = ft / T;
             auto load_row = [&](int rd, float2 (&x)[R]) {
                 const int row = rd * RROWS + rrow;
                 const float2* pp = probe_s + row * N + t;
                 if constexpr (DMA) {
-                    const float2* se = sf + row * LD + (s.y & 1) + t;
+                    const float2* se = (row < SROWS ? stg + row * SLD : sf + row * LD) + (s.y & 1) + t;
 #pragma unroll
                     for (int n1 = 0; n1 < R; ++n1) x[n1] = cmul(ldg2(pp + T * n1), se[T * n1]);
                 } else {
@@ -165,12 +177,19 @@ __global__ void __launch_bounds__(512, 1) k_ls_ws(Geometry g, const float2* __re
             };
 #pragma unroll 1
             for (int rp = 0; rp < ROUNDS; rp += 2) {
+                if (DMA) mbar_wait(&s_mbar[rp / 2], (uint32_t)(it & 1));
                 float2 xa[R], xb[R];
                 load_row(rp, xa);
                 load_row(rp + 1, xb);
                 __syncwarp();   // every lane of the warp has read its rows before any exchange write
                 row_fft<N, false, true>(xa, sf + (rp * RROWS + rrow) * LD, t, tw, tw + N);
                 row_fft<N, false, true>(xb, sf + ((rp + 1) * RROWS + rrow) * LD, t, tw, tw + N);
+                if (DMA && rp == 0) {
+                    // the staged rows are consumed: the next frame's first half may land there
+                    fence_proxy_async();
+                    bar_sync_n(BAR_FFT, NF);
+                    if (warp == 0 && i + gridDim.x < nfr) issue_dma(i + gridDim.x, 0);
+                }
             }
             bar_sync_n(BAR_FFT, NF);
             // ---- column pass phase 1: 4 rounds of 32 columns, sub-thread t = warp
@@ -192,11 +211,11 @@ __global__ void __launch_bounds__(512, 1) k_ls_ws(Geometry g, const float2* __re
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             tc_fence_before();
             bar_arrive_n(BAR_FULL + b, NT);
-            // ---- the frame buffer is free: the next frame's window copy flies during the wait
+            // ---- the frame buffer is free: the next frame's second window half may land in it
             if (DMA) {
                 fence_proxy_async();
                 bar_sync_n(BAR_FFT, NF);
-                if (warp == 0 && i + gridDim.x < nfr) issue_dma(i + gridDim.x);
+                if (warp == 0 && i + gridDim.x < nfr) issue_dma(i + gridDim.x, 1);
             } else {
                 bar_sync_n(BAR_FFT, NF);
             }
@@ -264,20 +283,14 @@ __global__ void __launch_bounds__(512, 1) k_ls_ws(Geometry g, const float2* __re
                         float2 X[4];
                         tmem_ld8(tq + (uint32_t)(256 * b + 32 * rd + 8 * gi), X);
 #pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            vb[go + e * R * N] = X[e];
-                            ls_push<KT, LSE>(wq[ew], qs, uc[e], X[e], dc[e], gk, eps2, S, m, lane);
-                        }
+                        for (int e = 0; e < 4; ++e) vb[go + e * R * N] = X[e];
+                        ls_push<KT, LSE>(wq[ew], qs, slice<0, 2>(uc), slice<0, 2>(X), slice<0, 2>(dc), gk, eps2, S,
+                                         m, lane);
+                        ls_push<KT, LSE>(wq[ew], qs, slice<2, 2>(uc), slice<2, 2>(X), slice<2, 2>(dc), gk, eps2, S,
+                                         m, lane);
                     }
                     ls_flush<KT, LSE>(wq[ew], qs, gk, eps2, S, m, lane);
-                    double dv[KC];
-#pragma unroll
-                    for (int k = 0; k < KC; ++k) dv[k] = (double)S[k];
-                    tot += warp_reduce_scatter<KC>(dv, lane);
-                    mom[0] += (double)m.A;
-                    mom[1] += (double)m.D;
-                    mom[2] += (double)m.sa;
-                    mom[3] += (double)m.sb;
+                    ls_run_out<KC>(S, m, tot, mom, lane);
                 }
                 // slot b read: the FFT group may overwrite it (frame it + 2) -- no arrival without a waiter
                 tc_fence_before();

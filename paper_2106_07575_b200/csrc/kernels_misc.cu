@@ -307,6 +307,7 @@ __global__ void k_begin_iter(DevState* st) {
     st->accepted = 0;
     st->kstar = -1;
     st->n_eval = 0;
+    st->n_pass = st->n_xpass = 0;
     st->restarted = 0;
     st->stalled = 0;
     st->need_exact = 0;
@@ -405,7 +406,7 @@ __global__ void __launch_bounds__(256) k_lsx(int64_t count, const float2* __rest
     __shared__ double sred[8][KC];
     __shared__ double smom[8][4];
     __shared__ float sgam[KC];
-    __shared__ LsWarpQ wq[EXACT ? 1 : 8];
+    __shared__ LsWarpQ<2> wq[EXACT ? 1 : 8];
     const int tid = threadIdx.x, lane = tid & 31;
     int base, cnt;
     ls_pass_range(pass, st->keff, cfg, base, cnt);
@@ -436,25 +437,32 @@ __global__ void __launch_bounds__(256) k_lsx(int64_t count, const float2* __rest
                 } else {
                     // warp-collective d > 0 compaction: out-of-range lanes push zeros
                     LsQState qs;
-#pragma unroll 4
-                    for (int i = 0; i < RUN; ++i) {
-                        const int64_t o = e0 + (int64_t)i * blockDim.x + tid;
-                        const bool ok = o < count;
-                        ls_push<KT, LSE>(wq[tid >> 5], qs, ok ? u[o] : make_float2(0.f, 0.f),
-                                    ok ? v[o] : make_float2(0.f, 0.f), ok ? __ldg(d + o) : 0.f, sgam, eps2, S, m,
-                                    lane);
+#pragma unroll 2
+                    for (int i = 0; i < RUN; i += 2) {
+                        float2 uu[2], vv[2];
+                        float dd[2];
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            const int64_t o = e0 + (int64_t)(i + e) * blockDim.x + tid;
+                            const bool ok = o < count;
+                            uu[e] = ok ? u[o] : make_float2(0.f, 0.f);
+                            vv[e] = ok ? v[o] : make_float2(0.f, 0.f);
+                            dd[e] = ok ? __ldg(d + o) : 0.f;
+                        }
+                        ls_push<KT, LSE>(wq[tid >> 5], qs, uu, vv, dd, sgam, eps2, S, m, lane);
                     }
                     ls_flush<KT, LSE>(wq[tid >> 5], qs, sgam, eps2, S, m, lane);
                 }
             });
-            double dv[KC];
+            if constexpr (EXACT) {
+                // the exact sums keep the fp64 reduce-scatter (no screening bound to absorb fp32 levels)
+                double dv[KC];
 #pragma unroll
-            for (int k = 0; k < KC; ++k) dv[k] = (double)S[k];
-            tot += warp_reduce_scatter<KC>(dv, lane);
-            mom[0] += (double)m.A;
-            mom[1] += (double)m.D;
-            mom[2] += (double)m.sa;
-            mom[3] += (double)m.sb;
+                for (int k = 0; k < KC; ++k) dv[k] = (double)S[k];
+                tot += warp_reduce_scatter<KC>(dv, lane);
+            } else {
+                ls_run_out<KC>(S, m, tot, mom, lane);
+            }
         }
     }
     ls_block_out<KC, 8>(tot, mom, sred, smom, part);
@@ -481,6 +489,7 @@ __device__ void pick_body(DevState* st, const SolverCfg& c, int pass, int exact_
                             LS_EPS_R * (st->ls_pass[KC] + c.gamma0 * st->ls_pass[KC + 2] +
                                         c.gamma0 * c.gamma0 * st->ls_pass[KC + 3]);
             st->n_eval = 1;
+            st->n_pass = 1;
             st->accepted = 1;
             st->kstar = 0;
             st->gamma = c.gamma0;
@@ -491,6 +500,7 @@ __device__ void pick_body(DevState* st, const SolverCfg& c, int pass, int exact_
             st->ls_hist[0] = dF;
             st->ls_bnd[0] = 0.0;
             st->n_exact += 1;
+            st->n_xpass = 1;
             if (!isfinite(dF)) {
                 st->numeric_error = 2;
                 st->err_iter = st->m;
@@ -501,6 +511,8 @@ __device__ void pick_body(DevState* st, const SolverCfg& c, int pass, int exact_
         }
     }
     if (!st->numeric_error && !st->accepted && cnt > 0) {
+        if (!exact_mode) st->n_pass += 1;
+        else if (st->need_exact == pass + 1) st->n_xpass += 1;
         if (!exact_mode) {
             const double A = st->ls_pass[KC], D = st->ls_pass[KC + 1];
             const double sa = st->ls_pass[KC + 2], sb = st->ls_pass[KC + 3];
@@ -575,6 +587,8 @@ __device__ void pick_body(DevState* st, const SolverCfg& c, int pass, int exact_
     t.grad_norm = sqrt(st->dy[0]);
     t.step_norm = st->gamma * sqrt(st->eta2);
     t.ms_grad = t.ms_dir = t.ms_ls = t.ms_update = t.ms_comm = 0.f;   // filled by the final stamp
+    t.ls_passes = st->n_pass;
+    t.ls_exact_passes = st->n_xpass;
     if (st->trace_ptr && st->trace_idx < st->trace_cap) st->trace_ptr[st->trace_idx] = t;
     st->trace_idx += 1;
     st->trace_written = 1;

@@ -40,7 +40,7 @@ __device__ __forceinline__ void n256_column(const float2* __restrict__ src, int 
     c = cb * COLB + lane;
     float2 x[R];
 #pragma unroll
-    for (int n1 = 0; n1 < R; ++n1) x[n1] = src[(int64_t)(T * n1 + t) * N + c];
+    for (int n1 = 0; n1 < R; ++n1) x[n1] = __ldcg(src + (int64_t)(T * n1 + t) * N + c);
     DFT<R, INV>::run(x);
 #pragma unroll
     for (int k1 = 1; k1 < R; ++k1) x[k1] = twmul<INV>(x[k1], tw[t * k1]);
@@ -56,30 +56,40 @@ __device__ __forceinline__ void n256_column(const float2* __restrict__ src, int 
 
 // ---------------------------------------------------------------------------------------------
 // k_grad (N = 256): u <- u + gamma v, r = u - d/u^*, y = conj(p) F^H r into v's slot.
+// A CLUSTER PAIR of CTAs shares each frame: CTA r transforms rows [128 r, 128 r + 128) in pass 1 and
+// columns [128 r, 128 r + 128) in pass 2, with one cluster barrier (release / acquire: the slot rows
+// the peer wrote are visible) in between.  Against one CTA per frame this halves the slot
+// intermediates in flight (74 x 512 KB instead of 148 x 512 KB), which otherwise overflowed L2
+// (ncu r2b: 39.4 B/px DRAM against 36 algorithmic).
 // ---------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(512, 1) k_grad256(Geometry g, float2* __restrict__ u, float2* __restrict__ v,
-                                                    const float* __restrict__ d, const float2* __restrict__ probe,
-                                                    const DevState* __restrict__ st, float eps) {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1)
+    k_grad256(Geometry g, float2* __restrict__ u, float2* __restrict__ v, const float* __restrict__ d,
+              const float2* __restrict__ probe, const DevState* __restrict__ st, float eps) {
     using namespace n256;
     extern __shared__ float2 smem[];
     float2* buf = smem;
     float2* tw = smem + BUF;
-    if (st->numeric_error) return;
+    if (st->numeric_error) return;   // uniform over the grid: both CTAs of a pair leave together
     ktime_start(st, 0);
     build_twiddles<N>(tw);
     build_row_twiddles<N>(tw + N);
     __syncthreads();
+    uint32_t rank, cid, ncl;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(cid));
+    asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(ncl));
     const float gam = (float)st->gamma;
     const bool upd = gam != 0.0f;
     const float eps2 = eps * eps, scale = 1.0f / (float)N;
     const int tid = threadIdx.x;
+    constexpr int HB = N / ROWB / 2;   // row batches (and column batches) per CTA
     // streamed once: u, v, d reads and the u / y writes; reused within microseconds: the slot rows
     const uint64_t pol_s = l2_evict_first(), pol_k = l2_evict_last();
-    for (int64_t j = blockIdx.x; j < g.n_local; j += gridDim.x) {
+    for (int64_t j = cid; j < g.n_local; j += ncl) {
         float2* vj = v + j * N * N;
-        // pass 1: rows
+        // pass 1: this CTA's rows
 #pragma unroll 1
-        for (int rb = 0; rb < N / ROWB; ++rb) {
+        for (int rb = rank * HB; rb < (int)(rank + 1) * HB; ++rb) {
             const int row = rb * ROWB + tid / T, t = tid % T;
             const int64_t base = j * N * N + (int64_t)row * N + t;
             float2 uu[R];
@@ -110,10 +120,12 @@ __global__ void __launch_bounds__(512, 1) k_grad256(Geometry g, float2* __restri
 #pragma unroll
             for (int k2 = 0; k2 < T; ++k2) st2_hint(dst + R * k2, x[k2], pol_k);
         }
-        __syncthreads();
-        // pass 2: columns, epilogue y = conj(p) X / N
+        // both halves of the row pass are in the slot (cluster-scope release / acquire)
+        asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+        asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+        // pass 2: this CTA's columns, epilogue y = conj(p) X / N
 #pragma unroll 1
-        for (int cb = 0; cb < N / COLB; ++cb) {
+        for (int cb = rank * (N / COLB / 2); cb < (int)(rank + 1) * (N / COLB / 2); ++cb) {
             float2 X[16];
             int c;
             n256_column<true>(vj, cb, buf, tw, X, c);
@@ -241,8 +253,23 @@ static int n256_smem(F* f) {
 
 int launch_grad256(const Geometry& g, float2* u, float2* v, const float* d, const float2* probe, const DevState* st,
                    float eps, int grid, cudaStream_t s) {
+    (void)grid;
+    static int pairs = 0;   // resident cluster pairs (one CTA per SM)
     if (n256_smem(k_grad256)) return -1;
-    k_grad256<<<grid, 512, n256::SMEM, s>>>(g, u, v, d, probe, st, eps);
+    if (pairs == 0) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(2 * 74, 1, 1);
+        cfg.blockDim = dim3(512, 1, 1);
+        cfg.dynamicSmemBytes = n256::SMEM;
+        int ncl = 0;
+        if (cudaOccupancyMaxActiveClusters(&ncl, k_grad256, &cfg) != cudaSuccess || ncl <= 0) {
+            cudaGetLastError();
+            ncl = 148 / 2;
+        }
+        pairs = ncl;
+    }
+    const int64_t np = g.n_local < pairs ? (g.n_local > 0 ? g.n_local : 1) : pairs;
+    k_grad256<<<(int)(2 * np), 512, n256::SMEM, s>>>(g, u, v, d, probe, st, eps);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
