@@ -131,6 +131,7 @@ struct ptyger_ctx {
     int* tile_ptr = nullptr;
     int* entries = nullptr;
     float2* frac = nullptr;      // per storage frame fractional offsets (subpixel mode only)
+    float* illum = nullptr;      // I = diag(G^H G) over the storage rows (object-grid LS moments, sc.qg)
     bool subpx = false;
     int ntx = 0, nty = 0;
     double *part_adj = nullptr, *part_fr = nullptr, *part_el = nullptr, *scratch = nullptr;
@@ -273,9 +274,10 @@ static int enqueue_iteration(ptyger_ctx* c, int p, std::string& err, int64_t& la
         LK(launch_dir(c->st, sc, s));
         ++launches;
     }
-    LK(launch_eta(g, gcur, c->eta, c->st, c->part_el, c->grid_el, s)); ++launches;
-    // ||eta||^2: summed over ranks here with the peer-memory transport (NCCL: with the pass-0 LS vector)
-    LK(launch_reduce(c->part_el, c->grid_el, 1, &c->st->ls_pass[LS_ETA], s, c->st, 0, 0, fuse)); ++launches;
+    LK(launch_eta(g, gcur, c->eta, sc.qg ? c->psi : nullptr, c->illum, c->st, c->part_el, c->grid_el, s)); ++launches;
+    // ||eta||^2 and the object-grid moments: summed over ranks here with the peer-memory transport (NCCL:
+    // with the pass-0 LS vector)
+    LK(launch_reduce(c->part_el, c->grid_el, 4, &c->st->ls_pass[LS_ETA], s, c->st, 0, 0, fuse)); ++launches;
     LK(launch_stamp(c->st, 2, s));   // DIR stage done
     ++launches;
     // LS stage (Alg.1 659-668).  Pass 0 computes v = G eta and screens trials 0..K-1; every pass
@@ -386,7 +388,7 @@ static void free_ctx(ptyger_ctx* c) {
     if (c->p2p) c->full = c->recv[0] = c->recv[1] = nullptr;   // inside the exchange window
     void* ptrs[] = {c->psi, c->g[0], c->g[1], c->eta, c->u, c->v, c->probe, c->probe_s, c->full, c->recv[0], c->recv[1], c->d,
                     c->pos, c->order, c->frac, c->tile_ptr, c->entries, c->part_adj, c->part_fr, c->part_el, c->scratch, c->st,
-                    c->d_tr};
+                    c->d_tr, c->illum};
     if (c->stream) cudaStreamSynchronize(c->stream);
     for (void* p : ptrs)
         if (p) cudaFreeAsync(p, 0);
@@ -498,6 +500,8 @@ static ptyger_status init_impl(ptyger_ctx* c, const float* object, const float* 
     if (fr)
         for (int64_t i = 0; i < 2 * n; ++i)
             if (fr[i] != 0.0f) c->subpx = true;
+    // the LS trials' non-log part from the object grid (G^H G = diag(I)): Poisson ML, integer positions
+    c->sc.qg = (c->sc.est == PTYGER_EST_ML && !c->subpx) ? 1 : 0;
     // ---- partition (host) ----
     const int foot = N + (c->subpx ? 1 : 0);
     const int rc = partition(scan, n, H, N, cfg.world, c->frame_rank, c->rows, err, foot);
@@ -724,6 +728,11 @@ static ptyger_status init_impl(ptyger_ctx* c, const float* object, const float* 
     }
     CK(cudaMemcpyAsync(c->tile_ptr, tptr.data(), sizeof(int) * tptr.size(), cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(c->entries, ent.data(), sizeof(int) * ent.size(), cudaMemcpyHostToDevice, c->stream));
+    if (c->sc.qg) {
+        c->illum = dalloc<float>((size_t)(c->SH * W), err, false);
+        if (!c->illum) return PTYGER_E_OOM;
+        LK(launch_illum(c->geo, c->probe, c->tile_ptr, c->entries, c->ntx, c->nty, c->illum, c->stream));
+    }
     init_trace("small uploads issued");
     unsigned long long* bad = dalloc<unsigned long long>(1, err, false);
     if (!bad) return PTYGER_E_OOM;

@@ -229,14 +229,17 @@ __device__ __forceinline__ float log1p_poly(float z) {
 }
 
 // Guarded exact definition, used where |u| < eps or |u + gamma v| < eps or 1 + z underflows.
-static __device__ __noinline__ float ls_term_slow(float a, float b, float c, float dd, float gam, float eps2) {
+// qg: the log part only (the non-log part q comes from the object grid, SolverCfg::qg).
+static __device__ __noinline__ float ls_term_slow(float a, float b, float c, float dd, float gam, float eps2,
+                                                  bool qg) {
     const float q = gam * fmaf(gam, b, a);
     const float cn = c + q;
     if (c >= eps2 && cn >= eps2) {
         const float z = q / c;
-        if (z > -0.999f) return fmaf(-dd, log1p_poly(z), q);
+        if (z > -0.999f) return qg ? -dd * log1p_poly(z) : fmaf(-dd, log1p_poly(z), q);
     }
-    return (cn - c) - dd * (logf(fmaxf(cn, eps2)) - logf(fmaxf(c, eps2)));
+    const float lg = -dd * (logf(fmaxf(cn, eps2)) - logf(fmaxf(c, eps2)));
+    return qg ? lg : (cn - c) + lg;
 }
 
 // Least-squares estimator terms t = q (1 - 2 sqrt(d) / (|u + g v| + |u|)), q = |u + g v|^2 - |u|^2
@@ -259,7 +262,7 @@ __device__ __forceinline__ void ls_screen_lse(float2 uu, float2 vv, float dd, co
 // EXACT terms (accurate log1p, ~1.7e-7 relative): t_k = q_k - d log1p(q_k / c).  Branch-free
 // fast path; a lane needing the guarded definition sends its warp through ls_term_slow.
 // KT trials (compile time) accumulate into acc[0..KT).
-template <int KT, bool LSE, int K>
+template <int KT, bool LSE, bool QG, int K>
 __device__ __forceinline__ void ls_exact(float2 uu, float2 vv, float dd, const float* sgam, float eps2,
                                          float (&acc)[K]) {
     static_assert(KT <= K, "trial count above capacity");
@@ -279,12 +282,12 @@ __device__ __forceinline__ void ls_exact(float2 uu, float2 vv, float dd, const f
         const float q = gam * fmaf(gam, b, a);
         const float z = q * rc;
         bad |= (c + q < eps2) | (z <= -0.999f);
-        t[k] = fmaf(-dd, log1p_poly(fmaxf(z, -0.999f)), q);
+        t[k] = QG ? -dd * log1p_poly(fmaxf(z, -0.999f)) : fmaf(-dd, log1p_poly(fmaxf(z, -0.999f)), q);
     }
     if (__any_sync(__activemask(), bad)) {
         if (bad) {
 #pragma unroll
-            for (int k = 0; k < KT; ++k) t[k] = ls_term_slow(a, b, c, dd, sgam[k], eps2);
+            for (int k = 0; k < KT; ++k) t[k] = ls_term_slow(a, b, c, dd, sgam[k], eps2, QG);
         }
     }
 #pragma unroll
@@ -341,7 +344,7 @@ struct LsWarpQ {
 // ML: cn = |u + gamma v|^2 is formed from the components of u + gamma v (each an fma of exact
 // inputs, correctly rounded), so w = cn / c keeps a few-ulp RELATIVE accuracy even when u + gamma v
 // nearly cancels (a pre-scaled u / |u| would lose it).
-template <int KT, bool LSE, int K, typename G>
+template <int KT, bool LSE, bool QG, int K, typename G>
 __device__ __forceinline__ void ls_screen_nz(float4 uv, float dd, const G& sgam, float eps2, float (&S)[K],
                                              LsMom& m) {
     const float2 uu = make_float2(uv.x, uv.y), vv = make_float2(uv.z, uv.w);
@@ -353,6 +356,7 @@ __device__ __forceinline__ void ls_screen_nz(float4 uv, float dd, const G& sgam,
         // applies the guarded definition R#4 (as does an FTZ underflow of w)
         const float rc = (c >= eps2) ? __fdividef(1.0f, c) : 0.0f;
         const float dl = dd * 0.693147182464599609375f;
+        if (QG) m.D += dd;   // the bound's D = sum d (no q-moment rounding to cover)
         float amax = 0.f;
         // Trials run in pairs on the paired FP32 pipe (FFMA2 / FMUL2: per lane the same fp32
         // operations as the scalar form).
@@ -404,13 +408,13 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 }
 
 // Screen every full batch of 32 queued pixels; move the remainder to the front of the queue.
-template <int KT, bool LSE, int QN, int K, typename G>
+template <int KT, bool LSE, bool QG, int QN, int K, typename G>
 __device__ __forceinline__ void ls_drain_full(LsWarpQ<QN>& q, LsQState& qs, const G& sgam, float eps2,
                                               float (&S)[K], LsMom& m, int lane) {
     __syncwarp();
     int b = 0;
 #pragma unroll 1
-    for (; b + 32 <= qs.pending; b += 32) ls_screen_nz<KT, LSE>(q.uv[b + lane], q.d[b + lane], sgam, eps2, S, m);
+    for (; b + 32 <= qs.pending; b += 32) ls_screen_nz<KT, LSE, QG>(q.uv[b + lane], q.d[b + lane], sgam, eps2, S, m);
     const int rem = qs.pending - b;
     float4 tu = make_float4(0.f, 0.f, 0.f, 0.f);
     float td = 0.f;
@@ -428,7 +432,9 @@ __device__ __forceinline__ void ls_drain_full(LsWarpQ<QN>& q, LsQState& qs, cons
 }
 
 // Push NP pixels per lane (all lanes together) into a queue sized for QN >= NP.
-template <int KT, bool LSE, int QN, int NP, int K, typename G>
+// QG (SolverCfg::qg): no per-pixel moments at all (the non-log part and the bound's q terms come from the
+// object grid); only the d > 0 compaction remains.
+template <int KT, bool LSE, bool QG, int QN, int NP, int K, typename G>
 __device__ __forceinline__ void ls_push(LsWarpQ<QN>& q, LsQState& qs, const float2 (&uu)[NP],
                                         const float2 (&vv)[NP], const float (&dd)[NP], const G& sgam, float eps2,
                                         float (&S)[K], LsMom& m, int lane) {
@@ -438,16 +444,18 @@ __device__ __forceinline__ void ls_push(LsWarpQ<QN>& q, LsQState& qs, const floa
 #pragma unroll
     for (int e = 0; e < NP; ++e) {
         const float2 u = uu[e], v = vv[e];
-        const float a2 = fmaf(u.x, v.x, u.y * v.y);   // a / 2
-        const float b = fmaf(v.x, v.x, v.y * v.y);
-        const float c = fmaf(u.x, u.x, u.y * u.y);
-        m.D += fmaf(0.12f, c, dd[e]);
-        m.sa2 += fabsf(a2);
-        if (LSE) m.sb += b;   // Poisson ML: sum b is zb (all pixels), folded in at ls_flush
         const bool nz = dd[e] != 0.0f;
-        if (!LSE || !nz) {
-            qs.za2 += a2;
-            qs.zb += b;
+        if constexpr (!QG) {
+            const float a2 = fmaf(u.x, v.x, u.y * v.y);   // a / 2
+            const float b = fmaf(v.x, v.x, v.y * v.y);
+            const float c = fmaf(u.x, u.x, u.y * u.y);
+            m.D += fmaf(0.12f, c, dd[e]);
+            m.sa2 += fabsf(a2);
+            if (LSE) m.sb += b;   // Poisson ML: sum b is zb (all pixels), folded in at ls_flush
+            if (!LSE || !nz) {
+                qs.za2 += a2;
+                qs.zb += b;
+            }
         }
         const unsigned mask = __ballot_sync(FULLMASK, nz);
         if (nz) {
@@ -458,24 +466,26 @@ __device__ __forceinline__ void ls_push(LsWarpQ<QN>& q, LsQState& qs, const floa
         off += __popc(mask);
     }
     qs.pending = off;
-    if (off >= 32) ls_drain_full<KT, LSE>(q, qs, sgam, eps2, S, m, lane);
+    if (off >= 32) ls_drain_full<KT, LSE, QG>(q, qs, sgam, eps2, S, m, lane);
 }
 
 // Drain the queue and fold the (za, zb) moments into S (call once per accumulation run).
-template <int KT, bool LSE, int QN, int K, typename G>
+template <int KT, bool LSE, bool QG, int QN, int K, typename G>
 __device__ __forceinline__ void ls_flush(LsWarpQ<QN>& q, LsQState& qs, const G& sgam, float eps2, float (&S)[K],
                                          LsMom& m, int lane) {
     if (qs.pending > 0) {
         __syncwarp();
-        if (lane < qs.pending) ls_screen_nz<KT, LSE>(q.uv[lane], q.d[lane], sgam, eps2, S, m);
+        if (lane < qs.pending) ls_screen_nz<KT, LSE, QG>(q.uv[lane], q.d[lane], sgam, eps2, S, m);
         qs.pending = 0;
         __syncwarp();
     }
-    const float za = 2.0f * qs.za2;
+    if constexpr (!QG) {
+        const float za = 2.0f * qs.za2;
 #pragma unroll
-    for (int k = 0; k < KT; ++k) S[k] += sgam[k] * fmaf(sgam[k], qs.zb, za);
-    if (!LSE) m.sb += qs.zb;
-    qs.za2 = qs.zb = 0.f;
+        for (int k = 0; k < KT; ++k) S[k] += sgam[k] * fmaf(sgam[k], qs.zb, za);
+        if (!LSE) m.sb += qs.zb;
+        qs.za2 = qs.zb = 0.f;
+    }
 }
 
 // Warp reduce-scatter of the K per-lane fp32 trial sums in fp32 (5 rounding levels of 2^-24 relative
@@ -512,41 +522,44 @@ __device__ __forceinline__ void ls_run_out(float (&S)[K], const LsMom& m, double
     mom[3] += (double)m.sb;
 }
 
-// Run body.template operator()<KT>() with KT = cnt (4..10) or cnt rounded up to an even count (<= 16):
-// the trial count of a pass is uniform for the whole launch, so one branch at the top selects a
+// Run body.template operator()<KT, LSE, QG>() with KT = cnt (4..10) or cnt rounded up to an even count
+// (<= 16): the trial count of a pass is uniform for the whole launch, so one branch at the top selects a
 // fully unrolled variant and only its code is executed (instruction-cache footprint of one).
 // Exact variants cover the adaptive pass-0 counts k*_prev + 3 around the typical k* = 4..7.
-template <bool LSE, typename F>
+template <bool LSE, bool QG, typename F>
 __device__ __forceinline__ void trial_dispatch_k(int cnt, F& body) {
     if (cnt <= 4)
-        body.template operator()<4, LSE>();
+        body.template operator()<4, LSE, QG>();
     else if (cnt == 5)
-        body.template operator()<5, LSE>();
+        body.template operator()<5, LSE, QG>();
     else if (cnt == 6)
-        body.template operator()<6, LSE>();
+        body.template operator()<6, LSE, QG>();
     else if (cnt == 7)
-        body.template operator()<7, LSE>();
+        body.template operator()<7, LSE, QG>();
     else if (cnt == 8)
-        body.template operator()<8, LSE>();
+        body.template operator()<8, LSE, QG>();
     else if (cnt == 9)
-        body.template operator()<9, LSE>();
+        body.template operator()<9, LSE, QG>();
     else if (cnt == 10)
-        body.template operator()<10, LSE>();
+        body.template operator()<10, LSE, QG>();
     else if (cnt <= 12)
-        body.template operator()<12, LSE>();
+        body.template operator()<12, LSE, QG>();
     else if (cnt <= 14)
-        body.template operator()<14, LSE>();
+        body.template operator()<14, LSE, QG>();
     else
-        body.template operator()<16, LSE>();
+        body.template operator()<16, LSE, QG>();
 }
 
-// ... and on the estimator (uniform for the whole run): body<KT, LSE>.
+// ... and on the estimator and the moment source (uniform for the whole run): body<KT, LSE, QG>.
+// The least-squares estimator keeps the per-pixel moments (its d > 0 term is not separable).
 template <typename F>
-__device__ __forceinline__ void trial_dispatch(int cnt, int est, F&& body) {
-    if (est == PTYGER_EST_LS)
-        trial_dispatch_k<true>(cnt, body);
+__device__ __forceinline__ void trial_dispatch(int cnt, const SolverCfg& c, F&& body) {
+    if (c.est == PTYGER_EST_LS)
+        trial_dispatch_k<true, false>(cnt, body);
+    else if (c.qg)
+        trial_dispatch_k<false, true>(cnt, body);
     else
-        trial_dispatch_k<false>(cnt, body);
+        trial_dispatch_k<false, false>(cnt, body);
 }
 
 // Block-level output of the screening partials: per-lane fp64 running total `tot` of entry

@@ -231,6 +231,48 @@ __device__ __forceinline__ void build_row_twiddles(float2* twr) {
     }
 }
 
+// ROW pass in two halves (row_fft = row_fft_a then row_fft_b): a = radix-R DFT + twiddles in
+// registers (no shared memory), b = the exchange through srow + the T-point DFTs.  Lets a caller
+// place a barrier between them (before its first write of the row buffer).
+template <int N, bool INV, bool TWR = false, typename TW = float2>
+__device__ __forceinline__ void row_fft_a(float2 (&x)[FFTCfg<N>::R], int t, const TW* tw, const TW* twr = nullptr) {
+    constexpr int R = FFTCfg<N>::R, T = FFTCfg<N>::T;
+    static_assert(T > 1, "row_fft_a needs T > 1");
+    DFT<R, INV>::run(x);
+#pragma unroll
+    for (int k1 = 1; k1 < R; ++k1) {
+        if constexpr (TWR)
+            x[k1] = twm<INV>(x[k1], twr, k1 * T + t);
+        else
+            x[k1] = twm<INV>(x[k1], tw, t * k1);
+    }
+}
+template <int N, bool INV>
+__device__ __forceinline__ void row_fft_b(float2 (&x)[FFTCfg<N>::R], float2* srow, int t) {
+    constexpr int R = FFTCfg<N>::R, T = FFTCfg<N>::T;
+#pragma unroll
+    for (int k1 = 0; k1 < R; ++k1) srow[T * k1 + (t ^ (k1 & (T - 1)))] = x[k1];
+    __syncwarp();
+    float2 y[R];
+#pragma unroll
+    for (int j = 0; j < R / T; ++j) {
+        const int k1 = j * T + t;
+#pragma unroll
+        for (int n2 = 0; n2 < T; ++n2) y[j * T + n2] = srow[T * k1 + (n2 ^ t)];
+    }
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < R / T; ++j) {
+        float2 b[T];
+#pragma unroll
+        for (int n2 = 0; n2 < T; ++n2) b[n2] = y[j * T + n2];
+        DFT<T, INV>::run(b);
+        const int k1 = j * T + t;
+#pragma unroll
+        for (int k2 = 0; k2 < T; ++k2) srow[k1 + R * k2] = b[k2];
+    }
+}
+
 // ROW pass for one row: x[n1] = input element at column T*n1 + t.  Leaves the row's DFT
 // (unnormalised) in srow[0..N) in natural order.  The T threads of the row must be
 // consecutive lanes of one warp and all 32 lanes must call this together.

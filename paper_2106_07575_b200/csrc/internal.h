@@ -12,8 +12,9 @@ constexpr int KMIN = 4;      // smallest adaptive pass-0 trial count
 constexpr int SMAX = 64;     // max trials per iteration (max_shrinks bound)
 constexpr int NDY = 7;       // DY partial sums per tile (+ Re<g, g_prev> for Polak-Ribiere)
 constexpr int LSP = KC + 4;  // screening partials: [S_0..S_{KC-1} | A, D, sum|a|, sum b]
-constexpr int LSW = LSP + 4; // reduced LS vector in DevState (eta^2 at LS_ETA)
-constexpr int LS_ETA = LSW - 1;
+constexpr int LSW = LSP + 4; // reduced LS vector in DevState: + ||eta||^2 and the object-grid moments
+constexpr int LS_ETA = LSP;  // ||eta||^2 over owned rows
+constexpr int LS_QA = LSP + 1, LS_QB = LSP + 2, LS_QC = LSP + 3;   // sum I 2Re(psi* eta), I|eta|^2, I|psi|^2
 
 // Device-resident scalar state of the iteration (all decisions are taken on the device).
 struct DevState {
@@ -25,6 +26,9 @@ struct DevState {
     double ls_hist[SMAX];    // DeltaF_k of every trial evaluated this iteration
     double ls_bnd[SMAX];     // error bound of ls_hist (0 = exact evaluation)
     double eta2;             // ||eta_m||^2 over owned rows (global after reduction)
+    // object-grid moments of this iteration's line (SolverCfg::qg): qa = sum_px a = sum_rho I 2 Re(psi* eta),
+    // qb = sum_px |v|^2 = sum_rho I |eta|^2, qc = sum_px |u|^2 = sum_rho I |psi|^2 (G^H G = diag I)
+    double qa, qb, qc;
     double F_init_part;      // scratch for k_fwd reductions
     int m;                   // iteration counter
     int accepted;            // 1 once a trial was accepted in this iteration
@@ -74,6 +78,10 @@ struct SolverCfg {
     double gamma0, tau, t, eps;
     int max_shrinks, direction, K;   // K = trials per extra pass and cap of the adaptive pass 0 (<= KC)
     int est;                         // PTYGER_EST_ML / PTYGER_EST_LS
+    // 1: the non-log part q_k = gamma_k a + gamma_k^2 b of the LS trial sums comes from the object grid
+    // (qa, qb of DevState; Parseval + G^H G = diag(I), exact for integer positions) instead of per frame
+    // pixel moments.  Set for the Poisson ML estimator with integer positions.
+    int qg;
 };
 
 // Trials [base, base + count) evaluated by LS pass p (host and device agree on this rule).
@@ -122,7 +130,12 @@ int launch_reduce(const double* part, int nblocks, int width, double* dst, cudaS
                   const DevState* st = nullptr, int mode = 0, int pass = 0, const P2PView* pv = nullptr,
                   const PickArgs* pick = nullptr);
 int launch_dir(DevState* st, const SolverCfg& c, cudaStream_t s);
-int launch_eta(const Geometry& g, const float2* gcur, float2* eta, const DevState* st,
+// illum = I(rho) = sum_j |p(rho - s_j)|^2 over this rank's frames (tile CSR, canonical order)
+int launch_illum(const Geometry& g, const float2* probe, const int* tile_ptr, const int* tile_frames, int ntx, int nty,
+                 float* illum, cudaStream_t s);
+// psi, illum non-null (SolverCfg::qg): also the object-grid moments qa, qb, qc (partials [eta2, qa, qb, qc])
+int launch_eta(const Geometry& g, const float2* gcur, float2* eta, const float2* psi, const float* illum,
+               const DevState* st,
                double* part, int grid, cudaStream_t s);
 int launch_pick(DevState* st, const SolverCfg& c, int pass, int exact_mode, int last_pass, cudaStream_t s);
 int launch_upd(const Geometry& g, float2* psi, const float2* eta, const DevState* st, int grid,

@@ -32,7 +32,7 @@ constexpr int SLD = N + 8;                  // row-scratch stride (complex)
 constexpr size_t BLK_BYTES = (size_t)N * QC * 8;           // 131072
 constexpr size_t SCR_OFF = BLK_BYTES;
 constexpr size_t TW_OFF = SCR_OFF + (size_t)SROWS * SLD * 8; // + 67584
-constexpr size_t DYN_BYTES = TW_OFF + (size_t)N * 8 + (size_t)R * T * 8;   // + row-pass table twr [k1][t]
+constexpr size_t DYN_BYTES = TW_OFF + (size_t)(N + R * T) * 16;   // float4 tw[N] + row-pass table twr [k1][t]
 }  // namespace c256
 
 __device__ __forceinline__ uint32_t c4_mapa(uint32_t saddr, uint32_t rank) {
@@ -70,8 +70,8 @@ __device__ __forceinline__ void c4_wait() { asm volatile("barrier.cluster.wait.a
 // Row pass of one row (16 sub-threads t of one row, consecutive lanes): x[n1] = input at column
 // 16 n1 + t.  After the transform x[k2] is output column t + 16 k2, owned by CTA k2 / 4 at local
 // column t + 16 (k2 % 4).  `first` (round 0): wait until every peer has released its block.
-template <bool INV>
-__device__ __forceinline__ void c4_row(float2 (&x)[16], float2* srow, int t, const float2* tw, int row,
+template <bool INV, typename TW>
+__device__ __forceinline__ void c4_row(float2 (&x)[16], float2* srow, int t, const TW* tw, int row,
                                        const uint32_t (&cb)[4], bool first) {
     using namespace c256;
     row_fft_regs<N, INV, true>(x, srow, t, tw, tw + N);   // twr [k1][t] follows tw
@@ -82,15 +82,15 @@ __device__ __forceinline__ void c4_row(float2 (&x)[16], float2* srow, int t, con
 }
 
 // Column pass on the local 256 x 64 block: phase 1 for local column cl, sub-thread t (= warp).
-template <bool INV>
-__device__ __forceinline__ void c4_col1(float2* blk, int cl, int t, const float2* tw) {
+template <bool INV, typename TW>
+__device__ __forceinline__ void c4_col1(float2* blk, int cl, int t, const TW* tw) {
     using namespace c256;
     float2 x[R];
 #pragma unroll
     for (int n1 = 0; n1 < R; ++n1) x[n1] = blk[(T * n1 + t) * QC + cl];
     DFT<R, INV>::run(x);
 #pragma unroll
-    for (int k1 = 1; k1 < R; ++k1) x[k1] = twmul<INV>(x[k1], tw[t * k1]);
+    for (int k1 = 1; k1 < R; ++k1) x[k1] = twm<INV>(x[k1], tw, t * k1);
 #pragma unroll
     for (int k1 = 0; k1 < R; ++k1) blk[(T * k1 + t) * QC + cl] = x[k1];
 }
@@ -116,11 +116,14 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(512, 1)
     extern __shared__ __align__(16) unsigned char smraw[];
     float2* blk = reinterpret_cast<float2*>(smraw);
     float2* scr = reinterpret_cast<float2*>(smraw + SCR_OFF);
-    float2* tw = reinterpret_cast<float2*>(smraw + TW_OFF);
+    float4* tw = reinterpret_cast<float4*>(smraw + TW_OFF);
+    // the d > 0 queues of the epilogue live in the row-pass scratch (free between the cluster
+    // barrier after the row pass and the next frame's row pass)
+    LsWarpQ<4>* wq = reinterpret_cast<LsWarpQ<4>*>(scr);
+    static_assert(sizeof(LsWarpQ<4>) * NW <= (size_t)SROWS * SLD * 8, "queues exceed the row scratch");
     __shared__ double sred[NW][KC];
     __shared__ double smom[NW][4];
     __shared__ float sgam[KC];
-    __shared__ LsWarpQ<1> wq[NW];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t rank = c4_rank();
     const int64_t cid = c4_id(), ncl = c4_count();
@@ -128,8 +131,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(512, 1)
     int base, cnt;
     ls_pass_range(0, st->keff, cfg, base, cnt);
     ktime_start(st, 1);
-    build_twiddles<N>(tw);
-    build_row_twiddles<N>(tw + N);
+    build_twiddles4<N, false>(tw);
     if (tid < KC) sgam[tid] = (float)trial_gamma(cfg.gamma0, cfg.tau, base + tid);
     uint32_t cb[4];
     {
@@ -180,7 +182,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(512, 1)
             const float2* __restrict__ ub = u + fb;
             const float* __restrict__ db = d + fb;
             float2* __restrict__ vb = v + fb;
-            if (cnt > 0) trial_dispatch(cnt, cfg.est, [&]<int KT, bool LSE>() {
+            if (cnt > 0) trial_dispatch(cnt, cfg, [&]<int KT, bool LSE, bool QG>() {
                 float gk[KT];
 #pragma unroll
                 for (int k = 0; k < KT; ++k) gk[k] = sgam[k];
@@ -211,16 +213,15 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(512, 1)
                             dn[e] = ld1_hint_na(db + gn + e * R * N, pol);
                         }
                     }
+                    float2 vv[4];
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
-                        float2 vv[1] = {mine[(gi * 4 + e) * QC]};
-                        float2 uu[1] = {uc[e]};
-                        float dd[1] = {dc[e]};
-                        st2_hint(vb + go + e * R * N, vv[0], pol);
-                        ls_push<KT, LSE>(wq[warp], qs, uu, vv, dd, gk, eps2, S, m, lane);
+                        vv[e] = mine[(gi * 4 + e) * QC];
+                        st2_hint(vb + go + e * R * N, vv[e], pol);
                     }
+                    ls_push<KT, LSE, QG>(wq[warp], qs, uc, vv, dc, gk, eps2, S, m, lane);
                 }
-                ls_flush<KT, LSE>(wq[warp], qs, gk, eps2, S, m, lane);
+                ls_flush<KT, LSE, QG>(wq[warp], qs, gk, eps2, S, m, lane);
             });
             ls_run_out<KC>(S, m, tot, mom, lane);
         }

@@ -305,7 +305,7 @@ __global__ void __launch_bounds__(512, 1) k_ls(Geometry g, const float2* __restr
             const float2* __restrict__ ub = u + fb;
             const float* __restrict__ db = d + fb;
             float2* __restrict__ vb = v + fb;
-            if (cnt > 0) trial_dispatch(cnt, cfg.est, [&]<int KT, bool LSE>() {
+            if (cnt > 0) trial_dispatch(cnt, cfg, [&]<int KT, bool LSE, bool QG>() {
                 float gk[KT];   // trial gammas in registers for the whole run
 #pragma unroll
                 for (int k = 0; k < KT; ++k) gk[k] = sgam[k];
@@ -348,9 +348,9 @@ __global__ void __launch_bounds__(512, 1) k_ls(Geometry g, const float2* __restr
                             if (valid) vb[go + e * R * N] = vc[e];
                             else vc[e] = make_float2(0.f, 0.f);
                         }
-                        ls_push<KT, LSE>(wq[warp], qs, slice<0, 2>(uc), slice<0, 2>(vc), slice<0, 2>(dc), gk, eps2,
+                        ls_push<KT, LSE, QG>(wq[warp], qs, slice<0, 2>(uc), slice<0, 2>(vc), slice<0, 2>(dc), gk, eps2,
                                          S, m, lane);
-                        ls_push<KT, LSE>(wq[warp], qs, slice<2, 2>(uc), slice<2, 2>(vc), slice<2, 2>(dc), gk, eps2,
+                        ls_push<KT, LSE, QG>(wq[warp], qs, slice<2, 2>(uc), slice<2, 2>(vc), slice<2, 2>(dc), gk, eps2,
                                          S, m, lane);
                     }
                 } else {
@@ -367,10 +367,10 @@ __global__ void __launch_bounds__(512, 1) k_ls(Geometry g, const float2* __restr
                         } else {
                             vv[0] = make_float2(0.f, 0.f);
                         }
-                        ls_push<KT, LSE>(wq[warp], qs, uu, vv, dd, gk, eps2, S, m, lane);
+                        ls_push<KT, LSE, QG>(wq[warp], qs, uu, vv, dd, gk, eps2, S, m, lane);
                     }
                 }
-                ls_flush<KT, LSE>(wq[warp], qs, gk, eps2, S, m, lane);
+                ls_flush<KT, LSE, QG>(wq[warp], qs, gk, eps2, S, m, lane);
             });
             ls_run_out<KC>(S, m, tot, mom, lane);
         }

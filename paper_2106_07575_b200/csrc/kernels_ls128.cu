@@ -96,6 +96,7 @@ __global__ void __launch_bounds__(512, 1) k_ls_ws(Geometry g, const float2* __re
     __shared__ LsWarpQ<2> wq[8];
     __shared__ uint32_t s_tmem;
     __shared__ __align__(8) uint64_t s_mbar[2];   // [0] staged rows 0..63, [1] rows 64..127 in sf
+    __shared__ int s_done[2];                      // FFT warps done reading [0] the staging, [1] the frame buffer
     float2* stg = reinterpret_cast<float2*>(smraw + STG_OFF);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const bool err = st->numeric_error != 0;
@@ -113,6 +114,7 @@ __global__ void __launch_bounds__(512, 1) k_ls_ws(Geometry g, const float2* __re
         mbar_init(&s_mbar[0], 1);
         mbar_init(&s_mbar[1], 1);
         fence_mbar_init();
+        s_done[0] = s_done[1] = 0;
     }
     tc_fence_before();
     __syncthreads();
@@ -145,6 +147,25 @@ __global__ void __launch_bounds__(512, 1) k_ls_ws(Geometry g, const float2* __re
         for (int q = 0; q < SROWS / 32; ++q) {
             const int r = q * 32 + lane;
             bulk_g2s(dst + r * ld, src + (int64_t)r * W, bytes, &s_mbar[h]);
+        }
+    };
+    // An FFT warp is done reading buffer h (0 staging, 1 frame buffer) of this frame: the LAST of the 8
+    // to get there issues the next frame's copy into it, so no warp waits for the others.  Generic reads
+    // -> release / acquire on the counter -> proxy fence -> async-proxy writes.
+    auto done_reading = [&](int64_t i, int h) {
+        __syncwarp();
+        int last = 0;
+        if (lane == 0) {
+            fence_proxy_async();
+            const int old = atomicAdd_block(&s_done[h], 1);
+            __threadfence_block();
+            last = old == NF / 32 - 1;
+            if (last) s_done[h] = 0;   // re-armed before any warp can reach this point again (bar B2)
+        }
+        last = __shfl_sync(FULLMASK, last, 0);
+        if (last) {
+            fence_proxy_async();
+            if (i + gridDim.x < nfr) issue_dma(i + gridDim.x, h);
         }
     };
 
@@ -181,15 +202,16 @@ __global__ void __launch_bounds__(512, 1) k_ls_ws(Geometry g, const float2* __re
                 float2 xa[R], xb[R];
                 load_row(rp, xa);
                 load_row(rp + 1, xb);
+                // the staged rows are consumed: the next frame's first half may land there
+                if (DMA && rp == 0) done_reading(i, 0);
+                row_fft_a<N, false, true>(xa, t, tw, tw + N);
+                row_fft_a<N, false, true>(xb, t, tw, tw + N);
+                // every FFT warp has finished the previous frame's column pass (its reads of the frame
+                // buffer) before this frame's first row writes land in it
+                if (rp == 0) bar_sync_n(BAR_FFT, NF);
                 __syncwarp();   // every lane of the warp has read its rows before any exchange write
-                row_fft<N, false, true>(xa, sf + (rp * RROWS + rrow) * LD, t, tw, tw + N);
-                row_fft<N, false, true>(xb, sf + ((rp + 1) * RROWS + rrow) * LD, t, tw, tw + N);
-                if (DMA && rp == 0) {
-                    // the staged rows are consumed: the next frame's first half may land there
-                    fence_proxy_async();
-                    bar_sync_n(BAR_FFT, NF);
-                    if (warp == 0 && i + gridDim.x < nfr) issue_dma(i + gridDim.x, 0);
-                }
+                row_fft_b<N, false>(xa, sf + (rp * RROWS + rrow) * LD, t);
+                row_fft_b<N, false>(xb, sf + ((rp + 1) * RROWS + rrow) * LD, t);
             }
             bar_sync_n(BAR_FFT, NF);
             // ---- column pass phase 1: 4 rounds of 32 columns, sub-thread t = warp
@@ -211,14 +233,9 @@ __global__ void __launch_bounds__(512, 1) k_ls_ws(Geometry g, const float2* __re
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             tc_fence_before();
             bar_arrive_n(BAR_FULL + b, NT);
-            // ---- the frame buffer is free: the next frame's second window half may land in it
-            if (DMA) {
-                fence_proxy_async();
-                bar_sync_n(BAR_FFT, NF);
-                if (warp == 0 && i + gridDim.x < nfr) issue_dma(i + gridDim.x, 1);
-            } else {
-                bar_sync_n(BAR_FFT, NF);
-            }
+            // ---- this warp's reads of the frame buffer are done: the next frame's second window half
+            // may land in it once all eight are (the barrier before the next row writes orders the rest)
+            if (DMA) done_reading(i, 1);
         }
     } else {
         // ============================ epilogue group ============================
@@ -226,7 +243,7 @@ __global__ void __launch_bounds__(512, 1) k_ls_ws(Geometry g, const float2* __re
         const float eps2 = (float)(cfg.eps * cfg.eps);
         int nmine = 0;
         for (int64_t i = blockIdx.x; i < nfr; i += gridDim.x) ++nmine;
-        trial_dispatch(cnt, cfg.est, [&]<int KT, bool LSE>() {
+        trial_dispatch(cnt, cfg, [&]<int KT, bool LSE, bool QG>() {
             float gk[KT];   // trial gammas in registers for the whole run
 #pragma unroll
             for (int k = 0; k < KT; ++k) gk[k] = sgam[k];
@@ -284,12 +301,12 @@ __global__ void __launch_bounds__(512, 1) k_ls_ws(Geometry g, const float2* __re
                         tmem_ld8(tq + (uint32_t)(256 * b + 32 * rd + 8 * gi), X);
 #pragma unroll
                         for (int e = 0; e < 4; ++e) vb[go + e * R * N] = X[e];
-                        ls_push<KT, LSE>(wq[ew], qs, slice<0, 2>(uc), slice<0, 2>(X), slice<0, 2>(dc), gk, eps2, S,
+                        ls_push<KT, LSE, QG>(wq[ew], qs, slice<0, 2>(uc), slice<0, 2>(X), slice<0, 2>(dc), gk, eps2, S,
                                          m, lane);
-                        ls_push<KT, LSE>(wq[ew], qs, slice<2, 2>(uc), slice<2, 2>(X), slice<2, 2>(dc), gk, eps2, S,
+                        ls_push<KT, LSE, QG>(wq[ew], qs, slice<2, 2>(uc), slice<2, 2>(X), slice<2, 2>(dc), gk, eps2, S,
                                          m, lane);
                     }
-                    ls_flush<KT, LSE>(wq[ew], qs, gk, eps2, S, m, lane);
+                    ls_flush<KT, LSE, QG>(wq[ew], qs, gk, eps2, S, m, lane);
                     ls_run_out<KC>(S, m, tot, mom, lane);
                 }
                 // slot b read: the FFT group may overwrite it (frame it + 2) -- no arrival without a waiter

@@ -164,6 +164,41 @@ __global__ void __launch_bounds__(256) k_adj(Geometry g, const float2* __restric
     }
 }
 
+// Illumination I(rho) = sum_j |p(rho - s_j)|^2 over the frames covering rho (the diagonal of G^H G,
+// integer positions), same tiles / frame lists / order as k_adj: once at init, for the object-grid
+// moments of the line search (SolverCfg::qg).
+__global__ void __launch_bounds__(256) k_illum(Geometry g, const float2* __restrict__ probe,
+                                               const int4* __restrict__ ent, const int* __restrict__ tile_ptr,
+                                               int ntx, float* __restrict__ illum) {
+    const int tile = blockIdx.x;
+    const int tx = tile % ntx, ty = tile / ntx;
+    const int lane = threadIdx.x & 31, wy = threadIdx.x >> 5;
+    const int64_t col = (int64_t)tx * 32 + lane;
+    const int64_t row0 = (int64_t)ty * 32 + wy;
+    const int N = g.N;
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int e = tile_ptr[tile]; e < tile_ptr[tile + 1]; ++e) {
+        const int4 en = __ldg(ent + e);
+        const int dc = (int)(col - en.z);
+        if ((unsigned)dc >= (unsigned)N) continue;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int dr = (int)(row0 + 8 * i - en.y);
+            if ((unsigned)dr < (unsigned)N) {
+                const float2 pv = ldg2(probe + dr * N + dc);
+                acc[i] = fmaf(pv.x, pv.x, fmaf(pv.y, pv.y, acc[i]));
+            }
+        }
+    }
+    if (col < g.W) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int64_t r = row0 + 8 * i;
+            if (r < g.SH) illum[r * g.W + col] = acc[i];
+        }
+    }
+}
+
 // After the NCCL band exchange: g[band] += neighbour's partial; DY partials on band rows.
 __global__ void __launch_bounds__(256) k_band_add(float2* __restrict__ gcur, const float2* __restrict__ recv,
                                                   int64_t row_lo, int64_t rows, int64_t W,
@@ -371,8 +406,12 @@ __device__ void dir_body(DevState* st, const SolverCfg& c) {
 
 __global__ void k_dir(DevState* st, SolverCfg c) { dir_body(st, c); }
 
-// eta = -g + alpha eta (Eq.6) over the storage rows; ||eta||^2 over owned rows.
+// eta = -g + alpha eta (Eq.6) over the storage rows; ||eta||^2 over owned rows.  With the object-grid
+// moments (psi, illum set): also qa = sum I 2 Re(psi* eta), qb = sum I |eta|^2, qc = sum I |psi|^2 over the
+// storage rows (I counts this rank's frames only, so the sum over ranks counts every frame once), in
+// fp64 per element.  Partials per CTA: [eta^2, qa, qb, qc].
 __global__ void __launch_bounds__(256) k_eta(Geometry g, const float2* __restrict__ gcur, float2* __restrict__ eta,
+                                             const float2* __restrict__ psi, const float* __restrict__ illum,
                                              const DevState* __restrict__ st, double* __restrict__ part) {
     __shared__ double sred[8];
     const float2 al = make_float2((float)st->alpha_re, (float)st->alpha_im);
@@ -380,6 +419,7 @@ __global__ void __launch_bounds__(256) k_eta(Geometry g, const float2* __restric
     const int64_t total = g.SH * g.W;
     const int64_t lo = g.own_lo * g.W, hi = g.own_hi * g.W;
     float s = 0.f;
+    double qa = 0.0, qb = 0.0, qc = 0.0;
     if (!err) {
         for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
             const float2 gv = gcur[i];
@@ -387,12 +427,24 @@ __global__ void __launch_bounds__(256) k_eta(Geometry g, const float2* __restric
             const float2 ne = csub(cmul(al, ev), gv);
             eta[i] = ne;
             if (i >= lo && i < hi) s += ne.x * ne.x + ne.y * ne.y;
+            if (psi) {
+                const float2 pv = psi[i];
+                const float w = __ldg(illum + i);
+                qa += (double)(w * fmaf(pv.x, ne.x, pv.y * ne.y));
+                qb += (double)(w * fmaf(ne.x, ne.x, ne.y * ne.y));
+                qc += (double)(w * fmaf(pv.x, pv.x, pv.y * pv.y));
+            }
         }
     }
     const double t = block_sum<256>((double)s, sred);
-    if (threadIdx.x == 0) part[blockIdx.x] = t;
+    if (threadIdx.x == 0) part[(int64_t)blockIdx.x * 4] = t;
+    const double a = block_sum<256>(qa, sred);
+    if (threadIdx.x == 0) part[(int64_t)blockIdx.x * 4 + 1] = 2.0 * a;
+    const double b = block_sum<256>(qb, sred);
+    if (threadIdx.x == 0) part[(int64_t)blockIdx.x * 4 + 2] = b;
+    const double c = block_sum<256>(qc, sred);
+    if (threadIdx.x == 0) part[(int64_t)blockIdx.x * 4 + 3] = c;
 }
-
 
 // Further LS passes over the cached (u, v, d): trials [base, base + count) of pass `pass`
 // (ls_pass_range).  SCREEN mode runs unless an earlier pass accepted; EXACT mode runs only when
@@ -427,12 +479,12 @@ __global__ void __launch_bounds__(256) k_lsx(int64_t count, const float2* __rest
             LsMom m;
 #pragma unroll
             for (int k = 0; k < KC; ++k) S[k] = 0.f;
-            trial_dispatch(cnt, cfg.est, [&]<int KT, bool LSE>() {
+            trial_dispatch(cnt, cfg, [&]<int KT, bool LSE, bool QG>() {
                 if constexpr (EXACT) {
 #pragma unroll 4
                     for (int i = 0; i < RUN; ++i) {
                         const int64_t o = e0 + (int64_t)i * blockDim.x + tid;
-                        if (o < count) ls_exact<KT, LSE>(u[o], v[o], __ldg(d + o), sgam, eps2, S);
+                        if (o < count) ls_exact<KT, LSE, QG>(u[o], v[o], __ldg(d + o), sgam, eps2, S);
                     }
                 } else {
                     // warp-collective d > 0 compaction: out-of-range lanes push zeros
@@ -449,9 +501,9 @@ __global__ void __launch_bounds__(256) k_lsx(int64_t count, const float2* __rest
                             vv[e] = ok ? v[o] : make_float2(0.f, 0.f);
                             dd[e] = ok ? __ldg(d + o) : 0.f;
                         }
-                        ls_push<KT, LSE>(wq[tid >> 5], qs, uu, vv, dd, sgam, eps2, S, m, lane);
+                        ls_push<KT, LSE, QG>(wq[tid >> 5], qs, uu, vv, dd, sgam, eps2, S, m, lane);
                     }
-                    ls_flush<KT, LSE>(wq[tid >> 5], qs, sgam, eps2, S, m, lane);
+                    ls_flush<KT, LSE, QG>(wq[tid >> 5], qs, sgam, eps2, S, m, lane);
                 }
             });
             if constexpr (EXACT) {
@@ -476,7 +528,16 @@ __global__ void __launch_bounds__(256) k_lsx(int64_t count, const float2* __rest
 // gamma = 0, stalled (R#9).  The last pass writes the trace and sets the next iteration's
 // adaptive pass-0 trial count keff = clamp(k* + 3, KMIN, K) (K after a stall).
 __device__ void pick_body(DevState* st, const SolverCfg& c, int pass, int exact_mode, int last_pass) {
-    if (pass == 0 && !exact_mode) st->eta2 = st->ls_pass[LS_ETA];
+    if (pass == 0 && !exact_mode) {
+        st->eta2 = st->ls_pass[LS_ETA];
+        st->qa = st->ls_pass[LS_QA];
+        st->qb = st->ls_pass[LS_QB];
+        st->qc = st->ls_pass[LS_QC];
+    }
+    // SolverCfg::qg: the frame passes summed only the log parts; the non-log part of DeltaF_k is
+    // gamma_k qa + gamma_k^2 qb from the object grid (identical in the screening and the exact pass,
+    // so it adds nothing to the screening bound)
+    auto qpart = [&](double gk) { return c.qg ? gk * fma(gk, st->qb, st->qa) : 0.0; };
     int base, cnt;
     ls_pass_range(pass, st->keff, c, base, cnt);
     if (c.direction == PTYGER_DIR_GD && !st->numeric_error && pass == 0) {
@@ -484,7 +545,7 @@ __device__ void pick_body(DevState* st, const SolverCfg& c, int pass, int exact_
         // is always updated from the EXACT evaluation of DeltaF_0 (guarded definition R#4), never
         // from the screened value, which may be non-finite where |u| < eps.
         if (!exact_mode) {
-            st->ls_hist[0] = st->ls_pass[0];
+            st->ls_hist[0] = st->ls_pass[0] + qpart(c.gamma0);
             st->ls_bnd[0] = LS_EPS_D * st->ls_pass[KC + 1] +
                             LS_EPS_R * (st->ls_pass[KC] + c.gamma0 * st->ls_pass[KC + 2] +
                                         c.gamma0 * c.gamma0 * st->ls_pass[KC + 3]);
@@ -496,7 +557,7 @@ __device__ void pick_body(DevState* st, const SolverCfg& c, int pass, int exact_
             st->need_exact = 1;
             st->k_unc = 0;
         } else if (st->need_exact == 1) {
-            const double dF = st->ls_pass[0];
+            const double dF = st->ls_pass[0] + qpart(c.gamma0);
             st->ls_hist[0] = dF;
             st->ls_bnd[0] = 0.0;
             st->n_exact += 1;
@@ -519,7 +580,7 @@ __device__ void pick_body(DevState* st, const SolverCfg& c, int pass, int exact_
             for (int k = 0; k < cnt; ++k) {
                 const int kk = base + k;
                 const double gk = trial_gamma(c.gamma0, c.tau, kk);
-                const double S = st->ls_pass[k];
+                const double S = st->ls_pass[k] + qpart(gk);
                 const double B = LS_EPS_D * D + LS_EPS_R * (A + gk * sa + gk * gk * sb);
                 st->ls_hist[kk] = S;
                 st->ls_bnd[kk] = B;
@@ -539,8 +600,8 @@ __device__ void pick_body(DevState* st, const SolverCfg& c, int pass, int exact_
             }
         } else if (st->need_exact == pass + 1) {
             for (int kk = st->k_unc; kk < base + cnt; ++kk) {
-                const double dF = st->ls_pass[kk - base];
                 const double gk = trial_gamma(c.gamma0, c.tau, kk);
+                const double dF = st->ls_pass[kk - base] + qpart(gk);
                 st->ls_hist[kk] = dF;
                 st->ls_bnd[kk] = 0.0;
                 st->n_eval = kk + 1;
@@ -717,9 +778,15 @@ int launch_dir(DevState* st, const SolverCfg& c, cudaStream_t s) {
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
-int launch_eta(const Geometry& g, const float2* gcur, float2* eta, const DevState* st, double* part,
-               int grid, cudaStream_t s) {
-    k_eta<<<grid, 256, 0, s>>>(g, gcur, eta, st, part);
+int launch_eta(const Geometry& g, const float2* gcur, float2* eta, const float2* psi, const float* illum,
+               const DevState* st, double* part, int grid, cudaStream_t s) {
+    k_eta<<<grid, 256, 0, s>>>(g, gcur, eta, psi, illum, st, part);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+int launch_illum(const Geometry& g, const float2* probe, const int* tile_ptr, const int* tile_frames, int ntx, int nty,
+                 float* illum, cudaStream_t s) {
+    k_illum<<<ntx * nty, 256, 0, s>>>(g, probe, reinterpret_cast<const int4*>(tile_frames), tile_ptr, ntx, illum);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
