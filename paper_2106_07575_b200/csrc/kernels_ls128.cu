@@ -28,6 +28,7 @@
 // so k_reduce / k_pick consume them unchanged.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "dev.cuh"
 #include "tma.cuh"
@@ -149,6 +150,22 @@ __global__ void __launch_bounds__(512, 1) k_ls_ws(Geometry g, const float2* __re
             bulk_g2s(dst + r * ld, src + (int64_t)r * W, bytes, &s_mbar[h]);
         }
     };
+    // Staged half (h = 0) of the next frame, per warp: the 8 rows this warp reads in rounds 0 and 1 (a
+    // row's 8 sub-threads sit in one warp), so no other warp's reads are overwritten and no counter is
+    // needed; warp 0 posts the transaction count of all 64 rows (the phase cannot complete before it).
+    auto issue_own_staged = [&](int64_t inext) {
+        const int jn = order[inext];
+        const int2 sn = pos[jn];
+        const int off = sn.y & 1;
+        const uint32_t bytes = (uint32_t)(N + 2 * off) * 8u;
+        __syncwarp();
+        if (warp == 0 && lane == 0) mbar_arrive_expect_tx(&s_mbar[0], bytes * SROWS);
+        if (lane < 8) {
+            fence_proxy_async();
+            const int r = (lane < 4 ? 0 : RROWS) + 4 * warp + (lane & 3);
+            bulk_g2s(stg + r * SLD, eta + (int64_t)(sn.x + r) * W + (sn.y - off), bytes, &s_mbar[0]);
+        }
+    };
     // An FFT warp is done reading buffer h (0 staging, 1 frame buffer) of this frame: the LAST of the 8
     // to get there issues the next frame's copy into it, so no warp waits for the others.  Generic reads
     // -> release / acquire on the counter -> proxy fence -> async-proxy writes.
@@ -202,8 +219,9 @@ __global__ void __launch_bounds__(512, 1) k_ls_ws(Geometry g, const float2* __re
                 float2 xa[R], xb[R];
                 load_row(rp, xa);
                 load_row(rp + 1, xb);
-                // the staged rows are consumed: the next frame's first half may land there
-                if (DMA && rp == 0) done_reading(i, 0);
+                // this warp's staged rows (4w..4w+3, 32+4w..32+4w+3: exactly the rows it read) are
+                // consumed: the next frame's copies of them are issued right away by the warp itself
+                if (DMA && rp == 0 && i + gridDim.x < nfr) issue_own_staged(i + gridDim.x);
                 row_fft_a<N, false, true>(xa, t, tw, tw + N);
                 row_fft_a<N, false, true>(xb, t, tw, tw + N);
                 // every FFT warp has finished the previous frame's column pass (its reads of the frame
