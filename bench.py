@@ -553,8 +553,8 @@ def main():
         if total * world >= 170e9:
             try:
                 lf, (lpsi, lp, lscan, ld_head) = time_frames(args, wl, world, rank, local, dev, coll_dev,
-                                                             args.large_steps, 2, False)
-                large = {"config": frames_config(wl, args, world), "steps": args.large_steps, "warmup": 2,
+                                                             args.large_steps, 3, False)
+                large = {"config": frames_config(wl, args, world), "steps": args.large_steps, "warmup": 3,
                          "metric": METRIC, "unit": UNIT,
                          **{k: v for k, v in lf.items() if k not in ("e2e", "host_wall_s")}}
                 large["lower_bound"] = lower_bound(wl.N, wl.n, wl.H, wl.W, lf["ms_per_step"], peaks()[0],

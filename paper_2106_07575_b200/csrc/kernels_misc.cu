@@ -420,20 +420,41 @@ __global__ void __launch_bounds__(256) k_eta(Geometry g, const float2* __restric
     const int64_t lo = g.own_lo * g.W, hi = g.own_hi * g.W;
     float s = 0.f;
     double qa = 0.0, qb = 0.0, qc = 0.0;
+    auto elem = [&](int64_t i, float2 gv, float2 ev, float2& ne) {
+        ne = csub(cmul(al, ev), gv);
+        if (i >= lo && i < hi) s += ne.x * ne.x + ne.y * ne.y;
+    };
+    auto moments = [&](float2 ne, float2 pv, float w) {
+        qa += (double)(w * fmaf(pv.x, ne.x, pv.y * ne.y));
+        qb += (double)(w * fmaf(ne.x, ne.x, ne.y * ne.y));
+        qc += (double)(w * fmaf(pv.x, pv.x, pv.y * pv.y));
+    };
     if (!err) {
-        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-            const float2 gv = gcur[i];
-            const float2 ev = eta[i];
-            const float2 ne = csub(cmul(al, ev), gv);
-            eta[i] = ne;
-            if (i >= lo && i < hi) s += ne.x * ne.x + ne.y * ne.y;
+        // two elements per thread and step (16-B accesses); total is even (W even) or the tail is scalar
+        const int64_t npair = total / 2;
+        const float4* g4 = reinterpret_cast<const float4*>(gcur);
+        float4* e4 = reinterpret_cast<float4*>(eta);
+        const float4* p4 = reinterpret_cast<const float4*>(psi);
+        const float2* i2 = reinterpret_cast<const float2*>(illum);
+        for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < npair; k += (int64_t)gridDim.x * blockDim.x) {
+            const float4 gv = g4[k], ev = e4[k];
+            float2 n0, n1;
+            elem(2 * k, make_float2(gv.x, gv.y), make_float2(ev.x, ev.y), n0);
+            elem(2 * k + 1, make_float2(gv.z, gv.w), make_float2(ev.z, ev.w), n1);
+            e4[k] = make_float4(n0.x, n0.y, n1.x, n1.y);
             if (psi) {
-                const float2 pv = psi[i];
-                const float w = __ldg(illum + i);
-                qa += (double)(w * fmaf(pv.x, ne.x, pv.y * ne.y));
-                qb += (double)(w * fmaf(ne.x, ne.x, ne.y * ne.y));
-                qc += (double)(w * fmaf(pv.x, pv.x, pv.y * pv.y));
+                const float4 pv = p4[k];
+                const float2 w = __ldg(i2 + k);
+                moments(n0, make_float2(pv.x, pv.y), w.x);
+                moments(n1, make_float2(pv.z, pv.w), w.y);
             }
+        }
+        if ((total & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+            const int64_t i = total - 1;
+            float2 n0;
+            elem(i, gcur[i], eta[i], n0);
+            eta[i] = n0;
+            if (psi) moments(n0, psi[i], illum[i]);
         }
     }
     const double t = block_sum<256>((double)s, sred);
@@ -458,7 +479,7 @@ __global__ void __launch_bounds__(256) k_lsx(int64_t count, const float2* __rest
     __shared__ double sred[8][KC];
     __shared__ double smom[8][4];
     __shared__ float sgam[KC];
-    __shared__ LsWarpQ<2> wq[EXACT ? 1 : 8];
+    __shared__ LsWarpQ<4> wq[EXACT ? 1 : 8];
     const int tid = threadIdx.x, lane = tid & 31;
     int base, cnt;
     ls_pass_range(pass, st->keff, cfg, base, cnt);
@@ -487,21 +508,26 @@ __global__ void __launch_bounds__(256) k_lsx(int64_t count, const float2* __rest
                         if (o < count) ls_exact<KT, LSE, QG>(u[o], v[o], __ldg(d + o), sgam, eps2, S);
                     }
                 } else {
-                    // warp-collective d > 0 compaction: out-of-range lanes push zeros
+                    // warp-collective d > 0 compaction: out-of-range lanes push zeros.  Eight pixels'
+                    // u, v, d per thread are loaded before any is used (a streaming pass: memory-level
+                    // parallelism, not arithmetic, sets its speed)
                     LsQState qs;
-#pragma unroll 2
-                    for (int i = 0; i < RUN; i += 2) {
-                        float2 uu[2], vv[2];
-                        float dd[2];
+#pragma unroll 1
+                    for (int i = 0; i < RUN; i += 8) {
+                        float2 uu[8], vv[8];
+                        float dd[8];
 #pragma unroll
-                        for (int e = 0; e < 2; ++e) {
+                        for (int e = 0; e < 8; ++e) {
                             const int64_t o = e0 + (int64_t)(i + e) * blockDim.x + tid;
                             const bool ok = o < count;
-                            uu[e] = ok ? u[o] : make_float2(0.f, 0.f);
-                            vv[e] = ok ? v[o] : make_float2(0.f, 0.f);
-                            dd[e] = ok ? __ldg(d + o) : 0.f;
+                            uu[e] = ok ? ldg2_na(u + o) : make_float2(0.f, 0.f);
+                            vv[e] = ok ? ldg2_na(v + o) : make_float2(0.f, 0.f);
+                            dd[e] = ok ? ldg1_na(d + o) : 0.f;
                         }
-                        ls_push<KT, LSE, QG>(wq[tid >> 5], qs, uu, vv, dd, sgam, eps2, S, m, lane);
+                        ls_push<KT, LSE, QG>(wq[tid >> 5], qs, slice<0, 4>(uu), slice<0, 4>(vv), slice<0, 4>(dd), sgam,
+                                             eps2, S, m, lane);
+                        ls_push<KT, LSE, QG>(wq[tid >> 5], qs, slice<4, 4>(uu), slice<4, 4>(vv), slice<4, 4>(dd), sgam,
+                                             eps2, S, m, lane);
                     }
                     ls_flush<KT, LSE, QG>(wq[tid >> 5], qs, sgam, eps2, S, m, lane);
                 }

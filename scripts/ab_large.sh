@@ -1,16 +1,12 @@
 #!/bin/bash
-# A/B of library variants / env toggles on the large config: bash scripts/ab_large.sh TAG "ENV=.." ...
+# gpurun: large-view A/B over env settings (each argument: VAR=val ...), 5 timed iterations after 3 warm-up.
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
 mkdir -p gpurun_out
-TAG=$1; shift
-i=0
-for e in "$@"; do
-  env $e timeout 600 python bench.py --config ${CONFIG:-large} --steps 10 --warmup 3 --no-cpu-baseline --e2e-steps 0 > gpurun_out/abl_${TAG}_$i.log 2>&1
-  python - "gpurun_out/abl_${TAG}_$i.log" "$e" <<'PY'
-import json,sys
-for l in open(sys.argv[1]):
-    if l.startswith("{"):
-        d=json.loads(l); print(sys.argv[2],"value %.4g"%d["value"],"ms %.3f"%d["ms_per_step"],{k:round(v,3) for k,v in d["stage_ms"].items()},"shrinks",d.get("mean_shrinks"))
-PY
-  i=$((i+1))
+python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
+for SET in "$@"; do
+  echo -n "$SET: "
+  env $SET timeout 900 python bench.py --config large --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 0 2>>gpurun_out/ab_large.err | python -c "
+import sys, json
+d = json.loads([l for l in sys.stdin.read().splitlines() if l.startswith('{')][-1]); r = d['roofline']
+print('ms %.2f k_ls %.2f k_grad %.2f iter_frac %.3f stage %s passes %s' % (d['ms_per_step'], r['k_ls_avg_ms'], r['k_grad_avg_ms'], d['iteration_roofline']['frac'], {k: round(v, 2) for k, v in d['stage_ms'].items()}, d.get('ls_passes')))"
 done
