@@ -323,3 +323,34 @@ def test_cg_converges_faster_than_steepest_descent():
         sd[it + 1] = tr.F
     for it in (40, 100):
         assert trs[it - 1].F < sd[it] - 20.0, (it, trs[it - 1].F, sd[it])
+
+
+def test_object_grid_q_moments_split_the_line_search():
+    """The GPU line search (SolverCfg::qg, DESIGN 7) sums only the log part of DeltaF_k over the frame
+    pixels and takes the non-log part gamma qa + gamma^2 qb from the OBJECT grid, qa = sum I 2 Re(psi* eta),
+    qb = sum I |eta|^2 (Parseval per frame + G^H G = diag(I), integer positions).  Pinned against the
+    definition F(psi + gamma eta) - F(psi) (Eq.2) by brute force on a small problem: a dropped
+    factor 2, a conjugate on the wrong side or a wrong illumination fails it."""
+    H, N = 40, 8
+    psi = I.random_complex((H, H), seed=3) + 1.5
+    eta = 0.3 * I.random_complex((H, H), seed=4)
+    p = I.random_complex((N, N), seed=5)
+    scan = I.make_scan(H, H, N, 4, 6, 1, seed=6)
+    u = O.forward_G(psi, p, scan)
+    v = O.forward_G(eta, p, scan)
+    rng = np.random.default_rng(7)
+    d = rng.poisson(np.abs(u) ** 2).astype(np.float64)
+    Ill = O.illumination(p, scan, psi.shape)
+    qa = float(np.sum(Ill * 2.0 * np.real(np.conj(psi) * eta)))
+    qb = float(np.sum(Ill * np.abs(eta) ** 2))
+    F0 = O.objective_F(u, d)
+    for gam in (1.0, 0.25, 1.0 / 64):
+        w = np.abs(u + gam * v) ** 2 / np.abs(u) ** 2
+        split = gam * qa + gam * gam * qb - float(np.sum(d * np.log(w)))
+        ref = O.objective_F(O.forward_G(psi + gam * eta, p, scan), d) - F0
+        scale = float(np.sum(np.abs(u + gam * v) ** 2) + np.sum(np.abs(u) ** 2))
+        assert abs(split - ref) <= 1e-11 * scale, (gam, split, ref)
+        # the per-pixel moments it replaces give the same value
+        a = 2.0 * np.real(np.conj(u) * v)
+        b = np.abs(v) ** 2
+        assert abs(gam * np.sum(a) + gam * gam * np.sum(b) - (gam * qa + gam * gam * qb)) <= 1e-11 * scale
