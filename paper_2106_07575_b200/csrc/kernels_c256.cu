@@ -314,7 +314,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(512, 1)
     k_ls_c256ws(Geometry g, const float2* __restrict__ eta, const float2* __restrict__ probe_s,
                 const int2* __restrict__ pos, const int* __restrict__ order, const float2* __restrict__ u,
                 float2* __restrict__ v, const float* __restrict__ d, SolverCfg cfg, double* __restrict__ part,
-                const DevState* __restrict__ st) {
+                const DevState* __restrict__ st, int pf) {
     using namespace c4w;
     extern __shared__ __align__(16) unsigned char smraw[];
     float2* blk = reinterpret_cast<float2*>(smraw);
@@ -463,8 +463,14 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(512, 1)
             for (int64_t i = cid; i < nfr; i += ncl, ++it) {
                 const int b = it & 1;
                 const int64_t jf = order[i];
-                // (no L2 prefetch of u, d here: this or the next frame's quarter prefetched into L2
-                // measured 63.7 / 68.3 ms against 61.6 ms without)
+                // this frame's u, d into L2: CTA r prefetches full rows [64 r, 64 r + 64) (contiguous
+                // 128 + 64 KB), so the cluster covers the frame once and every CTA finds its column
+                // quarter in L2 (per-CTA strided quarters, 256 small prefetches, measured slower)
+                if (pf) {
+                    const int64_t ro = jf * (int64_t)(N * N) + (int64_t)rank * QC * N;
+                    if (ew == 0) prefetch_l2_frame(u + ro, QC * N * 8, lane);
+                    else if (ew == 1) prefetch_l2_frame(d + ro, QC * N * 4, lane);
+                }
                 c4_bar_sync(BAR_FULL + b, NT);
                 c4_tc_after();
 #pragma unroll 1
@@ -607,7 +613,8 @@ int launch_ls_c256(const Geometry& g, const float2* eta, const float2* probe_s, 
     if (c256_ws()) {
         const int grid = c256ws_grid(g.n_local);
         if (grid < 0) return -1;
-        k_ls_c256ws<<<grid, c4w::NT, c4w::DYN_BYTES, s>>>(g, eta, probe_s, pos, order, u, v, d, c, part, st);
+        static const int pf = getenv("PTYGER_C256_PF") ? atoi(getenv("PTYGER_C256_PF")) : 1;
+        k_ls_c256ws<<<grid, c4w::NT, c4w::DYN_BYTES, s>>>(g, eta, probe_s, pos, order, u, v, d, c, part, st, pf);
         return cudaGetLastError() == cudaSuccess ? 0 : -1;
     }
     const int grid = c256_grid(k_ls_c256, g.n_local);

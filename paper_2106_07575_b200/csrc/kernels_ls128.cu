@@ -86,7 +86,8 @@ __global__ void __launch_bounds__(512, 1) k_ls_ws(Geometry g, const float2* __re
                                                   const float2* __restrict__ probe_s, const int2* __restrict__ pos,
                                                   const int* __restrict__ order, const float2* __restrict__ u,
                                                   float2* __restrict__ v, const float* __restrict__ d, SolverCfg cfg,
-                                                  double* __restrict__ part, const DevState* __restrict__ st) {
+                                                  double* __restrict__ part, const DevState* __restrict__ st,
+                                                  int pf) {
     using namespace ws;
     extern __shared__ __align__(16) unsigned char smraw[];
     float2* sf = reinterpret_cast<float2*>(smraw);
@@ -270,8 +271,10 @@ __global__ void __launch_bounds__(512, 1) k_ls_ws(Geometry g, const float2* __re
                 const int b = it & 1;
                 const int64_t jf = order[i];
                 // this frame's u, d into L2 while its transform is still running
-                if (ew == 0) prefetch_l2_frame(u + jf * N * N, N * N * 8, lane);
-                else if (ew == 1) prefetch_l2_frame(d + jf * N * N, N * N * 4, lane);
+                if (pf) {
+                    if (ew == 0) prefetch_l2_frame(u + jf * N * N, N * N * 8, lane);
+                    else if (ew == 1) prefetch_l2_frame(d + jf * N * N, N * N * 4, lane);
+                }
                 bar_sync_n(BAR_FULL + b, NT);
                 tc_fence_after();
 #pragma unroll 1
@@ -346,16 +349,17 @@ int launch_ls_ws(const Geometry& g, const float2* eta, const float2* probe_s, co
                  const DevState* st, cudaStream_t s) {
     // the row DMA needs 16-B aligned window rows: even object width, integer positions
     const bool dma = (g.W % 2 == 0) && g.frac == nullptr;
+    static const int pf = getenv("PTYGER_PF") ? atoi(getenv("PTYGER_PF")) : 1;   // L2 prefetch of u, d
     if (dma) {
         if (cudaFuncSetAttribute(k_ls_ws<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ws::DYN_BYTES) !=
             cudaSuccess)
             return -1;
-        k_ls_ws<true><<<grid, ws::NT, ws::DYN_BYTES, s>>>(g, eta, probe_s, pos, order, u, v, d, c, part, st);
+        k_ls_ws<true><<<grid, ws::NT, ws::DYN_BYTES, s>>>(g, eta, probe_s, pos, order, u, v, d, c, part, st, pf);
     } else {
         if (cudaFuncSetAttribute(k_ls_ws<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ws::DYN_BYTES) !=
             cudaSuccess)
             return -1;
-        k_ls_ws<false><<<grid, ws::NT, ws::DYN_BYTES, s>>>(g, eta, probe_s, pos, order, u, v, d, c, part, st);
+        k_ls_ws<false><<<grid, ws::NT, ws::DYN_BYTES, s>>>(g, eta, probe_s, pos, order, u, v, d, c, part, st, pf);
     }
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
