@@ -485,6 +485,9 @@ __global__ void __launch_bounds__(256) k_lsx(int64_t count, const float2* __rest
     ls_pass_range(pass, st->keff, cfg, base, cnt);
     const bool run = cnt > 0 && !st->numeric_error &&
                      (EXACT ? (st->need_exact == pass + 1) : (!st->accepted));
+    // nothing to evaluate (the common case: pass 0 decided): leave at once.  The matching k_reduce
+    // skips too (same conditions), and with cnt = 0 its pick ignores the partials.
+    if (!run) return;
     if (tid < KC) sgam[tid] = (float)trial_gamma(cfg.gamma0, cfg.tau, base + tid);
     __syncthreads();
     const float eps2 = (float)(cfg.eps * cfg.eps);
