@@ -74,8 +74,9 @@ typedef struct {
     double eps;           /* modulus guard, 1e-16 (R#4)                                   */
     int32_t max_shrinks;  /* trials per iteration before a stall (gamma = 0), 32 (R#9)    */
     int32_t direction;    /* PTYGER_DIR_*                                                 */
-    int32_t ls_batch;     /* K in [4, 16] (default 16): trials per extra LS pass over the frames and the
-                             cap of pass 0, whose trial count adapts on the device to k*_prev + 3 */
+    int32_t ls_batch;     /* K in [4, 16] (default 16): cap of the adaptive pass-0 trial count (k*_prev + 3)
+                             and trials per extra LS pass over the frames (the first extra pass takes
+                             min(K, 8): a k* past pass 0 is usually a jump of a few) */
     int32_t estimator;    /* PTYGER_EST_ML (default) or PTYGER_EST_LS                          */
     int32_t device;       /* CUDA device ordinal                                          */
     int32_t rank;         /* this process's rank, 0..world-1                              */

@@ -287,7 +287,8 @@ static int enqueue_iteration(ptyger_ctx* c, int p, std::string& err, int64_t& la
     ++launches;
     // pass 0 evaluates keff trials (adaptive on the device, >= KMIN), later passes K each
     const int rest = sc.max_shrinks > KMIN ? sc.max_shrinks - KMIN : 0;
-    const int npass = 1 + (rest + sc.K - 1) / sc.K;
+    const int k1 = ls_k1(sc);
+    const int npass = 1 + (rest > 0 ? 1 : 0) + (rest > k1 ? (rest - k1 + sc.K - 1) / sc.K : 0);
     const int wscreen = LSP;
     for (int pass = 0; pass < npass; ++pass) {
         const bool fused = pass == 0;

@@ -84,10 +84,16 @@ struct SolverCfg {
     int qg;
 };
 
-// Trials [base, base + count) evaluated by LS pass p (host and device agree on this rule).
+// Trials [base, base + count) evaluated by LS pass p (host and device agree on this rule): pass 0
+// the adaptive keff = k*_prev + 3; pass 1 (k* jumped past keff, usually by a few) the next
+// K1 = min(K, 8) trials; later passes K each.  A pass over (u, v, d) costs a full read of the far
+// fields plus, per d > 0 pixel, a MUFU log per trial: 16 trials made the large view's pass 1
+// compute-bound (28.7 ms, ALU 53 %, MUFU 39 %, DRAM 56 %).
+__host__ __device__ inline int ls_k1(const SolverCfg& c) { return c.K < 8 ? c.K : 8; }
 __host__ __device__ inline void ls_pass_range(int pass, int keff, const SolverCfg& c, int& base, int& count) {
-    base = pass == 0 ? 0 : keff + (pass - 1) * c.K;
-    count = pass == 0 ? keff : c.K;
+    const int k1 = ls_k1(c);
+    base = pass == 0 ? 0 : pass == 1 ? keff : keff + k1 + (pass - 2) * c.K;
+    count = pass == 0 ? keff : pass == 1 ? k1 : c.K;
     if (base + count > c.max_shrinks) count = c.max_shrinks - base;
     if (count < 0) count = 0;
 }
