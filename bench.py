@@ -394,16 +394,28 @@ def time_frames(args, w, world, rank, local, dev, coll_dev, steps, warmup, with_
     n_local_bytes_ls = 20.0 * n * N * N / world + 8.0 * w.H * w.W / world  # v w, u r, d r + eta once
     pk, pk_kind = peaks()
     cand = {"k_grad": (kt["k_grad"], n_local_bytes_grad), "k_ls": (kt["k_ls"], n_local_bytes_ls)}
-    it_bytes = (64.0 * n * N * N + 80.0 * w.H * w.W) / world
+    # + 92 B per object pixel: DY reads, eta, eta gather, update, and the object-grid LS moments (psi, I)
+    it_bytes = (64.0 * n * N * N + 92.0 * w.H * w.W) / world
     dom = max(cand, key=lambda k: cand[k][0])
     dur_ms, algo_bytes = cand[dom]
     achieved = algo_bytes / (dur_ms / 1e3) / 1e9
+    # the kernel that actually runs for this role at this N (default paths; the env toggles of
+    # DESIGN.md 7 select the single-group LS kernels)
+    if dom == "k_ls":
+        if N == 256:
+            kname = "k_ls_c256" if os.environ.get("PTYGER_C256_WS") == "0" else "k_ls_c256ws"
+        elif N == 128:
+            kname = "k_ls" if os.environ.get("PTYGER_LS_WS") == "0" else "k_ls_ws"
+        else:
+            kname = "k_ls"
+    else:
+        kname = "k_grad256" if N == 256 else "k_grad"
     traffic = None
     prof_json = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof_json):
         try:
             with open(prof_json) as f:
-                traffic = json.load(f).get(w.name, {}).get(dom)
+                traffic = json.load(f).get(w.name, {}).get(kname)
         except Exception:
             traffic = None
 
@@ -449,13 +461,13 @@ def time_frames(args, w, world, rank, local, dev, coll_dev, steps, warmup, with_
     torch.cuda.empty_cache()
     fields = {
         "value": value, "ms_per_step": ms / steps,
-        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": pk, "peak_kind": pk_kind,
+        "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": pk, "peak_kind": pk_kind,
                      "unit": "GB/s", "frac": achieved / pk, "traffic": traffic,
                      "algorithmic_bytes_per_launch": algo_bytes, "avg_launch_ms": dur_ms,
                      "timing": "device globaltimer per launch, timed region (%d launches)" % ktimes[dom][1],
                      "k_grad_avg_ms": kt["k_grad"], "k_ls_avg_ms": kt["k_ls"]},
         # whole-iteration design-S roofline: 64 B per frame pixel (k_grad 36, k_ls 20,
-        # k_adj 8) + 80 B per object pixel (DY reads, eta, eta gather, update) per CG iteration
+        # k_adj 8) + 92 B per object pixel (DY reads, eta, eta gather, update, LS moments) per CG iteration
         "iteration_roofline": {"algorithmic_bytes": it_bytes, "achieved_GBps": it_bytes / (ms / steps) / 1e6,
                                "peak_GBps": pk, "frac": it_bytes / (ms / steps) / 1e6 / pk},
         "stage_ms": stage_ms(trs),
