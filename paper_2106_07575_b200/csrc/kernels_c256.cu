@@ -459,10 +459,30 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(512, 1)
 #pragma unroll
             for (int k = 0; k < KT; ++k) gk[k] = sgam[k];
             const uint64_t pol = l2_evict_first();   // u, d read once, v written once per pass
+            // u, d of one group of 4 elements: frame jf, round rd (column 64 rank + 32 (rd / 2) + lane,
+            // rows t + 16 k2 with t = ew + 8 (rd % 2)), elements k2 = 4 gi .. 4 gi + 3.  The loads run
+            // one group ahead ACROSS rounds and frames (the next round's / frame's first group is issued
+            // during the last group of the current one), so no round starts on an exposed L2 latency.
+            auto elem_base = [&](int64_t jf, int rd) -> int64_t {
+                return jf * (int64_t)(N * N) + (int64_t)(ew + 8 * (rd & 1)) * N + (int64_t)rank * QC + (rd >> 1) * 32 +
+                       lane;
+            };
+            float2 un[4];
+            float dn[4];
+            auto load_group = [&](int64_t jf, int rd, int gi) {
+                const int64_t o = elem_base(jf, rd) + (int64_t)gi * 4 * R * N;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    un[e] = ld2_hint_na(u + o + e * R * N, pol);
+                    dn[e] = ld1_hint_na(d + o + e * R * N, pol);
+                }
+            };
+            if (nmine > 0) load_group(order[cid], 0, 0);
             int it = 0;
             for (int64_t i = cid; i < nfr; i += ncl, ++it) {
                 const int b = it & 1;
                 const int64_t jf = order[i];
+                const int64_t jnext = i + ncl < nfr ? (int64_t)order[i + ncl] : -1;
                 // this frame's u, d into L2: CTA r prefetches full rows [64 r, 64 r + 64) (contiguous
                 // 128 + 64 KB), so the cluster covers the frame once and every CTA finds its column
                 // quarter in L2 (per-CTA strided quarters, 256 small prefetches, measured slower)
@@ -475,24 +495,12 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(512, 1)
                 c4_tc_after();
 #pragma unroll 1
                 for (int rd = 0; rd < 4; ++rd) {
-                    // column 64 rank + 32 (rd / 2) + lane, rows t + 16 k2 with t = ew + 8 (rd % 2)
-                    const int t = ew + 8 * (rd & 1);
-                    const int64_t fb = jf * (int64_t)(N * N) + (int64_t)t * N + (int64_t)rank * QC + (rd >> 1) * 32 + lane;
-                    const float2* __restrict__ ub = u + fb;
-                    const float* __restrict__ db = d + fb;
-                    float2* __restrict__ vb = v + fb;
+                    float2* __restrict__ vb = v + elem_base(jf, rd);
                     float S[KC];
                     LsMom m;
 #pragma unroll
                     for (int k = 0; k < KC; ++k) S[k] = 0.f;
                     LsQState qs;
-                    float2 un[4];
-                    float dn[4];
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        un[e] = ld2_hint_na(ub + e * R * N, pol);
-                        dn[e] = ld1_hint_na(db + e * R * N, pol);
-                    }
 #pragma unroll 1
                     for (int gi = 0; gi < T / 4; ++gi) {
                         const int go = gi * 4 * R * N;
@@ -503,14 +511,12 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(512, 1)
                             uc[e] = un[e];
                             dc[e] = dn[e];
                         }
-                        if (gi + 1 < T / 4) {
-                            const int gn = go + 4 * R * N;
-#pragma unroll
-                            for (int e = 0; e < 4; ++e) {
-                                un[e] = ld2_hint_na(ub + gn + e * R * N, pol);
-                                dn[e] = ld1_hint_na(db + gn + e * R * N, pol);
-                            }
-                        }
+                        if (gi + 1 < T / 4)
+                            load_group(jf, rd, gi + 1);
+                        else if (rd + 1 < 4)
+                            load_group(jf, rd + 1, 0);
+                        else if (jnext >= 0)
+                            load_group(jnext, 0, 0);
                         float2 X[4];
                         c4_tmem_ld8(tq + (uint32_t)(256 * b + 32 * rd + 8 * gi), X);
 #pragma unroll

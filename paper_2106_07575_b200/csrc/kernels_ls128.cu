@@ -266,10 +266,32 @@ __global__ void __launch_bounds__(512, 1) k_ls_ws(Geometry g, const float2* __re
             float gk[KT];   // trial gammas in registers for the whole run
 #pragma unroll
             for (int k = 0; k < KT; ++k) gk[k] = sgam[k];
+            // u, d of one group of 4 elements: frame jf, round rd (column c = 32 rd + lane), elements
+            // q = 4 gi .. 4 gi + 3 at rows (q / T) T + ew + R (q % T).  The loads run one group ahead
+            // ACROSS rounds and frames, so no round starts on an exposed L2 latency.
+            auto elem_base = [&](int64_t jf, int rd) -> int64_t {
+                return jf * (int64_t)(N * N) + (int64_t)ew * N + rd * 32 + lane;
+            };
+            auto goff = [](int gi) -> int {
+                const int q0 = 4 * gi;
+                return ((q0 / T) * T + R * (q0 % T)) * N;
+            };
+            float2 un[4];
+            float dn[4];
+            auto load_group = [&](int64_t jf, int rd, int gi) {
+                const int64_t o = elem_base(jf, rd) + goff(gi);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    un[e] = ldg2_na(u + o + e * R * N);
+                    dn[e] = ldg1_na(d + o + e * R * N);
+                }
+            };
+            if (nmine > 0) load_group(order[blockIdx.x], 0, 0);
             int it = 0;
             for (int64_t i = blockIdx.x; i < nfr; i += gridDim.x, ++it) {
                 const int b = it & 1;
                 const int64_t jf = order[i];
+                const int64_t jnext = i + gridDim.x < nfr ? (int64_t)order[i + gridDim.x] : -1;
                 // this frame's u, d into L2 while its transform is still running
                 // (issued by the FFT group half a frame earlier, or one frame ahead: measured no better
                 // than no prefetch at all, 3.12 / 2.98 ms against 2.72 ms)
@@ -281,29 +303,15 @@ __global__ void __launch_bounds__(512, 1) k_ls_ws(Geometry g, const float2* __re
                 tc_fence_after();
 #pragma unroll 1
                 for (int rd = 0; rd < CROUNDS; ++rd) {
-                    // column c = 32 rd + lane; element q of the thread sits at row (q / T) T + ew + R (q % T)
-                    const int c = rd * 32 + lane;
-                    const int64_t fb = jf * (int64_t)(N * N) + (int64_t)ew * N + c;
-                    const float2* __restrict__ ub = u + fb;
-                    const float* __restrict__ db = d + fb;
-                    float2* __restrict__ vb = v + fb;
+                    float2* __restrict__ vb = v + elem_base(jf, rd);
                     float S[KC];
                     LsMom m;
 #pragma unroll
                     for (int k = 0; k < KC; ++k) S[k] = 0.f;
                     LsQState qs;
-                    float2 un[4];
-                    float dn[4];
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        un[e] = ldg2_na(ub + e * R * N);
-                        dn[e] = ldg1_na(db + e * R * N);
-                    }
 #pragma unroll 1
                     for (int gi = 0; gi < R / 4; ++gi) {
-                        // groups of 4 consecutive q share j = q / T: offsets step by R N inside a group
-                        const int q0 = 4 * gi;
-                        const int go = ((q0 / T) * T + R * (q0 % T)) * N;
+                        const int go = goff(gi);
                         float2 uc[4];
                         float dc[4];
 #pragma unroll
@@ -311,15 +319,12 @@ __global__ void __launch_bounds__(512, 1) k_ls_ws(Geometry g, const float2* __re
                             uc[e] = un[e];
                             dc[e] = dn[e];
                         }
-                        if (gi + 1 < R / 4) {
-                            const int q1 = q0 + 4;
-                            const int gn = ((q1 / T) * T + R * (q1 % T)) * N;
-#pragma unroll
-                            for (int e = 0; e < 4; ++e) {
-                                un[e] = ldg2_na(ub + gn + e * R * N);
-                                dn[e] = ldg1_na(db + gn + e * R * N);
-                            }
-                        }
+                        if (gi + 1 < R / 4)
+                            load_group(jf, rd, gi + 1);
+                        else if (rd + 1 < CROUNDS)
+                            load_group(jf, rd + 1, 0);
+                        else if (jnext >= 0)
+                            load_group(jnext, 0, 0);
                         float2 X[4];
                         tmem_ld8(tq + (uint32_t)(256 * b + 32 * rd + 8 * gi), X);
 #pragma unroll
