@@ -55,7 +55,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-large", action="store_true",
                     help="skip the large-view sub-record (8192^2, 256^2, 99 856 frames) of the paper-config run")
-    ap.add_argument("--large-steps", type=int, default=5)
+    ap.add_argument("--large-steps", type=int, default=10)
     return ap.parse_args()
 
 
