@@ -404,6 +404,9 @@ def time_frames(args, w, world, rank, local, dev, coll_dev, steps, warmup, with_
     if dom == "k_ls":
         if N == 256:
             kname = "k_ls_c256" if os.environ.get("PTYGER_C256_WS") == "0" else "k_ls_c256ws"
+            if kname == "k_ls_c256ws" and os.environ.get("PTYGER_C256_SIDE", "110") != "0":
+                # + the side kernel on the SMs the four-CTA clusters leave idle (one launch span)
+                kname = "k_ls_c256ws+k_ls256_side"
         elif N == 128:
             kname = "k_ls" if os.environ.get("PTYGER_LS_WS") == "0" else "k_ls_ws"
         else:

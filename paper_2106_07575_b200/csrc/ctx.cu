@@ -144,7 +144,8 @@ struct ptyger_ctx {
     cudaEvent_t ev_it[2] = {nullptr, nullptr};
     float last_ms = 0.f;
     int grid_fr = 0, grid_el = 0;
-    int parts_ls = 0;    // per-CTA partial rows written by the LS pass-0 frame kernel
+    int parts_ls = 0;    // per-CTA partial rows written by the LS pass-0 frame kernel(s)
+    int ls_side = 0;     // N = 256: CTAs of the side LS kernel (c256_ls_side), 0 = none
     int m_host = 0;
     int pending_iters = 0;   // iterations launched by ptyger_cg_launch, not yet waited for
     int64_t launches_per_iter = 0, last_launches = 0;
@@ -284,7 +285,7 @@ static int enqueue_iteration(ptyger_ctx* c, int p, std::string& err, int64_t& la
     // is followed by an exact re-evaluation that runs only when the screening left it undecided;
     // further passes (trials pK..pK+K-1) run only while nothing was accepted.
     LK(launch_ls(g, c->eta, c->probe, c->probe_s, c->pos, c->order, c->u, c->v, c->d, sc, c->part_fr, c->grid_fr, c->st, s));
-    ++launches;
+    launches += c->ls_side > 0 ? 2 : 1;   // N = 256: + the side kernel on the SMs the clusters leave idle
     // pass 0 evaluates keff trials (adaptive on the device, >= KMIN), later passes K each
     const int rest = sc.max_shrinks > KMIN ? sc.max_shrinks - KMIN : 0;
     const int k1 = ls_k1(sc);
@@ -607,6 +608,7 @@ static ptyger_status init_impl(ptyger_ctx* c, const float* object, const float* 
     // N = 256: the LS pass runs on clusters of four CTAs (large config: 96.7 -> 71.6 ms against the
     // v-slot transpose kernel); the GRAD pass keeps the v-slot kernel (kernels_n256.cu)
     c->parts_ls = N == 256 ? c256_ls_parts(nl) : c->grid_fr;
+    c->ls_side = N == 256 ? c256_ls_side(nl) : 0;
     if (c->parts_ls <= 0) {
         err = "cluster LS kernel setup failed";
         return PTYGER_E_CUDA;
@@ -842,6 +844,9 @@ static ptyger_status create_ctx(ptyger_ctx** out, const ptyger_config* cfg_in, c
     c->sc.max_shrinks = cfg.max_shrinks;
     c->sc.direction = cfg.direction;
     c->sc.K = cfg.ls_batch;
+    // margin of the adaptive pass-0 trial count over the previous k* (experiments: PTYGER_KEFF_ADD)
+    c->sc.kadd = getenv("PTYGER_KEFF_ADD") ? atoi(getenv("PTYGER_KEFF_ADD")) : 3;
+    if (c->sc.kadd < 0) c->sc.kadd = 0;
     c->sc.est = cfg.estimator;
     if (cfg.direction == PTYGER_DIR_GD) c->sc.max_shrinks = 1;   // Eq.4: one fixed step gamma0
     c->H = H;

@@ -82,6 +82,7 @@ struct SolverCfg {
     // (qa, qb of DevState; Parseval + G^H G = diag(I), exact for integer positions) instead of per frame
     // pixel moments.  Set for the Poisson ML estimator with integer positions.
     int qg;
+    int kadd;                        // adaptive pass-0 trials: keff = k*_prev + kadd (clamped to [KMIN, K])
 };
 
 // Trials [base, base + count) evaluated by LS pass p (host and device agree on this rule): pass 0
@@ -165,9 +166,15 @@ int launch_ls_ws(const Geometry& g, const float2* eta, const float2* probe_s, co
                  const DevState* st, cudaStream_t s);
 // cluster-of-four frame kernels for N = 256 (kernels_c256.cu); probe_s = probe / N
 int c256_ls_parts(int64_t nfr);
+int c256_ls_side(int64_t nfr);   // CTAs of the concurrent side kernel (0: none)
 int launch_ls_c256(const Geometry& g, const float2* eta, const float2* probe_s, const int2* pos, const int* order,
                    const float2* u, float2* v, const float* d, const SolverCfg& c, double* part, const DevState* st,
                    cudaStream_t s);
+// LS pass 0 for N = 256 on the SMs the clusters leave idle, frames [i0, n_local) of the canonical order,
+// concurrent with k_ls_c256ws (programmatic dependent launch); part: its first partial row (kernels_n256.cu)
+int launch_ls256_side(const Geometry& g, const float2* eta, const float2* probe_s, const int2* pos, const int* order,
+                      const float2* u, float2* v, const float* d, const SolverCfg& c, double* part, const DevState* st,
+                      int64_t i0, int grid, cudaStream_t s);
 int launch_scale_c(const float2* in, float2* out, int64_t n, float s, cudaStream_t st);
 int launch_band_add(float2* gcur, const float2* recv, int64_t row_lo, int64_t rows, int64_t W,
                     const float2* gprev, const float2* eta, int64_t own_lo, int64_t own_hi,

@@ -369,6 +369,9 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(512, 1)
     c4_arrive();
     c4_wait();
     const uint32_t tbase = s_tmem;
+    // every CTA of the grid is resident: release the side kernel (k_ls256_side, launched after this one
+    // with programmatic stream serialization) onto the SMs the clusters leave idle
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int64_t nfr = err ? 0 : g.n_local;
     const int wq4 = warp & 3, whalf = (warp & 7) >> 2;
     const uint32_t tq = tbase + ((uint32_t)(32 * wq4) << 16) + (uint32_t)(128 * whalf);
@@ -611,7 +614,49 @@ static bool c256_ws() {
     return ws;
 }
 
-int c256_ls_parts(int64_t nfr) { return c256_ws() ? c256ws_grid(nfr) : c256_grid(k_ls_c256, nfr); }
+// Side kernel on the SMs the clusters leave idle (kernels_n256.cu k_ls256_side): it takes the last
+// n2 = nfr * PTYGER_C256_SIDE / 1000 frames of the canonical order, one CTA per idle SM; off when fewer
+// frames than side CTAs.  Measured at the large view (profiles/r2_history.md, session 3): the side
+// kernel needs ~71 us per frame and SM against ~75-80 SM-us in the clusters, but the clusters slow by
+// ~7 % while it runs (the board is at its power cap), so the pass gains ~2.5 %: 55.9 ms without, 54.6 /
+// 54.4 ms at 100 / 120 per mille, 61.9 ms at 140 (the side kernel becomes the tail).
+static void c256_side_split(int64_t nfr, int cgrid, int64_t& n1, int& sgrid) {
+    static int sms = 0;
+    if (sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) sms = -1;
+    }
+    static const int share = getenv("PTYGER_C256_SIDE") ? atoi(getenv("PTYGER_C256_SIDE")) : 110;
+    n1 = nfr;
+    sgrid = 0;
+    const int idle = sms - cgrid;
+    if (!c256_ws() || idle <= 0 || share <= 0) return;
+    const int64_t n2 = nfr * share / 1000;
+    if (n2 < idle) return;
+    n1 = nfr - n2;
+    sgrid = idle;
+}
+
+int c256_ls_side(int64_t nfr) {
+    if (!c256_ws()) return 0;
+    const int cg = c256ws_grid(nfr);
+    if (cg < 0) return 0;
+    int64_t n1;
+    int sg;
+    c256_side_split(nfr, cg, n1, sg);
+    return sg;
+}
+
+int c256_ls_parts(int64_t nfr) {
+    if (!c256_ws()) return c256_grid(k_ls_c256, nfr);
+    const int cg = c256ws_grid(nfr);
+    if (cg < 0) return cg;
+    int64_t n1;
+    int sg;
+    c256_side_split(nfr, cg, n1, sg);
+    return cg + sg;
+}
 
 int launch_ls_c256(const Geometry& g, const float2* eta, const float2* probe_s, const int2* pos, const int* order,
                    const float2* u, float2* v, const float* d, const SolverCfg& c, double* part, const DevState* st,
@@ -620,8 +665,16 @@ int launch_ls_c256(const Geometry& g, const float2* eta, const float2* probe_s, 
         const int grid = c256ws_grid(g.n_local);
         if (grid < 0) return -1;
         static const int pf = getenv("PTYGER_C256_PF") ? atoi(getenv("PTYGER_C256_PF")) : 1;
-        k_ls_c256ws<<<grid, c4w::NT, c4w::DYN_BYTES, s>>>(g, eta, probe_s, pos, order, u, v, d, c, part, st, pf);
-        return cudaGetLastError() == cudaSuccess ? 0 : -1;
+        int64_t n1;
+        int sg;
+        c256_side_split(g.n_local, grid, n1, sg);
+        Geometry g1 = g;
+        g1.n_local = n1;
+        k_ls_c256ws<<<grid, c4w::NT, c4w::DYN_BYTES, s>>>(g1, eta, probe_s, pos, order, u, v, d, c, part, st, pf);
+        if (cudaGetLastError() != cudaSuccess) return -1;
+        if (sg > 0)
+            return launch_ls256_side(g, eta, probe_s, pos, order, u, v, d, c, part + (size_t)grid * LSP, st, n1, sg, s);
+        return 0;
     }
     const int grid = c256_grid(k_ls_c256, g.n_local);
     if (grid < 0) return -1;

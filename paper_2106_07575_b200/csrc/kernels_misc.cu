@@ -683,7 +683,7 @@ __device__ void pick_body(DevState* st, const SolverCfg& c, int pass, int exact_
     st->trace_idx += 1;
     st->trace_written = 1;
     st->m += 1;
-    st->keff = st->stalled ? c.K : min(c.K, max(KMIN, st->kstar + 3));
+    st->keff = st->stalled ? c.K : min(c.K, max(KMIN, st->kstar + c.kadd));
 }
 
 // Stage timestamps (ptyger_trace ms_* fields): a one-thread kernel between the stages of

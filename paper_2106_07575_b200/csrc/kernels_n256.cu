@@ -143,6 +143,137 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1)
 }
 
 // ---------------------------------------------------------------------------------------------
+// k_ls256_side: LS pass 0 for N = 256 on the SMs the four-CTA clusters of k_ls_c256ws leave idle (a GPC
+// whose SM count is not a multiple of four keeps 2 SMs free: 16 of 148 on B200).  It runs CONCURRENTLY
+// with the cluster kernel on a static tail of the canonical frame order [i0, n): the cluster kernel
+// releases it with a programmatic-dependent-launch trigger once all its CTAs are resident (so these
+// CTAs land on the free SMs and never delay a cluster), and it waits for the cluster grid's completion
+// (griddepcontrol.wait) before it exits, so the reduction launched after it sees both kernels' partials.
+// One CTA per frame, the frame's own v slot in HBM as the transpose buffer (pass 1: window rows x p/N ->
+// row DFTs -> slot rows; pass 2: 32-column batches back from L2 -> column DFTs = v), then the screening
+// epilogue of every LS kernel (dev.cuh ls_push / ls_flush) on (u, v, d).  Its per-CTA partial rows follow
+// the cluster kernel's in `part` (reduced in one fixed order: bitwise reproducible).
+// ---------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(512, 1)
+    k_ls256_side(Geometry g, const float2* __restrict__ eta, const float2* __restrict__ probe_s,
+                 const int2* __restrict__ pos, const int* __restrict__ order, const float2* __restrict__ u,
+                 float2* __restrict__ v, const float* __restrict__ d, SolverCfg cfg, double* __restrict__ part,
+                 const DevState* __restrict__ st, int64_t i0) {
+    using namespace n256;
+    extern __shared__ float2 smem[];
+    float2* buf = smem;
+    float2* tw = smem + BUF;
+    __shared__ double sred[16][KC];
+    __shared__ double smom[16][4];
+    __shared__ float sgam[KC];
+    __shared__ LsWarpQ<2> wq[16];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const bool err = st->numeric_error != 0;
+    int base, cnt;
+    ls_pass_range(0, st->keff, cfg, base, cnt);
+    ktime_start(st, 1);
+    build_twiddles<N>(tw);
+    build_row_twiddles<N>(tw + N);
+    if (tid < KC) sgam[tid] = (float)trial_gamma(cfg.gamma0, cfg.tau, base + tid);
+    __syncthreads();
+    const int64_t nfr = err ? 0 : g.n_local;
+    const float eps2 = (float)(cfg.eps * cfg.eps);
+    const uint64_t pol_s = l2_evict_first(), pol_k = l2_evict_last();
+    double tot = 0.0;
+    double mom[4] = {0.0, 0.0, 0.0, 0.0};
+    trial_dispatch(cnt, cfg, [&]<int KT, bool LSE, bool QG>() {
+        float gk[KT];
+#pragma unroll
+        for (int k = 0; k < KT; ++k) gk[k] = sgam[k];
+        for (int64_t i = i0 + blockIdx.x; i < nfr; i += gridDim.x) {
+            const int64_t j = order[i];
+            const int2 s = pos[j];
+            float2* vj = v + j * N * N;
+            // ---- pass 1: 8 batches of 32 rows, row DFTs -> slot rows (kept in L2)
+#pragma unroll 1
+            for (int rb = 0; rb < N / ROWB; ++rb) {
+                const int row = rb * ROWB + tid / T, t = tid % T;
+                float2 x[R];
+                window_row<R, T>(eta, g, s, j, row, t, probe_s + row * N + t, x);
+                __syncwarp();
+                row_fft_regs<N, false, true>(x, buf + (tid / T) * LD, t, tw, tw + N);
+                float2* dst = vj + (int64_t)row * N + t;
+#pragma unroll
+                for (int k2 = 0; k2 < T; ++k2) st2_hint(dst + R * k2, x[k2], pol_k);
+            }
+            __syncthreads();   // every slot row written (CTA-scope order of the global stores)
+            // ---- pass 2: 8 batches of 32 columns; X[k2] = v at row warp + 16 k2, column c
+#pragma unroll 1
+            for (int cb = 0; cb < N / COLB; ++cb) {
+                float2 X[R];
+                int c;
+                n256_column<false>(vj, cb, buf, tw, X, c);
+                // park X in this thread's own phase-2 slots of buf (read only by this thread) so the
+                // epilogue is a rolled loop over groups of four
+                float2* mine = buf + (T * warp) * COLB + lane;
+#pragma unroll
+                for (int k2 = 0; k2 < T; ++k2) mine[k2 * COLB] = X[k2];
+                const int64_t ob = j * N * N + (int64_t)warp * N + c;
+                float S[KC];
+                LsMom m;
+#pragma unroll
+                for (int k = 0; k < KC; ++k) S[k] = 0.f;
+                LsQState qs;
+#pragma unroll 1
+                for (int gi = 0; gi < T / 4; ++gi) {
+                    float2 uc[4], vc[4];
+                    float dc[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int64_t o = ob + (int64_t)(4 * gi + e) * R * N;
+                        uc[e] = ld2_hint_na(u + o, pol_s);
+                        dc[e] = ld1_hint_na(d + o, pol_s);
+                        vc[e] = mine[(4 * gi + e) * COLB];
+                        st2_hint(v + o, vc[e], pol_s);
+                    }
+                    ls_push<KT, LSE, QG>(wq[warp], qs, slice<0, 2>(uc), slice<0, 2>(vc), slice<0, 2>(dc), gk, eps2, S,
+                                         m, lane);
+                    ls_push<KT, LSE, QG>(wq[warp], qs, slice<2, 2>(uc), slice<2, 2>(vc), slice<2, 2>(dc), gk, eps2, S,
+                                         m, lane);
+                }
+                ls_flush<KT, LSE, QG>(wq[warp], qs, gk, eps2, S, m, lane);
+                ls_run_out<KC>(S, m, tot, mom, lane);
+            }
+            __syncthreads();   // buf free before the next frame's row exchanges
+        }
+    });
+    ktime_end(st, 1);
+    ls_block_out<KC, 16>(tot, mom, sred, smom, part);
+    // the kernels after this one in the stream must see the cluster kernel's partials as well
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+int launch_ls256_side(const Geometry& g, const float2* eta, const float2* probe_s, const int2* pos, const int* order,
+                      const float2* u, float2* v, const float* d, const SolverCfg& c, double* part, const DevState* st,
+                      int64_t i0, int grid, cudaStream_t s) {
+    static bool attr = false;
+    if (!attr) {
+        if (cudaFuncSetAttribute(k_ls256_side, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)n256::SMEM) !=
+            cudaSuccess)
+            return -1;
+        attr = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid, 1, 1);
+    cfg.blockDim = dim3(512, 1, 1);
+    cfg.dynamicSmemBytes = n256::SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, k_ls256_side, g, eta, probe_s, pos, order, u, v, d, c, part, st, i0) != cudaSuccess)
+        return -1;
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+// ---------------------------------------------------------------------------------------------
 // k_fwd (N = 256): u = F(p * psi[window]) (pass 1 rows -> u slot, pass 2 columns) and the Eq.2
 // objective partials (init / set_state; the LS pass runs on clusters of four, kernels_c256.cu).
 // ---------------------------------------------------------------------------------------------

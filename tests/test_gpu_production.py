@@ -103,3 +103,28 @@ def test_warm_start_trajectory_conditioned(L, name):
     assert all(F[i + 1] <= F[i] for i in range(len(F) - 1))
     assert rel(np.array(F), np.array([t.F for t in otr])) <= 1e-6
     pt.close()
+
+
+@pytest.mark.parametrize("name", ["n128m", "n256m"])
+def test_pass0_trial_count_does_not_change_the_iteration(L, name, monkeypatch):
+    """Eq.7 accepts the FIRST trial gamma_0 tau^k that satisfies the Armijo test; how many trials
+    one pass over the far fields evaluates (keff = k*_prev + PTYGER_KEFF_ADD, then the extra passes) is a
+    scheduling choice that must not change the iteration.  From the flat start psi_0 = 1 (k* jumps, extra
+    passes) and in the production kernels with more frames than CTAs / clusters: identical shrinks and
+    restarts, F and the object equal to float rounding (every trial sum S_k is accumulated in the same
+    order whatever the pass holds; only the screening bound, hence an exact re-evaluation, may differ)."""
+    psi_true, p, scan, d = get_fixture(name)
+    runs = []
+    for kadd in (0, 3, 12):
+        monkeypatch.setenv("PTYGER_KEFF_ADD", str(kadd))
+        pt = L.Ptyger(np.ones_like(psi_true), p, scan, d)
+        tr = pt.iterate(8)
+        runs.append(([t["shrinks"] for t in tr], [t["restarted"] for t in tr], np.array([t["F"] for t in tr]),
+                     [t["ls_passes"] for t in tr], pt.get_object()))
+        pt.close()
+    print(f"{name}: shrinks {runs[0][0]}, LS passes per kadd {[r[3] for r in runs]}")
+    for r in runs[1:]:
+        assert r[0] == runs[0][0] and r[1] == runs[0][1]
+        assert rel(r[2], runs[0][2]) <= 1e-9
+        assert rel(r[4], runs[0][4]) <= 1e-6
+    assert [r[3] for r in runs][0] != [r[3] for r in runs][2]   # the schedules really differed
