@@ -192,9 +192,6 @@ class Ptyger:
 
     def __init__(self, obj, probe, scan, d, config: Config | None = None, **cfg):
         self.cfg = config if config is not None else default_config(**cfg)
-        self._nccl_buf = None
-        if self.cfg.world > 1 and "nccl_id" in cfg and isinstance(cfg["nccl_id"], (bytes, bytearray)):
-            pass
         o = as_c64(obj)
         p = as_c64(probe)
         self.H, self.W = (o.shape[0], o.shape[1]) if o.ndim == 3 else (obj.shape[0], obj.shape[1])

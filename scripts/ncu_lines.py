@@ -15,8 +15,11 @@ ap = argparse.ArgumentParser()
 ap.add_argument("rep")
 ap.add_argument("--top", type=int, default=40)
 a = ap.parse_args()
-out = subprocess.run(["ncu", "-i", a.rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
-                     capture_output=True, text=True).stdout
+if a.rep.endswith(".csv"):   # a saved `ncu -i <rep> --page source --csv --print-source cuda,sass` export
+    out = open(a.rep).read()
+else:
+    out = subprocess.run(["ncu", "-i", a.rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+                         capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 hdr = None
 fname = "?"
