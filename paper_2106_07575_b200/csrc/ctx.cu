@@ -607,8 +607,8 @@ static ptyger_status init_impl(ptyger_ctx* c, const float* object, const float* 
     c->band_grid = c->sms * 2;
     // N = 256: the LS pass runs on clusters of four CTAs (large config: 96.7 -> 71.6 ms against the
     // v-slot transpose kernel); the GRAD pass keeps the v-slot kernel (kernels_n256.cu)
-    c->parts_ls = N == 256 ? c256_ls_parts(nl) : c->grid_fr;
-    c->ls_side = N == 256 ? c256_ls_side(nl) : 0;
+    c->parts_ls = N == 256 ? c256_ls_parts(nl, c->sc.side) : c->grid_fr;
+    c->ls_side = N == 256 ? c256_ls_side(nl, c->sc.side) : 0;
     if (c->parts_ls <= 0) {
         err = "cluster LS kernel setup failed";
         return PTYGER_E_CUDA;
@@ -847,6 +847,8 @@ static ptyger_status create_ctx(ptyger_ctx** out, const ptyger_config* cfg_in, c
     // margin of the adaptive pass-0 trial count over the previous k* (experiments: PTYGER_KEFF_ADD)
     c->sc.kadd = getenv("PTYGER_KEFF_ADD") ? atoi(getenv("PTYGER_KEFF_ADD")) : 3;
     if (c->sc.kadd < 0) c->sc.kadd = 0;
+    // N = 256: share of the frames (per mille) for the LS side kernel on the SMs the clusters leave idle
+    c->sc.side = getenv("PTYGER_C256_SIDE") ? atoi(getenv("PTYGER_C256_SIDE")) : 110;
     c->sc.est = cfg.estimator;
     if (cfg.direction == PTYGER_DIR_GD) c->sc.max_shrinks = 1;   // Eq.4: one fixed step gamma0
     c->H = H;

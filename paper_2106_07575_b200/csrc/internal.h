@@ -83,6 +83,7 @@ struct SolverCfg {
     // pixel moments.  Set for the Poisson ML estimator with integer positions.
     int qg;
     int kadd;                        // adaptive pass-0 trials: keff = k*_prev + kadd (clamped to [KMIN, K])
+    int side;                        // N = 256: per mille of the frames for the LS side kernel (0 = off)
 };
 
 // Trials [base, base + count) evaluated by LS pass p (host and device agree on this rule): pass 0
@@ -165,8 +166,8 @@ int launch_ls_ws(const Geometry& g, const float2* eta, const float2* probe_s, co
                  const float2* u, float2* v, const float* d, const SolverCfg& c, double* part, int grid,
                  const DevState* st, cudaStream_t s);
 // cluster-of-four frame kernels for N = 256 (kernels_c256.cu); probe_s = probe / N
-int c256_ls_parts(int64_t nfr);
-int c256_ls_side(int64_t nfr);   // CTAs of the concurrent side kernel (0: none)
+int c256_ls_parts(int64_t nfr, int side);
+int c256_ls_side(int64_t nfr, int side);   // CTAs of the concurrent side kernel (0: none)
 int launch_ls_c256(const Geometry& g, const float2* eta, const float2* probe_s, const int2* pos, const int* order,
                    const float2* u, float2* v, const float* d, const SolverCfg& c, double* part, const DevState* st,
                    cudaStream_t s);

@@ -615,19 +615,19 @@ static bool c256_ws() {
 }
 
 // Side kernel on the SMs the clusters leave idle (kernels_n256.cu k_ls256_side): it takes the last
-// n2 = nfr * PTYGER_C256_SIDE / 1000 frames of the canonical order, one CTA per idle SM; off when fewer
+// n2 = nfr * share / 1000 frames of the canonical order (SolverCfg::side, PTYGER_C256_SIDE at init,
+// default 110), one CTA per idle SM; off when fewer
 // frames than side CTAs.  Measured at the large view (profiles/r2_history.md, session 3): the side
 // kernel needs ~71 us per frame and SM against ~75-80 SM-us in the clusters, but the clusters slow by
 // ~7 % while it runs (the board is at its power cap), so the pass gains ~2.5 %: 55.9 ms without, 54.6 /
 // 54.4 ms at 100 / 120 per mille, 61.9 ms at 140 (the side kernel becomes the tail).
-static void c256_side_split(int64_t nfr, int cgrid, int64_t& n1, int& sgrid) {
+static void c256_side_split(int64_t nfr, int cgrid, int share, int64_t& n1, int& sgrid) {
     static int sms = 0;
     if (sms == 0) {
         int dev = 0;
         cudaGetDevice(&dev);
         if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) sms = -1;
     }
-    static const int share = getenv("PTYGER_C256_SIDE") ? atoi(getenv("PTYGER_C256_SIDE")) : 110;
     n1 = nfr;
     sgrid = 0;
     const int idle = sms - cgrid;
@@ -638,23 +638,23 @@ static void c256_side_split(int64_t nfr, int cgrid, int64_t& n1, int& sgrid) {
     sgrid = idle;
 }
 
-int c256_ls_side(int64_t nfr) {
+int c256_ls_side(int64_t nfr, int side) {
     if (!c256_ws()) return 0;
     const int cg = c256ws_grid(nfr);
     if (cg < 0) return 0;
     int64_t n1;
     int sg;
-    c256_side_split(nfr, cg, n1, sg);
+    c256_side_split(nfr, cg, side, n1, sg);
     return sg;
 }
 
-int c256_ls_parts(int64_t nfr) {
+int c256_ls_parts(int64_t nfr, int side) {
     if (!c256_ws()) return c256_grid(k_ls_c256, nfr);
     const int cg = c256ws_grid(nfr);
     if (cg < 0) return cg;
     int64_t n1;
     int sg;
-    c256_side_split(nfr, cg, n1, sg);
+    c256_side_split(nfr, cg, side, n1, sg);
     return cg + sg;
 }
 
@@ -667,7 +667,7 @@ int launch_ls_c256(const Geometry& g, const float2* eta, const float2* probe_s, 
         static const int pf = getenv("PTYGER_C256_PF") ? atoi(getenv("PTYGER_C256_PF")) : 1;
         int64_t n1;
         int sg;
-        c256_side_split(g.n_local, grid, n1, sg);
+        c256_side_split(g.n_local, grid, c.side, n1, sg);
         Geometry g1 = g;
         g1.n_local = n1;
         k_ls_c256ws<<<grid, c4w::NT, c4w::DYN_BYTES, s>>>(g1, eta, probe_s, pos, order, u, v, d, c, part, st, pf);

@@ -105,26 +105,39 @@ def test_warm_start_trajectory_conditioned(L, name):
     pt.close()
 
 
-@pytest.mark.parametrize("name", ["n128m", "n256m"])
-def test_pass0_trial_count_does_not_change_the_iteration(L, name, monkeypatch):
+SCHEDULES = {
+    # margin of the adaptive pass-0 trial count: keff = k*_prev + PTYGER_KEFF_ADD
+    "keff": [{"PTYGER_KEFF_ADD": "0"}, {"PTYGER_KEFF_ADD": "3"}, {"PTYGER_KEFF_ADD": "12"}],
+    # N = 256: share of the frames on the side kernel (k_ls256_side) next to the four-CTA clusters
+    "side": [{"PTYGER_C256_SIDE": "0"}, {"PTYGER_C256_SIDE": "110"}, {"PTYGER_C256_SIDE": "300"}],
+}
+
+
+@pytest.mark.parametrize("name,sched", [("n128m", "keff"), ("n256m", "keff"), ("n256m", "side")])
+def test_schedule_does_not_change_the_iteration(L, name, sched, monkeypatch):
     """Eq.7 accepts the FIRST trial gamma_0 tau^k that satisfies the Armijo test; how many trials
-    one pass over the far fields evaluates (keff = k*_prev + PTYGER_KEFF_ADD, then the extra passes) is a
-    scheduling choice that must not change the iteration.  From the flat start psi_0 = 1 (k* jumps, extra
-    passes) and in the production kernels with more frames than CTAs / clusters: identical shrinks and
-    restarts, F and the object equal to float rounding (every trial sum S_k is accumulated in the same
-    order whatever the pass holds; only the screening bound, hence an exact re-evaluation, may differ)."""
+    one pass over the far fields evaluates (keff = k*_prev + PTYGER_KEFF_ADD, then the extra passes) and which
+    kernel transforms which frame (N = 256: the side kernel's share) are scheduling choices that must not
+    change the iteration.  From the flat start psi_0 = 1 (k* jumps, extra passes) and in the production
+    kernels with more frames than CTAs / clusters: identical shrinks and restarts, F and the object equal to
+    float rounding (the trial sums S_k are accumulated in the same per-pixel order whatever the pass holds;
+    the frame -> CTA assignment changes only the order of the fp32 partial sums)."""
     psi_true, p, scan, d = get_fixture(name)
     runs = []
-    for kadd in (0, 3, 12):
-        monkeypatch.setenv("PTYGER_KEFF_ADD", str(kadd))
+    for env in SCHEDULES[sched]:
+        for k, val in env.items():
+            monkeypatch.setenv(k, val)
         pt = L.Ptyger(np.ones_like(psi_true), p, scan, d)
         tr = pt.iterate(8)
         runs.append(([t["shrinks"] for t in tr], [t["restarted"] for t in tr], np.array([t["F"] for t in tr]),
-                     [t["ls_passes"] for t in tr], pt.get_object()))
+                     [t["ls_passes"] for t in tr], pt.get_object(), pt.kernel_launches()))
         pt.close()
-    print(f"{name}: shrinks {runs[0][0]}, LS passes per kadd {[r[3] for r in runs]}")
+    print(f"{name} {sched}: shrinks {runs[0][0]}, LS passes {[r[3] for r in runs]}, launches {[r[5] for r in runs]}")
     for r in runs[1:]:
         assert r[0] == runs[0][0] and r[1] == runs[0][1]
         assert rel(r[2], runs[0][2]) <= 1e-9
         assert rel(r[4], runs[0][4]) <= 1e-6
-    assert [r[3] for r in runs][0] != [r[3] for r in runs][2]   # the schedules really differed
+    if sched == "keff":
+        assert runs[0][3] != runs[2][3]   # the pass schedules really differed
+    else:
+        assert runs[0][5] < runs[1][5]    # the side kernel really ran (one more launch per iteration)
