@@ -562,9 +562,49 @@ __device__ __forceinline__ void trial_dispatch(int cnt, const SolverCfg& c, F&& 
         trial_dispatch_k<false, false>(cnt, body);
 }
 
+// ls_run_out over the first KR entries only (KR >= the pass's trial count; the others are 0): an 8-entry
+// reduce-scatter costs half the shuffles of the 16-entry one when a pass holds <= 8 trials (the usual
+// pass 0); lane l then holds the warp total of entry l >> 2.
+template <int KR, int K>
+__device__ __forceinline__ void ls_run_out_r(float (&S)[K], const LsMom& m, double& tot, double (&mom)[4], int lane) {
+    static_assert(KR <= K, "reduce width above the array");
+    tot += warp_reduce_scatter_f<KR>(slice<0, KR>(S), lane);
+    mom[0] += (double)m.A;
+    mom[1] += (double)m.D;
+    mom[2] += 2.0 * (double)m.sa2;
+    mom[3] += (double)m.sb;
+}
+
 // Block-level output of the screening partials: per-lane fp64 running total `tot` of entry
 // lane >> (5 - log2 K) of S (after warp_reduce_scatter<K>), per-thread fp64 moments.  Writes
 // [S_0..S_{K-1} | A, D, sum|a|, sum b] for this CTA.  sred: [NW][K], smom: [NW][4].
+// ... from per-lane totals of a KR-entry reduce-scatter, written in the KC-entry row layout (entries
+// [KR, KC) zero) that k_reduce reads.
+template <int KR, int NW>
+__device__ __forceinline__ void ls_block_out_r(double tot, const double (&mom)[4], double (*sred)[KC],
+                                               double (*smom)[4], double* __restrict__ part) {
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    constexpr int P = Log2<KR>::value;
+    constexpr int G = 32 >> P;
+    if ((lane & (G - 1)) == 0) sred[warp][lane >> (5 - P)] = tot;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const double w = warp_sum(mom[i]);
+        if (lane == 0) smom[warp][i] = w;
+    }
+    __syncthreads();
+    if (tid < KC) {
+        double s = 0.0;
+        if (tid < KR)
+            for (int w = 0; w < NW; ++w) s += sred[w][tid];
+        part[(int64_t)blockIdx.x * (KC + 4) + tid] = s;
+    } else if (tid < KC + 4) {
+        double s = 0.0;
+        for (int w = 0; w < NW; ++w) s += smom[w][tid - KC];
+        part[(int64_t)blockIdx.x * (KC + 4) + tid] = s;
+    }
+}
+
 template <int K, int NW>
 __device__ __forceinline__ void ls_block_out(double tot, const double (&mom)[4], double (*sred)[K],
                                              double (*smom)[4], double* __restrict__ part) {

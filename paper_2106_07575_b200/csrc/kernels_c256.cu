@@ -530,7 +530,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(512, 1)
                                              S, m, lane);
                     }
                     ls_flush<KT, LSE, QG>(wq[ew], qs, gk, eps2, S, m, lane);
-                    ls_run_out<KC>(S, m, tot, mom, lane);
+                    ls_run_out_r<(KT <= 8 ? 8 : KC)>(S, m, tot, mom, lane);
                 }
                 // slot b read: the FFT group may overwrite it (frame it + 2) -- no arrival without a waiter
                 c4_tc_before();
@@ -546,7 +546,10 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(512, 1)
     c4_wait();
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(TMEM_COLS));
     ktime_end(st, 1);
-    ls_block_out<KC, 16>(tot, mom, sred, smom, part);
+    if (cnt <= 8)   // = KT <= 8 (trial_dispatch_k)
+        ls_block_out_r<8, 16>(tot, mom, sred, smom, part);
+    else
+        ls_block_out_r<KC, 16>(tot, mom, sred, smom, part);
 }
 
 // ----------------------------------------------------------------------------------------

@@ -335,7 +335,7 @@ __global__ void __launch_bounds__(512, 1) k_ls_ws(Geometry g, const float2* __re
                                          m, lane);
                     }
                     ls_flush<KT, LSE, QG>(wq[ew], qs, gk, eps2, S, m, lane);
-                    ls_run_out<KC>(S, m, tot, mom, lane);
+                    ls_run_out_r<(KT <= 8 ? 8 : KC)>(S, m, tot, mom, lane);
                 }
                 // slot b read: the FFT group may overwrite it (frame it + 2) -- no arrival without a waiter
                 tc_fence_before();
@@ -348,7 +348,10 @@ __global__ void __launch_bounds__(512, 1) k_ls_ws(Geometry g, const float2* __re
     tc_fence_after();
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(TMEM_COLS));
     ktime_end(st, 1);
-    ls_block_out<KC, 16>(tot, mom, sred, smom, part);
+    if (cnt <= 8)   // = KT <= 8 (trial_dispatch_k)
+        ls_block_out_r<8, 16>(tot, mom, sred, smom, part);
+    else
+        ls_block_out_r<KC, 16>(tot, mom, sred, smom, part);
 }
 
 int launch_ls_ws(const Geometry& g, const float2* eta, const float2* probe_s, const int2* pos, const int* order,

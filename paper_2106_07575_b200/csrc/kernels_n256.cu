@@ -237,13 +237,16 @@ __global__ void __launch_bounds__(512, 1)
                                          m, lane);
                 }
                 ls_flush<KT, LSE, QG>(wq[warp], qs, gk, eps2, S, m, lane);
-                ls_run_out<KC>(S, m, tot, mom, lane);
+                ls_run_out_r<(KT <= 8 ? 8 : KC)>(S, m, tot, mom, lane);
             }
             __syncthreads();   // buf free before the next frame's row exchanges
         }
     });
     ktime_end(st, 1);
-    ls_block_out<KC, 16>(tot, mom, sred, smom, part);
+    if (cnt <= 8)   // = KT <= 8 (trial_dispatch_k)
+        ls_block_out_r<8, 16>(tot, mom, sred, smom, part);
+    else
+        ls_block_out_r<KC, 16>(tot, mom, sred, smom, part);
     // the kernels after this one in the stream must see the cluster kernel's partials as well
     asm volatile("griddepcontrol.wait;" ::: "memory");
 }
